@@ -1,0 +1,134 @@
+/*
+ * alsub.h -- C ABI of the B200-native AlSub uniform-refinement library (arXiv 1809.06047).
+ *
+ * One uniform refinement level of a polygon mesh (Catmull-Clark primary; Loop and sqrt3
+ * variants), split as in the paper into a topology "build" step and a vertex-data "eval" step
+ * (Fig. module_core), repeated `levels` times:
+ *   - build: the mesh matrix M, its adjacency E = M M^T{Q_c+Q_c^{c-1}}[lambda]
+ *     and F = M M^T{Q_c}[gamma] with edge ids from the upper triangle of E, the refined
+ *     M_{i+1}, and the inherited crease matrix C_{i+1};
+ *   - eval: face points f = M^T P, edge points, vertex points
+ *     S = s1 + s2 + s3, boundary repair and crease overrides
+ *     (P:L410-457), Loop and sqrt3 variants.
+ *
+ * Conventions (binding):
+ *   - Child vertex numbering: CC [old V | face points F | edge points E]; Loop [old | edges];
+ *     sqrt3 [old | faces].
+ *   - Edge id = rank of the undirected edge (max, min) in ascending lexicographic order
+ *     (upper triangle of E enumerated column-major, P:L312 + P:L574).
+ *   - CC child face off_r + t = (v_t, ep(v_t,v_t+1), fp_r, ep(v_t-1,v_t)); Loop child faces
+ *     4r+t; sqrt3 child face 3i+t = (v_t, fp_F(v_t+1,v_t), fp_i).
+ *   - Boundary edges are infinitely sharp creases; vertex rules smooth / crease / corner with
+ *     semi-sharp blending; Chaikin-style sharpness inheritance (readings R6-R9).
+ *   - Positions are fp32 [V][3]; sharpness fp32 (+inf allowed).
+ *
+ * Pointers: every array argument may be a HOST or a DEVICE pointer (the library asks the CUDA
+ * driver which); host inputs are copied on `stream`, host outputs are written by a copy on
+ * `stream` followed by a stream synchronisation.  `stream` is a cudaStream_t (NULL = legacy).
+ * Errors: every call returns an alsub_status; alsub_last_error() gives a thread-local message.
+ * Concurrency: one handle must not be used from two threads at once; handles are independent.
+ */
+#ifndef ALSUB_H
+#define ALSUB_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct alsub_mesh alsub_mesh; /* opaque; owns every internal device table */
+
+typedef enum { ALSUB_CATMULL_CLARK = 0, ALSUB_LOOP = 1, ALSUB_SQRT3 = 2 } alsub_scheme;
+
+typedef enum {
+    ALSUB_OK = 0,
+    ALSUB_E_ARG = 1,         /* null pointer, negative count, unknown scheme, bad level            */
+    ALSUB_E_MESH = 2,        /* face order < 3, repeated vertex in a face, vertex id outside [0,V) */
+    ALSUB_E_NONMANIFOLD = 3, /* edge in > 2 faces, directed edge twice (orientation), or a vertex
+                                whose interior faces form more than one closed fan                */
+    ALSUB_E_SCHEME = 4,      /* Loop/sqrt3 on non-triangles; sqrt3 with boundary or creases        */
+    ALSUB_E_CREASE = 5,      /* crease pair not an edge, duplicate pair, sigma < 0 or NaN          */
+    ALSUB_E_OVERFLOW = 6,    /* a refined count or slot offset would exceed INT32_MAX              */
+    ALSUB_E_NOMEM = 7,       /* device allocation failed                                           */
+    ALSUB_E_CUDA = 8         /* any other CUDA runtime error                                       */
+} alsub_status;
+
+/* Optional device allocator (e.g. the PyTorch caching allocator).  NULL -> cudaMallocAsync. */
+typedef struct {
+    void *(*alloc)(size_t bytes, void *stream, void *ctx);
+    void (*free)(void *ptr, size_t bytes, void *stream, void *ctx);
+    void *ctx;
+} alsub_allocator;
+
+typedef struct {
+    int64_t verts, faces, edges, boundary_edges, face_slots;
+    int64_t creases_upper_bound; /* capacity of the crease list at this level (exact count is on
+                                    the device: see alsub_level_topology)                         */
+    int32_t face_order;          /* 3 or 4 when uniform, 0 = mixed                                */
+    int32_t edges_valid;         /* 1 if `edges` is known for this level (sqrt3 levels >= 1: 0)  */
+} alsub_counts;
+
+/* Build a handle from a control mesh (P:L224-226 mesh matrix in CSC form).
+ *   face_off     [num_faces+1] int32  exclusive offsets into face_vtx, face_off[0] = 0
+ *   face_vtx     [face_off[F]] int32  vertex ids in cyclic CCW order per face
+ *   pos          [num_verts][3] fp32
+ *   crease_pairs [num_creases][2] int32 vertex pairs (nullable if num_creases == 0)
+ *   crease_sigma [num_creases] fp32, >= 0, +inf allowed; 0 entries are ignored
+ *   alloc        nullable
+ * Copies every input (they may be freed on return), runs the level-0 build once on `stream`
+ * to validate the mesh and count its edges, and synchronises `stream` once.
+ * Errors: E_ARG, E_MESH, E_NONMANIFOLD, E_CREASE, E_OVERFLOW, E_NOMEM, E_CUDA (no handle). */
+alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t *face_vtx, int32_t num_faces,
+                               const float *pos, int32_t num_verts,
+                               const int32_t *crease_pairs, const float *crease_sigma, int32_t num_creases,
+                               const alsub_allocator *alloc, void *stream, alsub_mesh **out);
+
+/* Replace the level-0 positions (host or device [V][3] fp32). Stream-ordered. */
+alsub_status alsub_set_positions(alsub_mesh *mesh, const float *pos, void *stream);
+
+/* Dynamic mode: rebuild everything from the level-0 mesh matrix (a1-a3 of
+ * SURVEY.md 8(a)) and run `levels` build+eval iterations of `scheme`.  Fully asynchronous on
+ * `stream` (no host synchronisation); the first call per (scheme, levels) allocates the level
+ * tables and records a CUDA graph that later calls replay (env ALSUB_NO_GRAPH=1 disables).
+ * levels = 0 returns the input.  Errors: E_ARG, E_SCHEME, E_OVERFLOW, E_NOMEM, E_CUDA. */
+alsub_status alsub_refine(alsub_mesh *mesh, alsub_scheme scheme, int32_t levels, void *stream);
+
+/* Host-only: counts of level `level` of the last refine (level 0 always available). */
+alsub_status alsub_level_counts(const alsub_mesh *mesh, int32_t level, alsub_counts *out);
+
+/* Export the topology of level `level` (0 .. last refine's levels).  Every output is nullable.
+ *   face_vtx     [face_slots]       face_off [faces+1]
+ *   edge_vtx     [edges][2] (lo,hi) in edge-id order      (levels < last, or CC/Loop last)
+ *   edge_face    [edges][2] face of lo->hi, face of hi->lo, -1 = none
+ *   crease_pairs [creases_upper_bound][2] (lo,hi) ascending edge id; crease_sigma [...]
+ *   num_creases  [1] int32: the exact number written (boundary edges are not listed)
+ * Errors: E_ARG (level out of range, edges requested where not available). */
+alsub_status alsub_level_topology(const alsub_mesh *mesh, int32_t level, int32_t *face_vtx, int32_t *face_off,
+                                  int32_t *edge_vtx, int32_t *edge_face, int32_t *crease_pairs,
+                                  float *crease_sigma, int32_t *num_creases, void *stream);
+
+/* Export the positions of level `level` ([verts][3] fp32). */
+alsub_status alsub_level_positions(const alsub_mesh *mesh, int32_t level, float *pos, void *stream);
+
+/* Static mode (Fig. CC_singleSpMV top): evaluate `num_frames` frames of level-0
+ * vertex data through the topology of the last alsub_refine (same scheme, `levels` <= its
+ * levels) -- only the eval half of every module runs.
+ *   frames_in  [num_frames][V0][3] fp32,  frames_out [num_frames][V_levels][3] fp32
+ * Frames are processed in batches that share each topology read.  Stream-ordered.
+ * Errors: E_ARG (no prior refine / levels too large), E_NOMEM, E_CUDA. */
+alsub_status alsub_eval_frames(alsub_mesh *mesh, int32_t levels, const float *frames_in, int32_t num_frames,
+                               float *frames_out, void *stream);
+
+/* Number of kernel launches issued by the last alsub_refine / alsub_eval_frames call
+ * (a graph replay counts the kernels inside it). */
+int64_t alsub_last_launch_count(const alsub_mesh *mesh);
+
+void alsub_mesh_destroy(alsub_mesh *mesh);
+const char *alsub_last_error(void);
+const char *alsub_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ALSUB_H */

@@ -1,0 +1,249 @@
+"""Thin ctypes binding of the C ABI in include/alsub.h (argument marshalling only).
+
+Every step of the refinement runs in libalsub.so's sm_100a kernels; PyTorch provides device
+memory (its caching allocator is wired in as the library's allocator), streams and tensors.
+There is no CPU fallback: importing this module on a machine without the built library, or
+calling it without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libalsub.so")
+
+CATMULL_CLARK, LOOP, SQRT3 = 0, 1, 2
+SCHEMES = {"cc": CATMULL_CLARK, "catmull-clark": CATMULL_CLARK, "loop": LOOP, "sqrt3": SQRT3}
+STATUS = {0: "OK", 1: "E_ARG", 2: "E_MESH", 3: "E_NONMANIFOLD", 4: "E_SCHEME", 5: "E_CREASE",
+          6: "E_OVERFLOW", 7: "E_NOMEM", 8: "E_CUDA"}
+
+
+class AlsubError(RuntimeError):
+    def __init__(self, status, msg):
+        self.status = STATUS.get(status, str(status))
+        super().__init__(f"{self.status}: {msg}")
+
+
+class _Counts(C.Structure):
+    _fields_ = [("verts", C.c_int64), ("faces", C.c_int64), ("edges", C.c_int64), ("boundary_edges", C.c_int64),
+                ("face_slots", C.c_int64), ("creases_upper_bound", C.c_int64), ("face_order", C.c_int32),
+                ("edges_valid", C.c_int32)]
+
+
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
+class _Allocator(C.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("ctx", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libalsub.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    L.alsub_mesh_create.argtypes = [vp, vp, i32, vp, i32, vp, vp, i32, C.POINTER(_Allocator), vp, C.POINTER(vp)]
+    L.alsub_set_positions.argtypes = [vp, vp, vp]
+    L.alsub_refine.argtypes = [vp, C.c_int, i32, vp]
+    L.alsub_level_counts.argtypes = [vp, i32, C.POINTER(_Counts)]
+    L.alsub_level_topology.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.alsub_level_positions.argtypes = [vp, i32, vp, vp]
+    L.alsub_eval_frames.argtypes = [vp, i32, vp, i32, vp, vp]
+    L.alsub_last_launch_count.argtypes = [vp]
+    L.alsub_last_launch_count.restype = i64
+    L.alsub_mesh_destroy.argtypes = [vp]
+    L.alsub_mesh_destroy.restype = None
+    L.alsub_last_error.restype = C.c_char_p
+    L.alsub_version.restype = C.c_char_p
+    for f in ("alsub_mesh_create", "alsub_set_positions", "alsub_refine", "alsub_level_counts",
+              "alsub_level_topology", "alsub_level_positions", "alsub_eval_frames"):
+        getattr(L, f).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _check(st):
+    if st != 0:
+        raise AlsubError(st, lib().alsub_last_error().decode(errors="replace"))
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    raise TypeError(type(t))
+
+
+def _as(t, dtype):
+    """Contiguous tensor/array of the given dtype, keeping device tensors on the device."""
+    if isinstance(t, torch.Tensor):
+        return t.to(dtype).contiguous()
+    npdt = {torch.int32: np.int32, torch.float32: np.float32}[dtype]
+    return np.ascontiguousarray(np.asarray(t), dtype=npdt)
+
+
+def _stream(stream):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+class _TorchAllocator:
+    """The PyTorch caching allocator as the library's device allocator."""
+
+    def __init__(self, device):
+        self.device = device
+
+        def _a(nbytes, stream, ctx):
+            try:
+                return torch.cuda.caching_allocator_alloc(int(nbytes), self.device, int(stream or 0))
+            except Exception:
+                return None
+
+        def _f(ptr, nbytes, stream, ctx):
+            torch.cuda.caching_allocator_delete(int(ptr))
+
+        self._a, self._f = _ALLOC_FN(_a), _FREE_FN(_f)
+        self.struct = _Allocator(self._a, self._f, None)
+
+
+class Mesh:
+    """A control mesh on the GPU: ``alsub_mesh_create`` (P:L224-226 mesh matrix).
+
+    face_off int32[F+1], face_vtx int32[S], pos float32[V,3], crease int32[K,2], sigma float32[K]
+    -- torch tensors (CUDA or CPU) or numpy arrays (host)."""
+
+    def __init__(self, face_off, face_vtx, pos, crease=None, sigma=None, stream=None, torch_allocator=True):
+        if not torch.cuda.is_available():
+            raise RuntimeError("alsub needs a CUDA device (there is no CPU path)")
+        self._lib = lib()
+        self.device = torch.cuda.current_device()
+        self._keep = []
+        fo, fv, P = _as(face_off, torch.int32), _as(face_vtx, torch.int32), _as(pos, torch.float32)
+        if crease is None or len(crease) == 0:
+            cr, sg, K = None, None, 0
+        else:
+            cr, sg = _as(crease, torch.int32), _as(sigma, torch.float32)
+            K = int(cr.shape[0])
+        self._keep += [fo, fv, P, cr, sg]
+        V = int(P.shape[0]) if P.ndim == 2 else int(P.size // 3)
+        F = int(fo.shape[0]) - 1
+        self._alloc = _TorchAllocator(self.device) if torch_allocator else None
+        h = C.c_void_p()
+        st = self._lib.alsub_mesh_create(_ptr(fo), _ptr(fv), F, _ptr(P), V, _ptr(cr), _ptr(sg), K,
+                                         C.byref(self._alloc.struct) if self._alloc else None,
+                                         _stream(stream), C.byref(h))
+        self._keep = []
+        _check(st)
+        self._h = h
+        self.scheme = None
+        self.levels = None
+
+    # -- lifetime --
+    def close(self):
+        if getattr(self, "_h", None):
+            torch.cuda.synchronize()
+            self._lib.alsub_mesh_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- ABI calls --
+    def set_positions(self, pos, stream=None):
+        P = _as(pos, torch.float32)
+        _check(self._lib.alsub_set_positions(self._h, _ptr(P), _stream(stream)))
+        if isinstance(P, torch.Tensor) and P.is_cuda:
+            self._pos_keep = P  # keep alive until the stream consumes it
+
+    def refine(self, scheme, levels, stream=None):
+        sc = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
+        _check(self._lib.alsub_refine(self._h, sc, int(levels), _stream(stream)))
+        self.scheme, self.levels = sc, int(levels)
+        return self
+
+    def counts(self, level):
+        c = _Counts()
+        _check(self._lib.alsub_level_counts(self._h, int(level), C.byref(c)))
+        return {k: getattr(c, k) for k, _ in _Counts._fields_}
+
+    def positions(self, level, out=None, stream=None):
+        V = self.counts(level)["verts"]
+        if out is None:
+            out = torch.empty((V, 3), dtype=torch.float32, device="cuda")
+        _check(self._lib.alsub_level_positions(self._h, int(level), _ptr(out), _stream(stream)))
+        return out
+
+    def topology(self, level, faces=True, edges=False, creases=False, stream=None):
+        c = self.counts(level)
+        out = {}
+        dev = "cuda"
+        fv = torch.empty(c["face_slots"], dtype=torch.int32, device=dev) if faces else None
+        fo = torch.empty(c["faces"] + 1, dtype=torch.int32, device=dev) if faces else None
+        ev = torch.empty((c["edges"], 2), dtype=torch.int32, device=dev) if edges else None
+        ef = torch.empty((c["edges"], 2), dtype=torch.int32, device=dev) if edges else None
+        K = max(int(c["creases_upper_bound"]), 1)
+        cp = torch.empty((K, 2), dtype=torch.int32, device=dev) if creases else None
+        cs = torch.empty(K, dtype=torch.float32, device=dev) if creases else None
+        nk = np.zeros(1, dtype=np.int32) if creases else None
+        _check(self._lib.alsub_level_topology(self._h, int(level), _ptr(fv), _ptr(fo), _ptr(ev), _ptr(ef), _ptr(cp),
+                                              _ptr(cs), _ptr(nk), _stream(stream)))
+        if faces:
+            out["face_vtx"], out["face_off"] = fv, fo
+        if edges:
+            out["edge_vtx"], out["edge_face"] = ev, ef
+        if creases:
+            k = int(nk[0])
+            out["crease"], out["sigma"] = cp[:k], cs[:k]
+        return out
+
+    def eval_frames(self, frames, levels, out=None, stream=None):
+        """Static mode: frames [B, V0, 3] -> [B, V_levels, 3] through the stored topology."""
+        fr = _as(frames, torch.float32)
+        B = int(fr.shape[0])
+        VL = self.counts(levels)["verts"]
+        if out is None:
+            out = torch.empty((B, VL, 3), dtype=torch.float32, device="cuda")
+        _check(self._lib.alsub_eval_frames(self._h, int(levels), _ptr(fr), B, _ptr(out), _stream(stream)))
+        return out
+
+    @property
+    def last_launch_count(self):
+        return int(self._lib.alsub_last_launch_count(self._h))
+
+
+def version():
+    return lib().alsub_version().decode()
+
+
+def exported_symbols():
+    """Names declared in include/alsub.h (checked against the library by the CPU tests)."""
+    import re
+    hdr = open(os.path.join(os.path.dirname(_HERE), "include", "alsub.h")).read()
+    return sorted(set(re.findall(r"\b(alsub_[a-z_]+)\s*\(", hdr)))

@@ -1,0 +1,707 @@
+// api.cu -- the C ABI (include/alsub.h): handle lifetime, level plans, the level loop and its
+// CUDA-graph capture, static-mode frame evaluation and topology/position export.
+//
+// The host side only computes closed-form level counts and launches
+// kernels; every step of the refinement runs on the device.  One device->host read happens per
+// handle (at create: E_0, validation flags and special-list sizes); alsub_refine is fully
+// asynchronous and replayable as a CUDA graph.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/alsub.h"
+#include "internal.h"
+
+namespace alsub {
+void init_scheme_tables(cudaStream_t s);
+}
+
+using namespace alsub;
+
+static thread_local std::string g_err;
+
+static alsub_status fail(alsub_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+
+#define CU(call)                                                                                          \
+    do {                                                                                                  \
+        cudaError_t _e = (call);                                                                          \
+        if (_e != cudaSuccess) return fail(ALSUB_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+static bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct LevelHost {
+    int64_t V = 0, F = 0, S = 0, E = 0, B = 0;
+    int order = 4;
+    bool edges_valid = true;
+    int32_t *face_off = nullptr, *slot_face = nullptr, *face_vtx = nullptr, *face_edge = nullptr,
+            *face_twin = nullptr, *edge_slot = nullptr, *vtx_slot0 = nullptr;
+    uint32_t *bnd_word = nullptr;
+    int32_t *bnd_wcnt = nullptr, *bnd_wpre = nullptr;
+    int32_t *loop_cnt = nullptr, *loop_base = nullptr;
+    SpEdge *sp = nullptr;
+    int32_t sp_cap = 0;
+    int32_t *sp_count = nullptr;
+    int32_t sv_cap = 0;
+    int32_t *sv_count = nullptr;
+    SvAcc *sva = nullptr;
+    int32_t *inh_cnt = nullptr, *inh_off = nullptr;
+    float *pos = nullptr;
+};
+
+struct alsub_mesh {
+    alsub_allocator alloc{};
+    bool custom = false;
+    int device = 0;
+    std::vector<std::pair<void *, size_t>> mem_create, mem_plan, mem_frames;
+    // level-0 inputs
+    int32_t V0 = 0, F0 = 0, S0 = 0, Kin = 0, order0 = 0;
+    int32_t *in_face_off = nullptr, *in_face_vtx = nullptr, *in_crease = nullptr;
+    float *in_sigma = nullptr, *pos0 = nullptr;
+    Build0 b0{};
+    int32_t E0 = 0, B0 = 0, K0 = 0, NSV0 = 0;
+    bool user_creases = false;
+    int32_t *d_counts = nullptr;  // per level: [2l] sp_count, [2l+1] sv_count
+    int32_t *sv_vtx = nullptr;
+    void *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    void *scratch_create = nullptr;
+    size_t scratch_create_bytes = 0;
+    // plan
+    int scheme = -1, levels = -1;
+    std::vector<LevelHost> lv;
+    cudaGraphExec_t gexec = nullptr;
+    int64_t graph_launches = 0;
+    cudaStream_t cap_stream = nullptr;
+    int64_t last_launches = 0;
+    // frames
+    int frames_nb = 0;
+    std::vector<float *> frame_buf;
+};
+
+// ---------------- memory ----------------
+static void *dev_alloc(alsub_mesh *m, size_t bytes, cudaStream_t s, std::vector<std::pair<void *, size_t>> &list) {
+    if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~(size_t)255;
+    void *p = nullptr;
+    if (m->custom) {
+        p = m->alloc.alloc(bytes, (void *)s, m->alloc.ctx);
+    } else {
+        if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+    }
+    if (p) list.emplace_back(p, bytes);
+    return p;
+}
+
+static void free_list(alsub_mesh *m, std::vector<std::pair<void *, size_t>> &list, cudaStream_t s) {
+    for (auto &pr : list) {
+        if (m->custom) m->alloc.free(pr.first, pr.second, (void *)s, m->alloc.ctx);
+        else cudaFreeAsync(pr.first, s);
+    }
+    list.clear();
+}
+
+template <class T>
+static T *A(alsub_mesh *m, int64_t n, cudaStream_t s, std::vector<std::pair<void *, size_t>> &list, bool &ok) {
+    T *p = (T *)dev_alloc(m, sizeof(T) * (size_t)(n > 0 ? n : 1), s, list);
+    if (!p) ok = false;
+    return p;
+}
+
+// ---------------- device views ----------------
+static LevelDev dev_of(const LevelHost &L) {
+    LevelDev p{};
+    p.V = (int32_t)L.V; p.F = (int32_t)L.F; p.S = (int32_t)L.S; p.E = (int32_t)L.E; p.B = (int32_t)L.B;
+    p.order = L.order;
+    p.face_off = L.face_off; p.slot_face = L.slot_face;
+    p.face_vtx = L.face_vtx; p.face_edge = L.face_edge; p.face_twin = L.face_twin; p.edge_slot = L.edge_slot;
+    p.vtx_slot0 = L.vtx_slot0; p.bnd_word = L.bnd_word; p.bnd_wpre = L.bnd_wpre; p.loop_base = L.loop_base;
+    p.sp = L.sp; p.sp_count = L.sp_count; p.sp_cap = L.sp_cap;
+    p.sv_count = L.sv_count; p.sva = L.sva; p.sv_cap = L.sv_cap;
+    return p;
+}
+
+static ChildDev child_of(const LevelHost &L) {
+    ChildDev c{};
+    c.V = (int32_t)L.V; c.F = (int32_t)L.F; c.S = (int32_t)L.S; c.E = (int32_t)L.E;
+    c.face_vtx = L.face_vtx; c.face_edge = L.face_edge; c.face_twin = L.face_twin; c.edge_slot = L.edge_slot;
+    c.vtx_slot0 = L.vtx_slot0; c.bnd_word = L.bnd_word; c.bnd_wcnt = L.bnd_wcnt; c.bnd_wpre = L.bnd_wpre;
+    c.sp = L.sp; c.sp_count = L.sp_count; c.sp_cap = L.sp_cap; c.sv_count = L.sv_count;
+    return c;
+}
+
+static void set_level0_view(alsub_mesh *m, LevelHost &L) {
+    Build0 &b = m->b0;
+    L.V = m->V0; L.F = m->F0; L.S = m->S0; L.E = m->E0; L.B = m->B0;
+    L.order = m->order0;
+    L.face_off = m->in_face_off; L.slot_face = b.slot_face;
+    L.face_vtx = m->in_face_vtx; L.face_edge = b.face_edge; L.face_twin = b.face_twin;
+    L.edge_slot = b.edge_slot; L.vtx_slot0 = b.vtx_slot0;
+    L.bnd_word = b.bnd_word; L.bnd_wcnt = b.bnd_wcnt; L.bnd_wpre = b.bnd_wpre;
+    L.sp = b.sp; L.sp_cap = m->K0; L.sp_count = b.scalars + 2;
+    L.sv_cap = m->NSV0; L.sv_count = b.scalars + 3;
+    L.pos = m->pos0;
+}
+
+// ---------------- create ----------------
+static alsub_status map_flags(int32_t flags) {
+    if (flags & kFlagMesh) return fail(ALSUB_E_MESH, "face order < 3, repeated vertex in a face, or vertex index out of range");
+    if (flags & kFlagNonManifold) return fail(ALSUB_E_NONMANIFOLD, "non-manifold edge, inconsistent orientation or non-manifold vertex");
+    if (flags & kFlagCrease) return fail(ALSUB_E_CREASE, "crease pair is not an edge, is duplicated, or has sigma < 0 / NaN");
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t *face_vtx, int32_t num_faces,
+                                          const float *pos, int32_t num_verts, const int32_t *crease_pairs,
+                                          const float *crease_sigma, int32_t num_creases,
+                                          const alsub_allocator *alloc, void *stream, alsub_mesh **out) {
+    if (!out) return fail(ALSUB_E_ARG, "out is null");
+    *out = nullptr;
+    if (num_faces < 0 || num_verts < 0 || num_creases < 0) return fail(ALSUB_E_ARG, "negative count");
+    if (!face_off || (num_verts > 0 && !pos)) return fail(ALSUB_E_ARG, "null face_off / pos");
+    if (num_creases > 0 && (!crease_pairs || !crease_sigma)) return fail(ALSUB_E_ARG, "null crease arrays");
+    cudaStream_t s = (cudaStream_t)stream;
+    // face offsets on the host: S0, monotonicity, uniform order
+    std::vector<int32_t> off((size_t)num_faces + 1);
+    CU(cudaMemcpy(off.data(), face_off, sizeof(int32_t) * off.size(), cudaMemcpyDefault));
+    if (off[0] != 0) return fail(ALSUB_E_MESH, "face_off[0] != 0");
+    int order = -1;
+    for (int32_t r = 0; r < num_faces; ++r) {
+        int64_t c = (int64_t)off[r + 1] - off[r];
+        if (c < 3) return fail(ALSUB_E_MESH, "face " + std::to_string(r) + " has order < 3");
+        if (order == -1) order = (int)c;
+        else if (order != c) order = 0;
+    }
+    if (order == -1) order = 4;
+    if (order != 3 && order != 4) order = 0;
+    const int32_t S0 = off[num_faces];
+    if (S0 > 0 && !face_vtx) return fail(ALSUB_E_ARG, "null face_vtx");
+
+    alsub_mesh *m = new alsub_mesh();
+    if (alloc && alloc->alloc && alloc->free) { m->alloc = *alloc; m->custom = true; }
+    cudaGetDevice(&m->device);
+    m->V0 = num_verts; m->F0 = num_faces; m->S0 = S0; m->Kin = num_creases; m->order0 = order;
+    auto bail = [&](alsub_status st) {
+        std::string msg = g_err;
+        alsub_mesh_destroy(m);
+        g_err = msg;
+        return st;
+    };
+    bool ok = true;
+    auto &ML = m->mem_create;
+    m->in_face_off = A<int32_t>(m, num_faces + 1, s, ML, ok);
+    m->in_face_vtx = A<int32_t>(m, S0, s, ML, ok);
+    m->pos0 = A<float>(m, 3 * (int64_t)num_verts, s, ML, ok);
+    m->in_crease = A<int32_t>(m, 2 * (int64_t)num_creases, s, ML, ok);
+    m->in_sigma = A<float>(m, num_creases, s, ML, ok);
+    if (!ok) return bail(fail(ALSUB_E_NOMEM, "device allocation failed"));
+    cudaMemcpyAsync(m->in_face_off, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice, s);
+    if (S0 > 0) cudaMemcpyAsync(m->in_face_vtx, face_vtx, sizeof(int32_t) * S0, cudaMemcpyDefault, s);
+    if (num_verts > 0) cudaMemcpyAsync(m->pos0, pos, sizeof(float) * 3 * (size_t)num_verts, cudaMemcpyDefault, s);
+    if (num_creases > 0) {
+        cudaMemcpyAsync(m->in_crease, crease_pairs, sizeof(int32_t) * 2 * (size_t)num_creases, cudaMemcpyDefault, s);
+        cudaMemcpyAsync(m->in_sigma, crease_sigma, sizeof(float) * (size_t)num_creases, cudaMemcpyDefault, s);
+    }
+    Build0 &b = m->b0;
+    b.V = num_verts; b.F = num_faces; b.S = S0; b.K_in = num_creases; b.order = order;
+    b.face_off = m->in_face_off; b.face_vtx = m->in_face_vtx; b.crease_in = m->in_crease; b.sigma_in = m->in_sigma;
+    b.slot_face = A<int32_t>(m, S0, s, ML, ok);
+    b.sort_k = A<int32_t>(m, S0, s, ML, ok);
+    b.sort_v = A<int32_t>(m, S0, s, ML, ok);
+    b.sort_k2 = A<int32_t>(m, S0, s, ML, ok);
+    b.sort_v2 = A<int32_t>(m, S0, s, ML, ok);
+    b.vtx_off = A<int32_t>(m, (int64_t)num_verts + 1, s, ML, ok);
+    b.vtx_slot = A<int32_t>(m, S0, s, ML, ok);
+    b.edge_cnt = A<int32_t>(m, num_verts, s, ML, ok);
+    b.edge_off = A<int32_t>(m, num_verts, s, ML, ok);
+    b.face_edge = A<int32_t>(m, S0, s, ML, ok);
+    b.face_twin = A<int32_t>(m, S0, s, ML, ok);
+    b.vtx_slot0 = A<int32_t>(m, num_verts, s, ML, ok);
+    b.v_mark = A<int32_t>(m, num_verts, s, ML, ok);
+    b.v_idx = A<int32_t>(m, num_verts, s, ML, ok);
+    b.flags = A<int32_t>(m, 8, s, ML, ok);
+    b.scalars = A<int32_t>(m, 8, s, ML, ok);
+    m->scratch_bytes = sort_scratch_bytes(S0);
+    size_t sb = scan_scratch_bytes(std::max<int64_t>(num_verts, S0) + 1);
+    if (sb > m->scratch_bytes) m->scratch_bytes = sb;
+    m->scratch = dev_alloc(m, m->scratch_bytes, s, ML);
+    b.scratch = m->scratch;
+    m->scratch_create = m->scratch;
+    m->scratch_create_bytes = m->scratch_bytes;
+    if (!ok || !m->scratch) return bail(fail(ALSUB_E_NOMEM, "device allocation failed"));
+    cudaMemsetAsync(b.flags, 0, 8 * sizeof(int32_t), s);
+    cudaMemsetAsync(b.scalars, 0, 8 * sizeof(int32_t), s);
+    init_scheme_tables(s);
+    Launches L;
+    // stage 1: face validation
+    build0_validate(b, s, L);
+    int32_t flags = 0;
+    if (cudaMemcpyAsync(&flags, b.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return bail(fail(ALSUB_E_CUDA, std::string("level-0 validation: ") + cudaGetErrorString(cudaGetLastError())));
+    if (flags) return bail(map_flags(flags));
+    // stage 2: M^T + symbolic edge count -> E_0
+    build0_count_edges(b, s, L);
+    int32_t E0 = 0;
+    cudaMemcpyAsync(&E0, b.scalars + 0, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess)
+        return bail(fail(ALSUB_E_CUDA, std::string("level-0 edge count: ") + cudaGetErrorString(cudaGetLastError())));
+    m->E0 = E0;
+    b.E = E0;
+    const int64_t nw = ceil_div(E0 > 0 ? E0 : 1, 32);
+    b.edge_slot = A<int32_t>(m, E0, s, ML, ok);
+    b.bnd_word = A<uint32_t>(m, nw, s, ML, ok);
+    b.bnd_wcnt = A<int32_t>(m, nw, s, ML, ok);
+    b.bnd_wpre = A<int32_t>(m, nw, s, ML, ok);
+    b.edge_sigma = A<float>(m, E0, s, ML, ok);
+    b.edge_cidx = A<int32_t>(m, E0, s, ML, ok);
+    b.sp_flag = A<int32_t>(m, E0, s, ML, ok);
+    b.sp_off = A<int32_t>(m, E0, s, ML, ok);
+    b.sp = A<SpEdge>(m, E0, s, ML, ok);
+    b.sv_vtx = A<int32_t>(m, num_verts, s, ML, ok);
+    if (!ok) return bail(fail(ALSUB_E_NOMEM, "device allocation failed"));
+    build0_fill(b, true, s, L);
+    int32_t sc[8];
+    cudaMemcpyAsync(&flags, b.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(sc, b.scalars, sizeof(sc), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess)
+        return bail(fail(ALSUB_E_CUDA, std::string("level-0 build: ") + cudaGetErrorString(cudaGetLastError())));
+    if (flags) return bail(map_flags(flags));
+    m->B0 = sc[1];
+    m->K0 = sc[2];
+    m->NSV0 = sc[3];
+    m->user_creases = (m->K0 - m->B0) > 0;
+    CU(cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking));
+    m->last_launches = L.n;
+    *out = m;
+    g_err.clear();
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_set_positions(alsub_mesh *m, const float *pos, void *stream) {
+    if (!m || (!pos && m->V0 > 0)) return fail(ALSUB_E_ARG, "null argument");
+    if (m->V0 > 0)
+        CU(cudaMemcpyAsync(m->pos0, pos, sizeof(float) * 3 * (size_t)m->V0, cudaMemcpyDefault, (cudaStream_t)stream));
+    return ALSUB_OK;
+}
+
+// ---------------- plan ----------------
+static void free_plan(alsub_mesh *m, cudaStream_t s) {
+    if (m->gexec) { cudaGraphExecDestroy(m->gexec); m->gexec = nullptr; }
+    free_list(m, m->mem_plan, s);
+    free_list(m, m->mem_frames, s);
+    m->scratch = m->scratch_create;
+    m->scratch_bytes = m->scratch_create_bytes;
+    m->b0.scratch = m->scratch;
+    m->frame_buf.clear();
+    m->frames_nb = 0;
+    m->lv.clear();
+    m->scheme = m->levels = -1;
+}
+
+static alsub_status check_scheme(alsub_mesh *m, int scheme) {
+    if (scheme == ALSUB_LOOP || scheme == ALSUB_SQRT3) {
+        if (m->order0 != 3) return fail(ALSUB_E_SCHEME, "Loop and sqrt3 need a triangle mesh");
+    }
+    if (scheme == ALSUB_SQRT3) {
+        if (m->B0 > 0) return fail(ALSUB_E_SCHEME, "sqrt3 boundary rules are omitted by the paper (P:L1002)");
+        if (m->user_creases) return fail(ALSUB_E_SCHEME, "sqrt3 has no crease rules");
+    }
+    return ALSUB_OK;
+}
+
+static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_t s) {
+    free_plan(m, s);
+    std::vector<LevelHost> lv((size_t)levels + 1);
+    set_level0_view(m, lv[0]);
+    const bool special = scheme != ALSUB_SQRT3 && m->K0 > 0;
+    for (int l = 1; l <= levels; ++l) {
+        const LevelHost &p = lv[l - 1];
+        LevelHost &c = lv[l];
+        if (scheme == ALSUB_CATMULL_CLARK) {
+            c.V = p.V + p.F + p.E; c.F = p.S; c.S = 4 * p.S; c.E = 2 * p.E + p.S; c.B = 2 * p.B; c.order = 4;
+        } else if (scheme == ALSUB_LOOP) {
+            c.V = p.V + p.E; c.F = 4 * p.F; c.S = 12 * p.F; c.E = 2 * p.E + 3 * p.F; c.B = 2 * p.B; c.order = 3;
+        } else {
+            c.V = p.V + p.F; c.F = 3 * p.F; c.S = 9 * p.F; c.E = 3 * p.E; c.B = 0; c.order = 3;
+            c.edges_valid = false;
+        }
+        if (c.V > INT32_MAX || c.S > INT32_MAX || c.E > INT32_MAX || 4 * c.S > INT32_MAX)
+            return fail(ALSUB_E_OVERFLOW, "level " + std::to_string(l) + " exceeds int32 ids");
+        if (special) {
+            c.sp_cap = (int32_t)std::min<int64_t>(2 * (int64_t)p.sp_cap, INT32_MAX / 2);
+            c.sv_cap = p.sv_cap + p.sp_cap;
+        }
+    }
+    bool ok = true;
+    auto &ML = m->mem_plan;
+    const int64_t sv_total = special ? lv[levels].sv_cap : 1;
+    m->sv_vtx = A<int32_t>(m, sv_total, s, ML, ok);
+    m->b0.sv_vtx = m->sv_vtx;
+    m->d_counts = A<int32_t>(m, 2 * ((int64_t)levels + 1), s, ML, ok);
+    int64_t max_scan = std::max<int64_t>(m->V0, m->S0) + 1;
+    for (int l = 0; l <= levels; ++l) {
+        LevelHost &c = lv[l];
+        const bool has_child = l < levels;   // level l is refined
+        const bool adj = l + 1 < levels;     // child needs adjacency
+        if (l >= 1) {
+            c.face_vtx = A<int32_t>(m, c.S, s, ML, ok);
+            c.pos = A<float>(m, 3 * c.V, s, ML, ok);
+            if (has_child) {
+                c.face_twin = A<int32_t>(m, c.S, s, ML, ok);
+                c.vtx_slot0 = A<int32_t>(m, c.V, s, ML, ok);
+                if (scheme != ALSUB_SQRT3) {
+                    c.face_edge = A<int32_t>(m, c.S, s, ML, ok);
+                    c.edge_slot = A<int32_t>(m, c.E, s, ML, ok);
+                }
+                if (scheme == ALSUB_CATMULL_CLARK && c.B > 0) {
+                    const int64_t nw = ceil_div(c.E, 32);
+                    c.bnd_word = A<uint32_t>(m, nw, s, ML, ok);
+                    c.bnd_wcnt = A<int32_t>(m, nw, s, ML, ok);
+                    c.bnd_wpre = A<int32_t>(m, nw, s, ML, ok);
+                    max_scan = std::max<int64_t>(max_scan, nw);
+                }
+            }
+            if (special) {
+                c.sp = A<SpEdge>(m, c.sp_cap, s, ML, ok);
+                c.sp_count = m->d_counts + 2 * l;
+                c.sv_count = m->d_counts + 2 * l + 1;
+            }
+        }
+        if (scheme == ALSUB_LOOP && has_child && (adj || special)) {
+            c.loop_cnt = A<int32_t>(m, c.E, s, ML, ok);
+            c.loop_base = A<int32_t>(m, c.E, s, ML, ok);
+            max_scan = std::max<int64_t>(max_scan, c.E);
+        }
+        if (special && has_child) {
+            c.sva = A<SvAcc>(m, c.sv_cap, s, ML, ok);
+            c.inh_cnt = A<int32_t>(m, c.sp_cap, s, ML, ok);
+            c.inh_off = A<int32_t>(m, c.sp_cap, s, ML, ok);
+            max_scan = std::max<int64_t>(max_scan, c.sp_cap);
+        }
+        (void)adj;
+    }
+    size_t need = std::max(sort_scratch_bytes(m->S0), scan_scratch_bytes(max_scan));
+    if (need > m->scratch_bytes) {
+        void *p = dev_alloc(m, need, s, ML);
+        if (!p) ok = false;
+        m->scratch = p;
+        m->scratch_bytes = need;
+        m->b0.scratch = p;
+    }
+    if (!ok) {
+        free_plan(m, s);
+        return fail(ALSUB_E_NOMEM, "device allocation failed for the level tables");
+    }
+    m->lv = std::move(lv);
+    m->scheme = scheme;
+    m->levels = levels;
+    return ALSUB_OK;
+}
+
+// ---------------- the level loop ----------------
+static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
+    const int scheme = m->scheme, levels = m->levels;
+    // a1-a3: level-0 mesh matrix, M^T by radix sort, edge index, creases
+    build0_count_edges(m->b0, s, L);
+    build0_fill(m->b0, false, s, L);
+    const bool special = scheme != ALSUB_SQRT3 && m->K0 > 0;
+    for (int l = 0; l < levels; ++l) {
+        LevelHost &P = m->lv[l];
+        LevelHost &C = m->lv[l + 1];
+        const bool adj = l + 1 < levels;
+        LevelDev p = dev_of(P);
+        p.sv_vtx = m->sv_vtx;
+        ChildDev c = child_of(C);
+        c.sv_vtx = m->sv_vtx;
+        Frames fr{P.pos, C.pos, 3 * P.V, 3 * C.V, 1};
+        if (scheme == ALSUB_CATMULL_CLARK) {
+            cc_level(p, c, fr, true, adj, m->scratch, s, L);
+            if (special) {
+                crease_eval(p, fr, (int32_t)(P.V + P.F), true, s, L);
+                crease_inherit(p, c, 0, (int32_t)(P.V + P.F), P.inh_cnt, P.inh_off, m->scratch, s, L);
+            }
+        } else if (scheme == ALSUB_LOOP) {
+            if (adj || special) loop_edge_base(p, P.loop_cnt, P.loop_base, m->scratch, s, L);
+            loop_level(p, c, fr, true, adj, m->scratch, s, L);
+            if (special) {
+                crease_eval(p, fr, (int32_t)P.V, true, s, L);
+                crease_inherit(p, c, 1, (int32_t)P.V, P.inh_cnt, P.inh_off, m->scratch, s, L);
+            }
+        } else {
+            sqrt3_level(p, c, fr, true, adj, m->scratch, s, L);
+        }
+    }
+}
+
+static bool graphs_enabled() {
+    const char *e = getenv("ALSUB_NO_GRAPH");
+    return !(e && e[0] == '1');
+}
+
+extern "C" alsub_status alsub_refine(alsub_mesh *m, alsub_scheme scheme, int32_t levels, void *stream) {
+    if (!m) return fail(ALSUB_E_ARG, "null mesh");
+    if (scheme < ALSUB_CATMULL_CLARK || scheme > ALSUB_SQRT3) return fail(ALSUB_E_ARG, "unknown scheme");
+    if (levels < 0 || levels > 16) return fail(ALSUB_E_ARG, "levels must be in [0, 16]");
+    alsub_status st = check_scheme(m, scheme);
+    if (st != ALSUB_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (m->scheme != scheme || m->levels != levels) {
+        st = make_plan(m, scheme, levels, s);
+        if (st != ALSUB_OK) return st;
+    }
+    Launches L;
+    if (graphs_enabled()) {
+        if (!m->gexec) {
+            // the plan's allocations are stream-ordered on `s`: make the capture stream wait for them
+            cudaEvent_t ev;
+            CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            CU(cudaEventRecord(ev, s));
+            CU(cudaStreamWaitEvent(m->cap_stream, ev, 0));
+            CU(cudaStreamSynchronize(m->cap_stream));
+            cudaEventDestroy(ev);
+            cudaGraph_t g;
+            CU(cudaStreamBeginCapture(m->cap_stream, cudaStreamCaptureModeThreadLocal));
+            enqueue_refine(m, m->cap_stream, L);
+            cudaError_t ce = cudaStreamEndCapture(m->cap_stream, &g);
+            if (ce != cudaSuccess) return fail(ALSUB_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+            ce = cudaGraphInstantiate(&m->gexec, g, 0);
+            cudaGraphDestroy(g);
+            if (ce != cudaSuccess) { m->gexec = nullptr; return fail(ALSUB_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce)); }
+            m->graph_launches = L.n;
+        }
+        CU(cudaGraphLaunch(m->gexec, s));
+        m->last_launches = m->graph_launches;
+    } else {
+        enqueue_refine(m, s, L);
+        m->last_launches = L.n;
+    }
+    CU(cudaGetLastError());
+    return ALSUB_OK;
+}
+
+// ---------------- queries / export ----------------
+static const LevelHost *level_of(const alsub_mesh *m, int32_t level) {
+    if (level == 0 && m->lv.empty()) return nullptr;
+    if (level < 0 || level >= (int32_t)m->lv.size()) return nullptr;
+    return &m->lv[level];
+}
+
+extern "C" alsub_status alsub_level_counts(const alsub_mesh *m, int32_t level, alsub_counts *out) {
+    if (!m || !out) return fail(ALSUB_E_ARG, "null argument");
+    memset(out, 0, sizeof(*out));
+    if (level == 0) {
+        out->verts = m->V0; out->faces = m->F0; out->edges = m->E0; out->boundary_edges = m->B0;
+        out->face_slots = m->S0; out->creases_upper_bound = m->K0; out->face_order = m->order0;
+        out->edges_valid = 1;
+        return ALSUB_OK;
+    }
+    const LevelHost *L = level_of(m, level);
+    if (!L) return fail(ALSUB_E_ARG, "level not built (call alsub_refine first)");
+    out->verts = L->V; out->faces = L->F; out->edges = L->E; out->boundary_edges = L->B; out->face_slots = L->S;
+    out->creases_upper_bound = L->sp_cap; out->face_order = L->order;
+    out->edges_valid = (L->edges_valid && level < m->levels) ? 1 : 0;
+    return ALSUB_OK;
+}
+
+__global__ void k_iota_stride(int32_t *o, int64_t n, int32_t c) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) o[i] = (int32_t)(c * i);
+}
+
+// copy `bytes` from device src to dst (host or device)
+static cudaError_t copy_out(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);
+}
+
+extern "C" alsub_status alsub_level_topology(const alsub_mesh *mc, int32_t level, int32_t *face_vtx, int32_t *face_off,
+                                             int32_t *edge_vtx, int32_t *edge_face, int32_t *crease_pairs,
+                                             float *crease_sigma, int32_t *num_creases, void *stream) {
+    alsub_mesh *m = const_cast<alsub_mesh *>(mc);
+    if (!m) return fail(ALSUB_E_ARG, "null mesh");
+    cudaStream_t s = (cudaStream_t)stream;
+    LevelHost l0;
+    const LevelHost *L;
+    if (m->lv.empty()) {
+        if (level != 0) return fail(ALSUB_E_ARG, "level not built (call alsub_refine first)");
+        set_level0_view(m, l0);
+        L = &l0;
+    } else {
+        L = level_of(m, level);
+        if (!L) return fail(ALSUB_E_ARG, "level out of range");
+    }
+    std::vector<std::pair<void *, size_t>> tmp;
+    bool ok = true;
+    Launches Ln;
+    if (face_vtx) CU(copy_out(face_vtx, L->face_vtx, sizeof(int32_t) * (size_t)L->S, s));
+    if (face_off) {
+        if (level == 0) {
+            CU(copy_out(face_off, m->in_face_off, sizeof(int32_t) * ((size_t)L->F + 1), s));
+        } else {
+            int32_t *d = is_device_ptr(face_off) ? face_off : A<int32_t>(m, L->F + 1, s, tmp, ok);
+            if (!ok) return fail(ALSUB_E_NOMEM, "export buffer");
+            k_iota_stride<<<grid_for(L->F + 1), kThreads, 0, s>>>(d, L->F + 1, L->order);
+            if (d != face_off) CU(copy_out(face_off, d, sizeof(int32_t) * ((size_t)L->F + 1), s));
+        }
+    }
+    if (edge_vtx || edge_face) {
+        const bool have = L->edges_valid && (level == 0 || level < m->levels) && L->edge_slot && L->face_twin;
+        if (!have) { free_list(m, tmp, s); return fail(ALSUB_E_ARG, "edge tables are not kept for this level"); }
+        int32_t *dv = edge_vtx && !is_device_ptr(edge_vtx) ? A<int32_t>(m, 2 * L->E, s, tmp, ok) : edge_vtx;
+        int32_t *df = edge_face && !is_device_ptr(edge_face) ? A<int32_t>(m, 2 * L->E, s, tmp, ok) : edge_face;
+        if (!ok) return fail(ALSUB_E_NOMEM, "export buffer");
+        export_edges(dev_of(*L), dv, df, s, Ln);
+        if (dv != edge_vtx) CU(copy_out(edge_vtx, dv, sizeof(int32_t) * 2 * (size_t)L->E, s));
+        if (df != edge_face) CU(copy_out(edge_face, df, sizeof(int32_t) * 2 * (size_t)L->E, s));
+    }
+    if (crease_pairs || crease_sigma || num_creases) {
+        int32_t cnt = 0;
+        std::vector<SpEdge> sp;
+        if (L->sp && L->sp_count) {
+            CU(cudaMemcpyAsync(&cnt, L->sp_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+            sp.resize((size_t)cnt);
+            if (cnt > 0) CU(cudaMemcpyAsync(sp.data(), L->sp, sizeof(SpEdge) * cnt, cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+        }
+        std::vector<int32_t> pairs;
+        std::vector<float> sig;
+        for (const SpEdge &e : sp) {
+            if (e.flags & kSpBoundary) continue;
+            pairs.push_back(e.a);
+            pairs.push_back(e.b);
+            sig.push_back(e.sigma);
+        }
+        int32_t k = (int32_t)sig.size();
+        if (crease_pairs && k) CU(cudaMemcpyAsync(crease_pairs, pairs.data(), sizeof(int32_t) * 2 * k, cudaMemcpyDefault, s));
+        if (crease_sigma && k) CU(cudaMemcpyAsync(crease_sigma, sig.data(), sizeof(float) * k, cudaMemcpyDefault, s));
+        if (num_creases) CU(cudaMemcpyAsync(num_creases, &k, sizeof(int32_t), cudaMemcpyDefault, s));
+        CU(cudaStreamSynchronize(s));
+    }
+    if (!tmp.empty()) {
+        CU(cudaStreamSynchronize(s));
+        free_list(m, tmp, s);
+    }
+    if ((face_vtx && !is_device_ptr(face_vtx)) || (face_off && !is_device_ptr(face_off))) CU(cudaStreamSynchronize(s));
+    CU(cudaGetLastError());
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_level_positions(const alsub_mesh *m, int32_t level, float *pos, void *stream) {
+    if (!m || !pos) return fail(ALSUB_E_ARG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const float *src;
+    int64_t V;
+    if (level == 0) { src = m->pos0; V = m->V0; }
+    else {
+        const LevelHost *L = level_of(m, level);
+        if (!L) return fail(ALSUB_E_ARG, "level out of range");
+        src = L->pos; V = L->V;
+    }
+    CU(cudaMemcpyAsync(pos, src, sizeof(float) * 3 * (size_t)V, cudaMemcpyDefault, s));
+    if (!is_device_ptr(pos)) CU(cudaStreamSynchronize(s));
+    return ALSUB_OK;
+}
+
+// ---------------- static mode: frames ----------------
+extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const float *frames_in, int32_t num_frames,
+                                          float *frames_out, void *stream) {
+    if (!m || num_frames < 0 || (num_frames > 0 && (!frames_in || !frames_out))) return fail(ALSUB_E_ARG, "bad argument");
+    if (m->levels < 0 || levels < 0 || levels > m->levels) return fail(ALSUB_E_ARG, "levels exceed the last alsub_refine");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int scheme = m->scheme;
+    const int64_t V0 = m->V0, VL = m->lv[levels].V;
+    if (num_frames == 0) return ALSUB_OK;
+    if (levels == 0) {
+        CU(cudaMemcpyAsync(frames_out, frames_in, sizeof(float) * 3 * (size_t)V0 * num_frames, cudaMemcpyDefault, s));
+        return ALSUB_OK;
+    }
+    const bool in_dev = is_device_ptr(frames_in), out_dev = is_device_ptr(frames_out);
+    const int nb_max = 8;
+    const int nb = std::min(num_frames, nb_max);
+    // per-level batch buffers: [nb][V_l][3] for l = 0 (if host input) .. levels (if host output)
+    if (m->frames_nb < nb || (int)m->frame_buf.size() != m->levels + 1) {
+        free_list(m, m->mem_frames, s);
+        m->frame_buf.assign((size_t)m->levels + 1, nullptr);
+        bool ok = true;
+        for (int l = 0; l <= m->levels; ++l)
+            m->frame_buf[l] = A<float>(m, 3 * m->lv[l].V * nb, s, m->mem_frames, ok);
+        if (!ok) return fail(ALSUB_E_NOMEM, "frame batch buffers");
+        m->frames_nb = nb;
+    }
+    const bool special = scheme != ALSUB_SQRT3 && m->K0 > 0;
+    Launches L;
+    for (int32_t f0 = 0; f0 < num_frames; f0 += nb) {
+        const int n = std::min(nb, num_frames - f0);
+        const float *Pin = frames_in + 3 * V0 * (int64_t)f0;
+        if (!in_dev) {
+            CU(cudaMemcpyAsync(m->frame_buf[0], Pin, sizeof(float) * 3 * V0 * n, cudaMemcpyHostToDevice, s));
+            Pin = m->frame_buf[0];
+        }
+        float *Pout_final = out_dev ? frames_out + 3 * VL * (int64_t)f0 : m->frame_buf[levels];
+        const float *P = Pin;
+        for (int l = 0; l < levels; ++l) {
+            const LevelHost &Pl = m->lv[l];
+            float *Pn = (l + 1 == levels) ? Pout_final : m->frame_buf[l + 1];
+            LevelDev p = dev_of(Pl);
+            p.sv_vtx = m->sv_vtx;
+            ChildDev c{};
+            Frames fr{P, Pn, 3 * Pl.V, 3 * m->lv[l + 1].V, n};
+            if (scheme == ALSUB_CATMULL_CLARK) {
+                cc_level(p, c, fr, false, false, m->scratch, s, L);
+                if (special) crease_eval(p, fr, (int32_t)(Pl.V + Pl.F), false, s, L);
+            } else if (scheme == ALSUB_LOOP) {
+                loop_level(p, c, fr, false, false, m->scratch, s, L);
+                if (special) crease_eval(p, fr, (int32_t)Pl.V, false, s, L);
+            } else {
+                sqrt3_level(p, c, fr, false, false, m->scratch, s, L);
+            }
+            P = Pn;
+        }
+        if (!out_dev)
+            CU(cudaMemcpyAsync(frames_out + 3 * VL * (int64_t)f0, Pout_final, sizeof(float) * 3 * VL * n,
+                               cudaMemcpyDeviceToHost, s));
+    }
+    if (!out_dev) CU(cudaStreamSynchronize(s));
+    m->last_launches = L.n;
+    CU(cudaGetLastError());
+    return ALSUB_OK;
+}
+
+extern "C" int64_t alsub_last_launch_count(const alsub_mesh *m) { return m ? m->last_launches : 0; }
+
+extern "C" void alsub_mesh_destroy(alsub_mesh *m) {
+    if (!m) return;
+    cudaStream_t s = m->cap_stream ? m->cap_stream : (cudaStream_t)0;
+    cudaDeviceSynchronize();
+    if (m->gexec) cudaGraphExecDestroy(m->gexec);
+    m->gexec = nullptr;
+    free_list(m, m->mem_frames, s);
+    free_list(m, m->mem_plan, s);
+    free_list(m, m->mem_create, s);
+    cudaStreamSynchronize(s);
+    if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
+    delete m;
+}
+
+extern "C" const char *alsub_last_error(void) { return g_err.c_str(); }
+extern "C" const char *alsub_version(void) { return "alsub-b200 0.1 (sm_100a)"; }

@@ -1,0 +1,113 @@
+// common.cuh -- device-side helpers shared by the AlSub sm_100a kernels.
+//
+// Mesh representation on the device:
+//   slot h = one non-zero of the mesh matrix M: vertex face_vtx[h] of face face(h)
+//   at cyclic position h - off(face).  Reduced matrices (all quads / all triangles)
+//   have no column pointer: face(h) = h / c.  Level 0 with mixed orders keeps face_off[F+1]
+//   and a slot_face[S] table.
+//   face_edge[h]  id of the edge v(h) -> v(next(h))       (E's enumeration)
+//   face_twin[h]  slot of the reverse directed edge or -1 (F(j,i) of Eq. F)
+//   edge_slot[e]  smallest slot carrying edge e
+//   vtx_slot0[v]  one slot at vertex v (-1 = isolated); the 1-ring is walked with
+//                 next-around(h) = twin(prev(h))  (the rows of M, i.e. M^T's CSR, on demand)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define ALSUB_HD __host__ __device__ __forceinline__
+#define ALSUB_D __device__ __forceinline__
+
+namespace alsub {
+
+constexpr int kThreads = 256;
+
+// Topology accessors for a face order known at compile time (3, 4) or mixed (0).
+template <int ORDER>
+struct Topo {
+    const int32_t *face_off;   // [F+1]   (ORDER == 0 only)
+    const int32_t *slot_face;  // [S]     (ORDER == 0 only)
+    ALSUB_D int32_t face(int32_t h) const {
+        if constexpr (ORDER == 0) return __ldg(slot_face + h);
+        else return h / ORDER;
+    }
+    ALSUB_D int32_t first(int32_t f) const {
+        if constexpr (ORDER == 0) return __ldg(face_off + f);
+        else return f * ORDER;
+    }
+    ALSUB_D int32_t order(int32_t f) const {
+        if constexpr (ORDER == 0) return __ldg(face_off + f + 1) - __ldg(face_off + f);
+        else return ORDER;
+    }
+    ALSUB_D int32_t next(int32_t h) const {
+        if constexpr (ORDER == 4) return (h & ~3) | ((h + 1) & 3);
+        else if constexpr (ORDER == 3) { int32_t t = h % 3; return t == 2 ? h - 2 : h + 1; }
+        else { int32_t f = face(h); int32_t o = first(f); int32_t c = order(f); return h + 1 == o + c ? o : h + 1; }
+    }
+    ALSUB_D int32_t prev(int32_t h) const {
+        if constexpr (ORDER == 4) return (h & ~3) | ((h + 3) & 3);
+        else if constexpr (ORDER == 3) { int32_t t = h % 3; return t == 0 ? h + 2 : h - 1; }
+        else { int32_t f = face(h); int32_t o = first(f); int32_t c = order(f); return h == o ? o + c - 1 : h - 1; }
+    }
+};
+
+// fp32 [V][3] positions (the API layout).  12-byte gathers; the write side is coalesced
+// across a warp because consecutive threads own consecutive items.
+struct P3 {
+    float x, y, z;
+};
+ALSUB_D P3 ld3(const float *__restrict__ P, int64_t v) {
+    const float *p = P + 3 * v;
+    return P3{__ldg(p), __ldg(p + 1), __ldg(p + 2)};
+}
+// plain (coherent) load: for data written earlier in the same stream by another kernel
+ALSUB_D P3 ld3c(const float *P, int64_t v) {
+    const float *p = P + 3 * v;
+    return P3{p[0], p[1], p[2]};
+}
+ALSUB_D void st3(float *P, int64_t v, P3 a) {
+    float *p = P + 3 * v;
+    p[0] = a.x;
+    p[1] = a.y;
+    p[2] = a.z;
+}
+ALSUB_D P3 operator+(P3 a, P3 b) { return P3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+ALSUB_D P3 operator*(float s, P3 a) { return P3{s * a.x, s * a.y, s * a.z}; }
+ALSUB_D P3 p3zero() { return P3{0.f, 0.f, 0.f}; }
+
+// Boundary-edge prefix: bprefix(e) = number of boundary edges with id < e, from a bitmask and
+// per-word exclusive prefix.
+ALSUB_D int32_t bprefix(const uint32_t *__restrict__ words, const int32_t *__restrict__ wpre, int32_t e) {
+    int32_t w = e >> 5;
+    uint32_t m = __ldg(words + w) & ((1u << (e & 31)) - 1u);
+    return __ldg(wpre + w) + __popc(m);
+}
+
+// Special (boundary or creased) edge of a level: boundary edges are infinitely sharp creases
+// (reading R6).  Sorted by edge id.  ia/ib index the level's special-vertex table.
+struct SpEdge {
+    int32_t e, a, b, ia, ib;   // a < b
+    float sigma;               // > 0, +inf for boundary / infinitely sharp
+    int32_t flags;             // bit 0: boundary
+    int32_t pad;
+};
+constexpr int32_t kSpBoundary = 1;
+
+// Per special vertex accumulators: crease valency k and sharpness s (Eqs. CC_crease_valency /
+// CC_crease_vsharpness, fused as in P:L676-681), the first two sharp neighbours,
+// and the finite-crease sums used by sharpness inheritance (reading R8).
+struct SvAcc {
+    int32_t k;
+    int32_t nfin;
+    float finsum;
+    float sum;
+    int32_t inf;
+    int32_t nb0, nb1;
+    float s;
+};
+
+// Device-side status flags written by the level-0 build (read back by alsub_mesh_create).
+enum : int32_t {
+    kFlagMesh = 1, kFlagNonManifold = 2, kFlagCrease = 4, kFlagOrder = 8,
+};
+
+}  // namespace alsub

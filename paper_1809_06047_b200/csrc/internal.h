@@ -1,0 +1,126 @@
+// internal.h -- host-side declarations shared by the AlSub CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace alsub {
+
+// Counts kernel launches issued into a stream (reported by alsub_last_launch_count).
+struct Launches {
+    int64_t n = 0;
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline unsigned grid_for(int64_t n, int threads = kThreads) {
+    int64_t g = ceil_div(n > 0 ? n : 1, threads);
+    return (unsigned)g;
+}
+
+// ---------------- primitives (prims.cu) ----------------
+// Device-wide exclusive scan of int32 (decoupled look-back, one pass).  `total` (nullable)
+// receives the sum.  `scratch` must hold scan_scratch_bytes(n) bytes.
+size_t scan_scratch_bytes(int64_t n);
+void scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *total, void *scratch,
+                    cudaStream_t s, Launches &L);
+// LSD radix sort of (key, value) int32 pairs, keys in [0, 2^bits).  Stable.  Result in
+// keys/vals; keys_alt/vals_alt are ping-pong buffers of n entries.
+size_t sort_scratch_bytes(int64_t n);
+void radix_sort_pairs(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *vals_alt, int64_t n,
+                      int bits, void *scratch, cudaStream_t s, Launches &L);
+// CSR offsets of sorted keys: off[v] = first i with key[i] >= v, v in [0, nkeys] (run-length).
+void offsets_from_sorted(const int32_t *keys, int64_t n, int32_t *off, int32_t nkeys, cudaStream_t s,
+                         Launches &L);
+
+// ---------------- level-0 build (build0.cu) ----------------
+struct Build0 {
+    // inputs
+    int32_t V, F, S, K_in;
+    int order;  // 0 mixed, 3, 4
+    const int32_t *face_off, *face_vtx, *crease_in;
+    const float *sigma_in;
+    // outputs / work
+    int32_t *slot_face;           // [S] (all orders: used for validation & mixed topology)
+    int32_t *sort_k, *sort_v, *sort_k2, *sort_v2;  // [S]
+    int32_t *vtx_off, *vtx_slot;  // [V+1], [S] (M^T in CSR)
+    int32_t *edge_cnt, *edge_off; // [V], [V]
+    int32_t *face_edge, *face_twin, *edge_slot, *vtx_slot0;  // [S], [S], [E], [V]
+    uint32_t *bnd_word;           // [ceil(E/32)]
+    int32_t *bnd_wcnt, *bnd_wpre; // [ceil(E/32)]
+    float *edge_sigma;            // [E]
+    int32_t *edge_cidx;           // [E] crease index claiming the edge, -1
+    int32_t *sp_flag, *sp_off;    // [E]
+    int32_t *v_mark, *v_idx;      // [V]
+    SpEdge *sp;                   // [cap] special edges
+    int32_t *sv_vtx;              // [cap] special vertices
+    int32_t *flags;               // device status flags
+    int32_t *scalars;             // device scalars: [0] E, [1] B, [2] K special, [3] NSV
+    int32_t E;                    // host-known after the count pass (create) or plan (refine)
+    void *scratch;
+};
+void build0_validate(Build0 &b, cudaStream_t s, Launches &L);
+void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L);  // through edge_off + scalars[0]
+void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L);  // needs b.E
+
+// ---------------- per-level kernels ----------------
+struct LevelDev {
+    int32_t V, F, S, E, B;  // parent counts
+    int order;              // 0, 3, 4
+    const int32_t *face_off, *slot_face;  // order 0
+    const int32_t *face_vtx, *face_edge, *face_twin, *edge_slot, *vtx_slot0;
+    const uint32_t *bnd_word;
+    const int32_t *bnd_wpre;
+    const int32_t *loop_base;  // Loop: [E] exclusive scan of child-edge counts
+    // special lists of the parent level
+    const SpEdge *sp;
+    const int32_t *sp_count;   // device scalar
+    int32_t sp_cap;
+    const int32_t *sv_vtx;     // shared growing table
+    const int32_t *sv_count;   // device scalar (this level)
+    SvAcc *sva;                // [sv_cap] accumulators of this level
+    int32_t sv_cap;
+};
+struct ChildDev {
+    int32_t V, F, S, E;  // child counts
+    int32_t *face_vtx, *face_edge, *face_twin, *edge_slot, *vtx_slot0;
+    uint32_t *bnd_word;
+    int32_t *bnd_wcnt, *bnd_wpre;
+    SpEdge *sp;
+    int32_t *sp_count;
+    int32_t sp_cap;
+    int32_t *sv_vtx;
+    int32_t *sv_count;
+};
+
+// positions: P [nb][V][3] (frame stride Pstride floats), Pn [nb][V'][3]
+struct Frames {
+    const float *P;
+    float *Pn;
+    int64_t Pstride, Pnstride;
+    int nb;
+};
+
+// mode: adj = emit child adjacency (not the last level); topo = emit child faces;
+//       acc = accumulate crease valency/sharpness (refine) vs reuse stored (eval_frames)
+void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
+              cudaStream_t s, Launches &L);
+void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
+                cudaStream_t s, Launches &L);
+void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
+                 cudaStream_t s, Launches &L);
+// crease / boundary overrides and inheritance (crease.cu); ep_base = first edge-point id.
+void crease_eval(const LevelDev &p, const Frames &fr, int32_t ep_base, bool accumulate, cudaStream_t s,
+                 Launches &L);
+void crease_inherit(const LevelDev &p, const ChildDev &c, int scheme, int32_t ep_base, int32_t *cnt,
+                    int32_t *off, void *scratch, cudaStream_t s, Launches &L);
+// Loop child-edge counts -> loop_base (scan); cnt [E] scratch
+void loop_edge_base(const LevelDev &p, int32_t *cnt, int32_t *base, void *scratch, cudaStream_t s, Launches &L);
+// Boundary-edge word prefix of a level (bnd_wcnt -> bnd_wpre)
+void bnd_prefix(uint32_t *words, int32_t *wcnt, int32_t *wpre, int32_t nwords, void *scratch, cudaStream_t s,
+                Launches &L);
+
+// topology export helper: edge_vtx / edge_face from edge_slot + face_twin
+void export_edges(const LevelDev &p, int32_t *edge_vtx, int32_t *edge_face, cudaStream_t s, Launches &L);
+
+}  // namespace alsub

@@ -1,0 +1,311 @@
+// loop_sqrt3.cu -- the Loop (App. B) and sqrt3 (App. A) variants
+// (SURVEY.md 8(a) rows a10, a11).  Same structure as cc.cu: per-face, per-edge and per-vertex
+// gathers with closed-form child adjacency.
+//
+// Loop:   G(a,b) = vertex opposite the directed edge = face_vtx[prev(slot a->b)] (Eq. G);
+//         e = 3/8 (p_a + p_b) + 1/8 (p_G(a,b) + p_G(b,a)) (reading R11);
+//         S = (1 - n beta) p + beta sum p_j (Eq. loop_smooth);
+//         children (k, e_kl, e_mk), (l, e_lm, e_kl), (m, e_mk, e_lm), (e_kl, e_lm, e_mk).
+//         Child edge ids: the children of parent edge e are [(a,ep), (b,ep), (ep_x,ep) for the
+//         distinct edges x < e sharing a triangle with e, ascending]; base_e = scan of counts.
+// sqrt3:  f = barycenters; S = (1 - alpha) p + alpha/n sum p_j (Eqs. sqrt2, alpha);
+//         child 3i+t = (p_k, fp_F(l,k), fp_i) (CCW reading R13); closed only.
+#include "internal.h"
+
+namespace alsub {
+
+__constant__ float c_beta[65];   // Loop beta_n, n <= 64 (host: double -> fp32, reading R16)
+__constant__ float c_alpha[65];  // sqrt3 alpha_n
+
+ALSUB_D float loop_beta(int n) {
+    if (n <= 64) return c_beta[n];
+    const float c = 0.375f + 0.25f * cospif(2.0f / (float)n);
+    return (0.625f - c * c) / (float)n;
+}
+ALSUB_D float sqrt3_alpha(int n) {
+    if (n <= 64) return c_alpha[n];
+    return (4.0f - 2.0f * cospif(2.0f / (float)n)) / 9.0f;
+}
+
+void init_scheme_tables(cudaStream_t s) {
+    float beta[65], alpha[65];
+    beta[0] = alpha[0] = 0.f;
+    for (int n = 1; n <= 64; ++n) {
+        double c = 0.375 + 0.25 * cos(2.0 * M_PI / n);
+        beta[n] = (float)((0.625 - c * c) / n);
+        alpha[n] = (float)((4.0 - 2.0 * cos(2.0 * M_PI / n)) / 9.0);
+    }
+    cudaMemcpyToSymbolAsync(c_beta, beta, sizeof(beta), 0, cudaMemcpyHostToDevice, s);
+    cudaMemcpyToSymbolAsync(c_alpha, alpha, sizeof(alpha), 0, cudaMemcpyHostToDevice, s);
+}
+
+using T3 = Topo<3>;
+
+// ------------------------------------------------------------------------------------------
+// Loop
+// ------------------------------------------------------------------------------------------
+ALSUB_D int32_t tri_next(int32_t h) { int32_t t = h % 3; return t == 2 ? h - 2 : h + 1; }
+ALSUB_D int32_t tri_prev(int32_t h) { int32_t t = h % 3; return t == 0 ? h + 2 : h - 1; }
+
+// the (up to two) other edges of the face owning slot h
+ALSUB_D void other_edges(const int32_t *face_edge, int32_t h, int32_t &x, int32_t &y) {
+    x = __ldg(face_edge + tri_next(h));
+    y = __ldg(face_edge + tri_prev(h));
+}
+
+__global__ void __launch_bounds__(kThreads) k_loop_count(LevelDev p, int32_t *__restrict__ cnt) {
+    const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= p.E) return;
+    const int32_t h = __ldg(p.edge_slot + e), tw = __ldg(p.face_twin + h);
+    int32_t n[4];
+    other_edges(p.face_edge, h, n[0], n[1]);
+    n[2] = n[3] = INT32_MAX;
+    if (tw >= 0) other_edges(p.face_edge, tw, n[2], n[3]);
+    int32_t c = 2;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        bool dup = false;
+#pragma unroll
+        for (int k = 0; k < i; ++k) dup |= (n[k] == n[i]);
+        c += (n[i] < e && !dup);
+    }
+    cnt[e] = c;
+}
+
+void loop_edge_base(const LevelDev &p, int32_t *cnt, int32_t *base, void *scratch, cudaStream_t s, Launches &L) {
+    if (p.E <= 0) return;
+    k_loop_count<<<grid_for(p.E), kThreads, 0, s>>>(p, cnt);
+    L.n += 1;
+    scan_exclusive(cnt, base, p.E, nullptr, scratch, s, L);
+}
+
+// id of the child edge between ep_x and ep_m inside a face (x < m): base_m + 2 + rank of x among
+// the distinct neighbours of m (the other edges of m's two faces) -- all of which are compared with x.
+ALSUB_D int32_t loop_inner(const LevelDev &p, int32_t m, int32_t x, int32_t z, int32_t m_twin) {
+    int32_t n[3] = {z, INT32_MAX, INT32_MAX};
+    if (m_twin >= 0) other_edges(p.face_edge, m_twin, n[1], n[2]);
+    int32_t rank = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        bool dup = n[i] == x;
+#pragma unroll
+        for (int k = 0; k < i; ++k) dup |= (n[k] == n[i]);
+        rank += (n[i] < x && !dup);
+    }
+    return __ldg(p.loop_base + m) + 2 + rank;
+}
+
+template <bool ADJ>
+__global__ void __launch_bounds__(kThreads) k_loop_face(LevelDev p, ChildDev c) {
+    const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= p.F) return;
+    const int32_t V = p.V;
+    int32_t v[3], e[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        v[t] = __ldg(p.face_vtx + 3 * r + t);
+        e[t] = __ldg(p.face_edge + 3 * r + t);
+    }
+    int32_t *cfv = c.face_vtx + 12 * (int64_t)r;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        cfv[3 * t + 0] = v[t];
+        cfv[3 * t + 1] = V + e[t];
+        cfv[3 * t + 2] = V + e[(t + 2) % 3];
+    }
+    cfv[9] = V + e[0];
+    cfv[10] = V + e[1];
+    cfv[11] = V + e[2];
+    if constexpr (ADJ) {
+        int32_t tw[3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) tw[t] = __ldg(p.face_twin + 3 * r + t);
+        // inner edge between edges i and j of this face
+        auto inner = [&](int i, int j) {
+            const int k = 3 - i - j;  // the third edge
+            const int mi = e[i] > e[j] ? i : j, xi = e[i] > e[j] ? j : i;
+            return loop_inner(p, e[mi], e[xi], e[k], tw[mi]);
+        };
+        int32_t in01 = inner(0, 1), in12 = inner(1, 2), in20 = inner(2, 0);
+        const int32_t inner_t_tm1[3] = {in20, in01, in12};  // between e_t and e_{t-1}
+        int32_t *cfe = c.face_edge + 12 * (int64_t)r;
+        int32_t *cft = c.face_twin + 12 * (int64_t)r;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const int tn = (t + 1) % 3, tp = (t + 2) % 3;
+            cfe[3 * t + 0] = __ldg(p.loop_base + e[t]) + (v[t] > v[tn]);
+            cfe[3 * t + 1] = inner_t_tm1[t];
+            cfe[3 * t + 2] = __ldg(p.loop_base + e[tp]) + (v[t] > v[tp]);
+            const int32_t a = tw[t], b = tw[tp];
+            cft[3 * t + 0] = a >= 0 ? 3 * (4 * (a / 3) + (a % 3 + 1) % 3) + 2 : -1;
+            cft[3 * t + 1] = 3 * (4 * r + 3) + tp;
+            cft[3 * t + 2] = b >= 0 ? 3 * (4 * (b / 3) + b % 3) + 0 : -1;
+            c.edge_slot[inner_t_tm1[t]] = 12 * r + 3 * t + 1;
+        }
+        cfe[9] = in01;
+        cfe[10] = in12;
+        cfe[11] = in20;
+        cft[9] = 3 * (4 * r + 1) + 1;
+        cft[10] = 3 * (4 * r + 2) + 1;
+        cft[11] = 3 * (4 * r + 0) + 1;
+    }
+}
+
+ALSUB_D int32_t loop_c0(int32_t x) { return 12 * (x / 3) + 3 * (x % 3); }
+ALSUB_D int32_t loop_c2next(int32_t x) { return 3 * (4 * (x / 3) + (x % 3 + 1) % 3) + 2; }
+
+template <bool ADJ>
+__global__ void __launch_bounds__(kThreads) k_loop_edge(LevelDev p, ChildDev c, Frames fr) {
+    const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= p.E) return;
+    const int32_t h = __ldg(p.edge_slot + e), tw = __ldg(p.face_twin + h);
+    const int32_t va = __ldg(p.face_vtx + h), vb = __ldg(p.face_vtx + tri_next(h));
+    const int32_t g1 = __ldg(p.face_vtx + tri_prev(h));
+    const int32_t g2 = tw >= 0 ? __ldg(p.face_vtx + tri_prev(tw)) : -1;
+    const int32_t V = p.V;
+    for (int f = 0; f < fr.nb; ++f) {
+        const float *P = fr.P + f * fr.Pstride;
+        const P3 ab = ld3(P, va) + ld3(P, vb);
+        P3 out = tw < 0 ? 0.5f * ab : 0.375f * ab + 0.125f * (ld3(P, g1) + ld3(P, g2));
+        st3(fr.Pn + f * fr.Pnstride, (int64_t)V + e, out);
+    }
+    if constexpr (ADJ) {
+        const int32_t base = __ldg(p.loop_base + e);
+        const int32_t h_ab = va < vb ? h : tw, h_ba = va < vb ? tw : h;
+        int32_t o0 = INT32_MAX, o1 = INT32_MAX;
+        if (h_ab >= 0) { o0 = loop_c0(h_ab); o1 = loop_c2next(h_ab); }
+        if (h_ba >= 0) { o0 = min(o0, loop_c2next(h_ba)); o1 = min(o1, loop_c0(h_ba)); }
+        c.edge_slot[base + 0] = o0;
+        c.edge_slot[base + 1] = o1;
+        c.vtx_slot0[V + e] = loop_c0(h) + 1;
+    }
+}
+
+template <bool ADJ>
+__global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c, Frames fr) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= p.V) return;
+    const int32_t h0 = __ldg(p.vtx_slot0 + v);
+    if constexpr (ADJ) c.vtx_slot0[v] = h0 >= 0 ? loop_c0(h0) : -1;
+    for (int f = 0; f < fr.nb; ++f) {
+        const float *P = fr.P + f * fr.Pstride;
+        float *Pn = fr.Pn + f * fr.Pnstride;
+        const P3 pv = ld3(P, v);
+        if (h0 < 0) { st3(Pn, v, pv); continue; }
+        P3 acc = p3zero();
+        int32_t h = h0, n = 0;
+        bool bnd = false;
+        do {
+            acc = acc + ld3(P, __ldg(p.face_vtx + tri_next(h)));
+            ++n;
+            h = __ldg(p.face_twin + tri_prev(h));
+            if (h < 0) { bnd = true; break; }
+        } while (h != h0 && n < p.S);
+        if (bnd) { st3(Pn, v, pv); continue; }
+        const float beta = loop_beta(n);
+        st3(Pn, v, (1.0f - (float)n * beta) * pv + beta * acc);
+    }
+}
+
+void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
+                cudaStream_t s, Launches &L) {
+    (void)scratch;
+    const bool A = adj && topo;
+    if (topo && p.F > 0) {
+        if (A) k_loop_face<true><<<grid_for(p.F), kThreads, 0, s>>>(p, c);
+        else k_loop_face<false><<<grid_for(p.F), kThreads, 0, s>>>(p, c);
+        L.n += 1;
+    }
+    if (p.E > 0) {
+        if (A) k_loop_edge<true><<<grid_for(p.E), kThreads, 0, s>>>(p, c, fr);
+        else k_loop_edge<false><<<grid_for(p.E), kThreads, 0, s>>>(p, c, fr);
+        L.n += 1;
+    }
+    if (p.V > 0) {
+        if (A) k_loop_vertex<true><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
+        else k_loop_vertex<false><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
+        L.n += 1;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// sqrt3
+// ------------------------------------------------------------------------------------------
+template <bool ADJ>
+__global__ void __launch_bounds__(kThreads) k_s3_face(LevelDev p, ChildDev c, Frames fr, bool topo) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.F) return;
+    const int32_t V = p.V;
+    int32_t v[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) v[t] = __ldg(p.face_vtx + 3 * i + t);
+    for (int f = 0; f < fr.nb; ++f) {
+        const float *P = fr.P + f * fr.Pstride;
+        const P3 s = ld3(P, v[0]) + ld3(P, v[1]) + ld3(P, v[2]);
+        st3(fr.Pn + f * fr.Pnstride, (int64_t)V + i, (1.0f / 3.0f) * s);
+    }
+    if (!topo) return;
+    int32_t tw[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) tw[t] = __ldg(p.face_twin + 3 * i + t);
+    int32_t *cfv = c.face_vtx + 9 * (int64_t)i;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        cfv[3 * t + 0] = v[t];
+        cfv[3 * t + 1] = V + tw[t] / 3;
+        cfv[3 * t + 2] = V + i;
+    }
+    if constexpr (ADJ) {
+        int32_t *cft = c.face_twin + 9 * (int64_t)i;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const int32_t a = tw[t], b = tw[(t + 2) % 3];
+            const int32_t na = a / 3, ua = a % 3, nb = b / 3, wb = b % 3;
+            cft[3 * t + 0] = 3 * (3 * na + (ua + 1) % 3) + 2;
+            cft[3 * t + 1] = 3 * (3 * na + ua) + 1;
+            cft[3 * t + 2] = 3 * (3 * nb + wb) + 0;
+        }
+        c.vtx_slot0[V + i] = 9 * i + 2;
+    }
+}
+
+template <bool ADJ>
+__global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, ChildDev c, Frames fr) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= p.V) return;
+    const int32_t h0 = __ldg(p.vtx_slot0 + v);
+    if constexpr (ADJ) c.vtx_slot0[v] = h0 >= 0 ? 3 * h0 : -1;
+    for (int f = 0; f < fr.nb; ++f) {
+        const float *P = fr.P + f * fr.Pstride;
+        float *Pn = fr.Pn + f * fr.Pnstride;
+        const P3 pv = ld3(P, v);
+        if (h0 < 0) { st3(Pn, v, pv); continue; }
+        P3 acc = p3zero();
+        int32_t h = h0, n = 0;
+        do {
+            acc = acc + ld3(P, __ldg(p.face_vtx + tri_next(h)));
+            ++n;
+            h = __ldg(p.face_twin + tri_prev(h));
+        } while (h >= 0 && h != h0 && n < p.S);
+        const float alpha = sqrt3_alpha(n);
+        st3(Pn, v, (1.0f - alpha) * pv + (alpha / (float)n) * acc);
+    }
+}
+
+void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
+                 cudaStream_t s, Launches &L) {
+    (void)scratch;
+    const bool A = adj && topo;
+    if (p.F > 0) {
+        if (A) k_s3_face<true><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+        else k_s3_face<false><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+        L.n += 1;
+    }
+    if (p.V > 0) {
+        if (A) k_s3_vertex<true><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
+        else k_s3_vertex<false><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
+        L.n += 1;
+    }
+}
+
+}  // namespace alsub

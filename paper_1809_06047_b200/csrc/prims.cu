@@ -1,0 +1,247 @@
+// prims.cu -- device-wide primitives for the level-0 mesh-matrix build
+// and the count -> scan -> fill stages of the paper's two-stage constructions.
+//
+//  * scan_exclusive: single-pass decoupled look-back scan (one read + one write of the array).
+//  * radix_sort_pairs: stable LSD radix sort, 8-bit digits, histogram -> scan -> scatter per pass;
+//    the scatter ranks keys with warp match (__match_any_sync) so equal digits keep their order.
+//  * offsets_from_sorted: CSR column pointer of sorted keys ("segmented scan / run-length").
+#include "internal.h"
+
+namespace alsub {
+
+// ------------------------------------------------------------------------------------------
+// decoupled look-back scan
+// ------------------------------------------------------------------------------------------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+constexpr unsigned long long kStatAgg = 1ull << 62;
+constexpr unsigned long long kStatInc = 2ull << 62;
+constexpr unsigned long long kStatMask = (1ull << 62) - 1;
+
+size_t scan_scratch_bytes(int64_t n) {
+    int64_t tiles = ceil_div(n > 0 ? n : 1, kScanTile);
+    return (size_t)(tiles + 2) * sizeof(unsigned long long);
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+    const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int o = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= (unsigned)d) v += o;
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t *__restrict__ in, int32_t *__restrict__ out,
+                                                     int64_t n, unsigned long long *status, int32_t *total) {
+    __shared__ int s_tile;
+    __shared__ int s_data[kScanTile + kScanTile / 32];
+    __shared__ int s_warp[kScanThreads / 32];
+    __shared__ long long s_prefix;
+    unsigned *counter = reinterpret_cast<unsigned *>(status);  // word 0 = tile counter
+    unsigned long long *stat = status + 2;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_tile = (int)atomicAdd(counter, 1u);
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t base = (int64_t)tile * kScanTile;
+    // striped, coalesced load into padded smem
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int i = k * kScanThreads + tid;
+        int64_t g = base + i;
+        s_data[i + (i >> 5)] = g < n ? in[g] : 0;
+    }
+    __syncthreads();
+    int v[kScanItems];
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int i = tid * kScanItems + k;
+        v[k] = s_data[i + (i >> 5)];
+        sum += v[k];
+    }
+    int incl = warp_incl_scan(sum);
+    const int warp = tid >> 5, lane = tid & 31;
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < kScanThreads / 32 ? s_warp[lane] : 0;
+        w = warp_incl_scan(w);
+        if (lane < kScanThreads / 32) s_warp[lane] = w;
+    }
+    __syncthreads();
+    const int block_total = s_warp[kScanThreads / 32 - 1];
+    int excl = incl - sum + (warp > 0 ? s_warp[warp - 1] : 0);
+    if (tid == 0) {
+        long long prefix = 0;
+        if (tile == 0) {
+            atomicExch(&stat[0], kStatInc | (unsigned long long)block_total);
+        } else {
+            atomicExch(&stat[tile], kStatAgg | (unsigned long long)block_total);
+            int p = tile - 1;
+            while (true) {
+                unsigned long long w;
+                do {
+                    w = atomicAdd(&stat[p], 0ull);
+                } while ((w >> 62) == 0);
+                prefix += (long long)(w & kStatMask);
+                if ((w >> 62) == 2) break;
+                --p;
+            }
+            atomicExch(&stat[tile], kStatInc | (unsigned long long)(prefix + block_total));
+        }
+        s_prefix = prefix;
+    }
+    __syncthreads();
+    int run = (int)s_prefix + excl;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int i = tid * kScanItems + k;
+        s_data[i + (i >> 5)] = run;
+        run += v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int i = k * kScanThreads + tid;
+        int64_t g = base + i;
+        if (g < n) out[g] = s_data[i + (i >> 5)];
+    }
+    if (total && tid == 0 && base + kScanTile >= n) *total = (int)(s_prefix + block_total);
+}
+
+void scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *total, void *scratch, cudaStream_t s,
+                    Launches &L) {
+    if (n <= 0) {
+        if (total) cudaMemsetAsync(total, 0, sizeof(int32_t), s);
+        return;
+    }
+    cudaMemsetAsync(scratch, 0, scan_scratch_bytes(n), s);
+    int64_t tiles = ceil_div(n, kScanTile);
+    k_scan<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, n, (unsigned long long *)scratch, total);
+    L.n += 1;
+}
+
+// ------------------------------------------------------------------------------------------
+// LSD radix sort (stable), 8-bit digits
+// ------------------------------------------------------------------------------------------
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 8;
+constexpr int kSortTile = kSortThreads * kSortItems;
+
+static int64_t sort_blocks(int64_t n) { return ceil_div(n > 0 ? n : 1, kSortTile); }
+
+size_t sort_scratch_bytes(int64_t n) {
+    int64_t cnt = 256 * sort_blocks(n);
+    return (size_t)(2 * cnt + 16) * sizeof(int32_t) + scan_scratch_bytes(cnt) + 256;
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_rs_hist(const int32_t *__restrict__ keys, int64_t n, int shift,
+                                                        int32_t *__restrict__ counts, int nblocks) {
+    __shared__ int h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int k = 0; k < kSortItems; ++k) {
+        int64_t i = base + k * kSortThreads + threadIdx.x;
+        if (i < n) atomicAdd(&h[((uint32_t)keys[i] >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    counts[threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];  // digit-major
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_rs_scatter(const int32_t *__restrict__ keys,
+                                                           const int32_t *__restrict__ vals, int64_t n, int shift,
+                                                           const int32_t *__restrict__ offs, int nblocks,
+                                                           int32_t *__restrict__ okeys, int32_t *__restrict__ ovals) {
+    __shared__ int run[256];
+    __shared__ int wc[kSortThreads / 32][256];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    run[tid] = offs[tid * nblocks + blockIdx.x];
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int k = 0; k < kSortItems; ++k) {
+        for (int w = 0; w < kSortThreads / 32; ++w) wc[w][tid] = 0;
+        __syncthreads();
+        int64_t i = base + k * kSortThreads + tid;
+        bool valid = i < n;
+        int32_t key = valid ? keys[i] : 0;
+        int32_t val = valid ? vals[i] : 0;
+        unsigned d = valid ? (((uint32_t)key >> shift) & 255u) : 256u;  // 256 = invalid bucket
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        int rank = __popc(peers & ((1u << lane) - 1u));
+        int leader = __ffs(peers) - 1;
+        if (valid && lane == leader) wc[warp][d] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            int pos = run[d] + rank;
+            for (int w = 0; w < warp; ++w) pos += wc[w][d];
+            okeys[pos] = key;
+            ovals[pos] = val;
+        }
+        __syncthreads();
+        int add = 0;
+        for (int w = 0; w < kSortThreads / 32; ++w) add += wc[w][tid];
+        run[tid] += add;
+        __syncthreads();
+    }
+}
+
+void radix_sort_pairs(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *vals_alt, int64_t n, int bits,
+                      void *scratch, cudaStream_t s, Launches &L) {
+    if (n <= 1) return;
+    const int nblocks = (int)sort_blocks(n);
+    const int64_t cnt = 256 * (int64_t)nblocks;
+    int32_t *counts = (int32_t *)scratch;
+    int32_t *offs = counts + cnt;
+    void *scan_scratch = (void *)(((uintptr_t)(offs + cnt + 16) + 255) & ~(uintptr_t)255);
+    int passes = (bits + 7) / 8;
+    if (passes < 1) passes = 1;
+    int32_t *ka = keys, *va = vals, *kb = keys_alt, *vb = vals_alt;
+    for (int p = 0; p < passes; ++p) {
+        int shift = 8 * p;
+        k_rs_hist<<<nblocks, kSortThreads, 0, s>>>(ka, n, shift, counts, nblocks);
+        scan_exclusive(counts, offs, cnt, nullptr, scan_scratch, s, L);
+        k_rs_scatter<<<nblocks, kSortThreads, 0, s>>>(ka, va, n, shift, offs, nblocks, kb, vb);
+        L.n += 2;
+        int32_t *t;
+        t = ka; ka = kb; kb = t;
+        t = va; va = vb; vb = t;
+    }
+    if (ka != keys) {
+        cudaMemcpyAsync(keys, ka, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(vals, va, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// CSR offsets of sorted keys (run-length of the sorted key array)
+// ------------------------------------------------------------------------------------------
+__global__ void k_offsets(const int32_t *__restrict__ keys, int64_t n, int32_t *__restrict__ off, int32_t nkeys) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t k = keys[i];
+    int32_t kp = i == 0 ? -1 : keys[i - 1];
+    for (int32_t v = kp + 1; v <= k; ++v) off[v] = (int32_t)i;
+    if (i == n - 1)
+        for (int32_t v = k + 1; v <= nkeys; ++v) off[v] = (int32_t)n;
+}
+
+__global__ void k_fill_i32(int32_t *p, int64_t n, int32_t val) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = val;
+}
+
+void offsets_from_sorted(const int32_t *keys, int64_t n, int32_t *off, int32_t nkeys, cudaStream_t s, Launches &L) {
+    if (n == 0) {
+        cudaMemsetAsync(off, 0, sizeof(int32_t) * ((size_t)nkeys + 1), s);
+        return;
+    }
+    k_offsets<<<grid_for(n), kThreads, 0, s>>>(keys, n, off, nkeys);
+    L.n += 1;
+}
+
+}  // namespace alsub

@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Topology (face lists, edge ids/vertex pairs, F(i,j)/F(j,i), crease lists) bit-exact at every level;
+positions within 1e-5 x the control mesh's bounding-box diagonal (BASELINE.json north_star,
+SURVEY.md 8(c) c15).
+"""
+import numpy as np
+import pytest
+import torch
+
+import meshgen as mg
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def _gpu():
+    from paper_1809_06047_b200 import Mesh
+    return Mesh
+
+
+def diag_of(mesh):
+    p = mesh["pos"].astype(np.float64)
+    return float(np.linalg.norm(p.max(0) - p.min(0)))
+
+
+def compare(mesh, scheme, levels, edges=True, creases=True, oracle_recs=None):
+    Mesh = _gpu()
+    want = oracle_recs or oracle.refine(mesh, scheme, levels)
+    diag = diag_of(mesh)
+    worst = 0.0
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine(scheme, levels)
+        torch.cuda.synchronize()
+        for lv in range(levels + 1):
+            c = m.counts(lv)
+            w = want[lv]
+            assert (c["verts"], c["faces"]) == (w["V"], w["F"]), f"L{lv} counts"
+            want_edges = edges and lv < levels and c["edges_valid"]
+            t = m.topology(lv, edges=want_edges, creases=creases)
+            assert np.array_equal(t["face_vtx"].cpu().numpy(), w["face_vtx"]), f"L{lv} face_vtx"
+            assert np.array_equal(t["face_off"].cpu().numpy(), w["face_off"]), f"L{lv} face_off"
+            if want_edges:
+                assert c["edges"] == w["E"] and c["boundary_edges"] == w["B"], f"L{lv} E/B"
+                assert np.array_equal(t["edge_vtx"].cpu().numpy(), w["edge_vtx"]), f"L{lv} edge_vtx"
+                assert np.array_equal(t["edge_face"].cpu().numpy(), w["edge_face"]), f"L{lv} edge_face"
+            if creases and lv > 0:
+                assert np.array_equal(t["crease"].cpu().numpy(), w["crease"]), f"L{lv} crease pairs"
+                assert np.array_equal(t["sigma"].cpu().numpy(), w["sigma"]), f"L{lv} crease sigma"
+            P = m.positions(lv).cpu().numpy().astype(np.float64)
+            err = float(np.abs(P - w["pos"]).max()) / diag if w["V"] else 0.0
+            worst = max(worst, err)
+            assert err <= TOL, f"L{lv} positions: max err {err:.3e} x diag"
+    return worst
+
+
+def _octahedron():
+    pos = [(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)]
+    faces = [(0, 2, 4), (2, 1, 4), (1, 3, 4), (3, 0, 4), (2, 0, 5), (1, 2, 5), (3, 1, 5), (0, 3, 5)]
+    return mg._pack(faces, pos, name="octa")
+
+
+def _mixed_polys():
+    """Pentagon + hexagon + quads + triangles sharing edges, open boundary, creases."""
+    pos = [(0, 0, 0), (1, 0, 0), (2, 0, 0.2), (2.5, 1, 0), (2, 2, 0.1), (1, 2, 0), (0, 2, 0.3), (-0.5, 1, 0),
+           (1, 1, 0.5), (3, 0, 0), (3.5, 1.5, 0.2)]
+    faces = [(0, 1, 8, 6, 7), (1, 2, 3, 4, 5, 8), (5, 6, 8), (2, 9, 3), (9, 10, 3)]
+    return mg._pack(faces, pos, [(1, 8), (8, 5), (2, 3)], [1.5, 0.5, np.inf], name="mixed")
+
+
+CASES = [
+    ("cube", mg.cube, "cc", 3),
+    ("tet", mg.tetrahedron, "cc", 3),
+    ("tet_creased_cc", lambda: mg.tetrahedron(creased=True), "cc", 4),
+    ("tet_creased_loop", lambda: mg.tetrahedron(creased=True), "loop", 4),
+    ("ico_loop", mg.icosahedron, "loop", 4),
+    ("octa_loop", _octahedron, "loop", 3),
+    ("quad", mg.single_quad, "cc", 4),
+    ("grid_tris", lambda: mg.grid(5, 4, tri_cells=[(1, 1), (3, 2)]), "cc", 4),
+    ("mixed", _mixed_polys, "cc", 4),
+    ("armor_small", lambda: mg.armor(6, 5, 6, 1, 1, 2, name="armor_small"), "cc", 4),
+    ("armor_small_shuf", lambda: mg.shuffled(mg.armor(6, 5, 6, 1, 1, 2, name="armor_small")), "cc", 3),
+    ("torus_sqrt3", lambda: mg.torus_tris(20, 15), "sqrt3", 4),
+    ("octa_sqrt3", _octahedron, "sqrt3", 3),
+    ("torus_loop", lambda: mg.torus_tris(16, 12), "loop", 3),
+    ("grid_loop_bnd", lambda: mg.grid(4, 3, tri_cells=[(i, j) for i in range(4) for j in range(3)]), "loop", 3),
+]
+
+
+@pytest.mark.parametrize("name,mk,scheme,levels", CASES, ids=[c[0] for c in CASES])
+def test_parity_small(name, mk, scheme, levels):
+    compare(mk(), scheme, levels)
+
+
+def test_parity_semisharp_and_corners():
+    """Semi-sharp creases (0 < sigma < 1), a crease ending inside (dart), 3 creases at a vertex."""
+    g = mg.random_positions(mg.torus_quads(9, 7), seed=2, scale=0.3)
+    nu = 9
+    vid = lambda i, j: (j % 7) * nu + (i % nu)
+    pairs = [(vid(0, 0), vid(1, 0)), (vid(1, 0), vid(2, 0)), (vid(2, 0), vid(3, 0)),
+             (vid(1, 0), vid(1, 1)), (vid(1, 0), vid(1, 6)), (vid(5, 3), vid(6, 3))]
+    sig = [0.25, 0.75, 2.5, 1.25, np.inf, 0.5]
+    g["crease"], g["sigma"] = np.array(pairs, np.int32), np.array(sig, np.float32)
+    compare(g, "cc", 4)
+
+
+def test_parity_armor9k_L3():
+    compare(mg.armor9k(), "cc", 3)
+
+
+def test_parity_torus100k_sqrt3_L3():
+    compare(mg.torus100k(), "sqrt3", 3, edges=True)
+
+
+def test_parity_ico_loop_L6():
+    compare(mg.icosahedron(), "loop", 6)
+
+
+def test_parity_armor9k_L6_full():
+    """Config 3 at full size (35M faces), same launch configuration as bench.py."""
+    mesh = mg.armor9k()
+    worst = compare(mesh, "cc", 6, edges=False)
+    assert worst < TOL
+
+
+def test_graph_and_eager_bitwise_equal(monkeypatch):
+    Mesh = _gpu()
+    mesh = mg.armor(6, 5, 6, 1, 1, 2, name="armor_small")
+    outs = []
+    for env in ("0", "1"):
+        monkeypatch.setenv("ALSUB_NO_GRAPH", env)
+        with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+            m.refine("cc", 4)
+            m.refine("cc", 4)  # replay
+            outs.append((m.positions(4).cpu(), m.topology(4)["face_vtx"].cpu()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+def test_eval_frames_equals_refine():
+    """Static mode reproduces dynamic mode bitwise for the same vertex data."""
+    Mesh = _gpu()
+    mesh = mg.armor(8, 6, 7, 1, 2, 2, name="armor_f")
+    P0 = torch.from_numpy(mesh["pos"]).cuda()
+    frames = torch.stack([torch.from_numpy(mg.frame_positions(mesh["pos"], t, 64)) for t in range(5)]).cuda()
+    with Mesh(mesh["face_off"], mesh["face_vtx"], P0, mesh["crease"], mesh["sigma"]) as m:
+        m.refine("cc", 3)
+        out = m.eval_frames(frames, 3)
+        for t in range(5):
+            m.set_positions(frames[t])
+            m.refine("cc", 3)
+            ref = m.positions(3)
+            assert torch.equal(out[t], ref), f"frame {t}"
+    # and against the oracle for one frame
+    m2 = dict(mesh)
+    m2["pos"] = mg.frame_positions(mesh["pos"], 3, 64)
+    w = oracle.refine(m2, "cc", 3)[-1]["pos"]
+    assert np.abs(out[3].cpu().numpy() - w).max() / diag_of(mesh) < TOL
+
+
+def test_eval_frames_loop_and_sqrt3():
+    Mesh = _gpu()
+    for mesh, scheme in ((mg.tetrahedron(creased=True), "loop"), (mg.torus_tris(10, 8), "sqrt3")):
+        fr = torch.stack([torch.from_numpy(mg.random_positions(mesh, seed=s)["pos"]) for s in range(3)]).cuda()
+        with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+            m.refine(scheme, 3)
+            out = m.eval_frames(fr, 3)
+            for s in range(3):
+                mm = mg.random_positions(mesh, seed=s)
+                w = oracle.refine(mm, scheme, 3)[-1]["pos"]
+                d = diag_of(mm)
+                assert np.abs(out[s].cpu().numpy() - w).max() / d < TOL
+
+
+def test_host_pointers_roundtrip():
+    """C-ABI with HOST buffers in and out (the e2e path of bench.py)."""
+    from paper_1809_06047_b200 import alsub as A
+    import ctypes as C
+    mesh = mg.cube()
+    L = A.lib()
+    h = C.c_void_p()
+    st = L.alsub_mesh_create(mesh["face_off"].ctypes.data, mesh["face_vtx"].ctypes.data, 6, mesh["pos"].ctypes.data,
+                             8, None, None, 0, None, None, C.byref(h))
+    assert st == 0
+    assert L.alsub_refine(h, 0, 2, None) == 0
+    out = np.zeros((98, 3), np.float32)
+    fv = np.zeros(96 * 4, np.int32)
+    assert L.alsub_level_positions(h, 2, out.ctypes.data, None) == 0
+    assert L.alsub_level_topology(h, 2, fv.ctypes.data, None, None, None, None, None, None, None) == 0
+    w = oracle.refine(mesh, "cc", 2)[-1]
+    assert np.array_equal(fv, w["face_vtx"]) and np.abs(out - w["pos"]).max() < 1e-6
+    L.alsub_mesh_destroy(h)
+
+
+def test_error_statuses():
+    from paper_1809_06047_b200 import AlsubError
+    Mesh = _gpu()
+    pos = np.zeros((5, 3), np.float32)
+
+    def status(mesh, scheme=None):
+        try:
+            with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+                if scheme:
+                    m.refine(scheme, 1)
+        except AlsubError as e:
+            return e.status
+        return "OK"
+
+    assert status(mg._pack([(0, 1, 2), (0, 1, 3)], pos)) == "E_NONMANIFOLD"
+    assert status(mg._pack([(0, 1, 2), (1, 0, 3), (0, 1, 4)], pos)) == "E_NONMANIFOLD"
+    assert status(mg._pack([(0, 1, 7)], pos)) == "E_MESH"
+    assert status(mg._pack([(0, 1)], pos)) == "E_MESH"
+    assert status(mg._pack([(0, 1, 1, 2)], pos)) == "E_MESH"
+    c = mg.cube()
+    assert status(dict(c, crease=np.array([[0, 7]], np.int32), sigma=np.array([1.0], np.float32))) == "E_CREASE"
+    assert status(dict(c, crease=np.array([[0, 1]], np.int32), sigma=np.array([-1.0], np.float32))) == "E_CREASE"
+    assert status(dict(c, crease=np.array([[0, 1], [1, 0]], np.int32), sigma=np.array([1.0, 2.0], np.float32))) == "E_CREASE"
+    assert status(c, "loop") == "E_SCHEME"
+    assert status(mg.grid(2, 2, tri_cells=[(0, 0), (1, 0), (0, 1), (1, 1)]), "sqrt3") == "E_SCHEME"
+    # two closed fans glued at a vertex (two tetrahedra sharing vertex 0)
+    tpos = np.random.default_rng(0).standard_normal((7, 3)).astype(np.float32)
+    f1 = [(0, 1, 2), (0, 3, 1), (0, 2, 3), (1, 3, 2)]
+    f2 = [(0, 4, 5), (0, 6, 4), (0, 5, 6), (4, 6, 5)]
+    assert status(mg._pack(f1 + f2, tpos)) == "E_NONMANIFOLD"
+
+
+def test_empty_and_isolated():
+    Mesh = _gpu()
+    # isolated vertex 4 passes through unchanged
+    mesh = mg._pack([(0, 1, 2, 3)], [(0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (5, 5, 5)])
+    compare(mesh, "cc", 2)
+    # levels = 0 returns the input
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"]) as m:
+        m.refine("cc", 0)
+        assert np.array_equal(m.positions(0).cpu().numpy(), mesh["pos"])
+
+
+def test_deterministic():
+    Mesh = _gpu()
+    mesh = mg.armor(6, 5, 6, 1, 1, 2, name="armor_small")
+    res = []
+    for _ in range(2):
+        with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+            m.refine("cc", 4)
+            res.append(m.positions(4).cpu())
+    assert torch.equal(res[0], res[1])
