@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""Benchmark: refined faces/s of AlSub uniform refinement on B200 (BASELINE.json metric).
+
+Default workload (N=1): SURVEY.md 8(d) config 3 -- Catmull-Clark level 6 of the ArmorGuy-shaped
+creased mesh armor9k (8,590 faces -> 34,897,920 faces).  A step is one alsub_refine(CC, 6): the
+whole hot path (level-0 mesh matrix, radix-sort M^T, edge index, creases, then 6 levels of
+topology + geometry), replayed as a CUDA graph with inputs resident in HBM.  L2 is flushed (a
+256 MiB write) between timed steps.  With N > 1 ranks (torchrun) each rank refines its own
+independent mesh (seed 1809 + rank): weak scaling, no collective on the data path.
+
+--config 5: static-mode frames (armor50k CC level 4, 4096 frames split over the ranks, batches
+of 8 frames per step through alsub_eval_frames).
+
+--impl reference: the CPU oracle (oracle/, plain single-threaded C) timed on this host on a
+bounded sample of the same workload -- rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import meshgen as mg  # noqa: E402
+
+METRIC = "refined faces/sec per level (topo+geometry) and achieved HBM GB/s vs B200 peak"
+PAPER_CONTEXT = "ArmorGuy CC level 6 (35.2M faces) in ~40 ms on a GTX 1080 Ti (PAPER.md P:L91, P:L735)"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------------------------------
+# algorithmic bytes: every array a kernel touches, read or written once
+# ------------------------------------------------------------------------------------------
+def level_counts(m, levels):
+    """Per-level counts from the library (alsub_level_counts)."""
+    out = []
+    for l in range(levels + 1):
+        c = m.counts(l)
+        out.append(dict(V=c["verts"], F=c["faces"], S=c["face_slots"], E=c["edges"]))
+    return out
+
+
+def kernel_bytes_cc(name, c, adj):
+    """Algorithmic bytes of one launch of a CC level kernel; c = parent counts."""
+    V, F, S, E = c["V"], c["F"], c["S"], c["E"]
+    if name == "cc_face":
+        rd = 4 * S + 4 * S + 12 * V + (4 * S if adj else 0)            # face_vtx, face_edge, P (+face_twin)
+        wr = 12 * F + 16 * S + ((16 * S + 16 * S + 4 * F) if adj else 0)  # f, child faces (+face_edge', face_twin', slot0')
+    elif name == "cc_edge":
+        rd = 4 * E + 4 * S + 4 * E + 12 * V + 12 * F                     # edge_slot, face_vtx, face_twin[owner], P, f
+        wr = 12 * E + ((4 * (2 * E + S) + 4 * E) if adj else 0)           # e (+edge_slot', slot0')
+    elif name == "cc_vertex":
+        rd = 4 * V + 4 * S + 4 * S + 12 * V + 12 * F                     # slot0, face_vtx, face_twin, P, f
+        wr = 12 * V + (4 * V if adj else 0)
+    else:
+        return None
+    return rd + wr
+
+
+def survey_level_bytes_cc(c, final):
+    """SURVEY.md 8(d) per-level compulsory model: read 4S + 4S + 16E + 12V, write 16F' + 12V'
+    (+16F' face_edge' + 16E' edge tables when another level follows)."""
+    V, F, S, E = c["V"], c["F"], c["S"], c["E"]
+    Vn, Fn, En = V + F + E, S, 2 * E + S
+    b = 8 * S + 16 * E + 12 * V + 16 * Fn + 12 * Vn
+    if not final:
+        b += 16 * Fn + 16 * En
+    return b
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons while the timed region runs."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index, period=0.002):
+        self.samples, self.reasons = [], 0
+        self.period = period
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_oracle_baseline(mesh, levels, label):
+    """The oracle as it stands, single-threaded, on this host: faces/s of the final level."""
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    recs = oracle.refine(mesh, "cc", levels)
+    dt = time.perf_counter() - t0
+    F = recs[-1]["F"]
+    return {"value": F / dt, "unit": "faces/s", "cores": 1, "kind": "oracle",
+            "sample": f"{label}: CC levels 0->{levels} ({F} faces) in {dt:.2f} s, single-threaded C oracle (fp64)",
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    mesh = mg.armor9k()
+    levels = args.ref_levels or (5 if args.steps <= 12 else 4)
+    times = []
+    F = None
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        recs = oracle.refine(mesh, "cc", levels)
+        dt = time.perf_counter() - t0
+        F = recs[-1]["F"]
+        del recs
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1000 * sum(times) / len(times)
+    value = F / (ms / 1000)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "faces/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "armor9k_cc_L6 (config 3), bounded sample", "scheme": "catmull-clark",
+                       "levels_sampled": levels, "faces_out": F},
+            "cpu_baseline": {"value": value, "unit": "faces/s", "cores": 1, "kind": "oracle",
+                             "sample": f"armor9k CC levels 0->{levels} ({F} faces) per step, single-threaded C oracle"},
+            "e2e": {"value": value, "unit": "faces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_alsub(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1809_06047_b200 import Mesh
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    peak, peak_src = peaks()
+    if args.config == 5:
+        return run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, peak_src)
+
+    levels = args.levels
+    mesh = mg.armor9k(seed=mg.SEED_TOPO + rank)
+    stream = torch.cuda.current_stream()
+    m = Mesh(torch.from_numpy(mesh["face_off"]).to(dev), torch.from_numpy(mesh["face_vtx"]).to(dev),
+             torch.from_numpy(mesh["pos"]).to(dev), torch.from_numpy(mesh["crease"]).to(dev),
+             torch.from_numpy(mesh["sigma"]).to(dev))
+    m.refine("cc", levels)  # plan + eager run
+    m.refine("cc", levels)  # records the CUDA graph
+    cnt = level_counts(m, levels)
+    Fout, Vout = cnt[-1]["F"], cnt[-1]["V"]
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        m.refine("cc", levels)
+    torch.cuda.synchronize()
+    launches_per_step = m.last_launch_count
+    K = args.steps
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        for i in range(K):
+            flush.fill_(float(i))
+            ev0[i].record(stream)
+            m.refine("cc", levels)
+            ev1[i].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    total_ms = max_over_ranks(sum(step_ms))
+    ms_per_step = total_ms / K
+    value = world * Fout * K / (total_ms / 1000.0)
+
+    # ---- per-kernel timing (CUDA events between launches, eager), averaged over reps ----
+    reps = max(3, min(10, K))
+    acc = {}
+    for _ in range(reps):
+        flush.fill_(2.0)
+        for name, lvl, ms in m.refine_profile("cc", levels):
+            acc.setdefault((name, lvl), []).append(ms)
+    kt = {k: sum(v) / len(v) for k, v in acc.items()}
+    prof_step = sum(kt.values())
+    per_level = []
+    for lvl in range(-1, levels):
+        ks = {n: t for (n, l), t in kt.items() if l == lvl}
+        row = {"level": lvl, "ms": sum(ks.values())}
+        if lvl >= 0:
+            c = cnt[lvl]
+            final = lvl == levels - 1
+            sb = survey_level_bytes_cc(c, final)
+            row.update(faces_out=cnt[lvl + 1]["F"], survey_bytes=sb,
+                       survey_GBps=sb / (row["ms"] * 1e6) if row["ms"] > 0 else None)
+            row["survey_frac"] = row["survey_GBps"] / peak if row["survey_GBps"] else None
+            kk = {}
+            for n, t in ks.items():
+                b = kernel_bytes_cc(n, c, not final)
+                kk[n] = {"ms": t, "alg_bytes": b, "GBps": (b / (t * 1e6)) if b else None,
+                         "frac": (b / (t * 1e6) / peak) if b else None}
+            row["kernels"] = kk
+        per_level.append(row)
+    # dominant kernel = the largest share of the step
+    (dname, dlvl), dms = max(kt.items(), key=lambda kv: kv[1])
+    dbytes = kernel_bytes_cc(dname, cnt[dlvl], dlvl < levels - 1) if dlvl >= 0 else None
+    achieved = dbytes / (dms * 1e6) if dbytes else None
+    traffic = None
+    prof_sum = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof_sum):
+        try:
+            ps = json.load(open(prof_sum))
+            traffic = ps.get("kernels", {}).get(f"{dname}@L{dlvl}", {}).get("dram_bytes")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": f"{dname} (level {dlvl}->{dlvl + 1})", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "alg_bytes_per_launch": dbytes, "avg_launch_ms": dms, "share_of_step": dms / prof_step,
+                "peak_source": peak_src}
+
+    # ---- e2e through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, mesh, levels, Fout, Vout, dev, flush)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_baseline(mg.armor9k(), levels, "armor9k (config 3), the full workload")
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "faces/s", "n_gpus": world, "steps": K,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"armor9k_cc_L{levels} (SURVEY config 3)", "scheme": "catmull-clark",
+                           "levels": levels, "control_faces": int(len(mesh["face_off"]) - 1),
+                           "faces_out": int(Fout), "verts_out": int(Vout),
+                           "l2": "256 MiB buffer written between timed steps (L2 flush)",
+                           "parallelism": f"{world} independent mesh replicas" if world > 1 else "single GPU",
+                           "graph": True},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches_per_step * K), "launches_per_step": int(launches_per_step),
+                "clocks": sampler.summary(), "levels": per_level, "profile_step_ms": prof_step,
+                "paper_context": PAPER_CONTEXT}
+        print(json.dumps(line), flush=True)
+    m.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, mesh, levels, Fout, Vout, dev, flush):
+    """Same metric through the public C ABI with HOST buffers: per step alsub_mesh_create from pinned
+    host arrays (H2D inside), alsub_refine (eager, one-shot), positions + faces back to pinned host."""
+    import torch
+    from paper_1809_06047_b200 import Mesh
+    pin = lambda a: torch.from_numpy(a).pin_memory()
+    fo, fv, P, cr, sg = pin(mesh["face_off"]), pin(mesh["face_vtx"]), pin(mesh["pos"]), pin(mesh["crease"]), pin(mesh["sigma"])
+    out_P = torch.empty((Vout, 3), dtype=torch.float32).pin_memory()
+    out_F = torch.empty(4 * Fout, dtype=torch.int32).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in (fo, fv, P, cr, sg))
+    d2h = out_P.numel() * 4 + out_F.numel() * 4
+    from paper_1809_06047_b200 import alsub as A
+    L = A.lib()
+    stream = torch.cuda.current_stream()
+    steps = max(2, min(args.steps, 5))
+    times = []
+    for i in range(1 + steps):
+        flush.fill_(3.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        m = Mesh(fo, fv, P, cr, sg)
+        m.refine("cc", levels)
+        A._check(L.alsub_level_positions(m._h, levels, out_P.data_ptr(), stream.cuda_stream))
+        A._check(L.alsub_level_topology(m._h, levels, out_F.data_ptr(), None, None, None, None, None, None,
+                                        stream.cuda_stream))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        m.close()
+        if i > 0:
+            times.append(e0.elapsed_time(e1))
+    ms = sum(times) / len(times)
+    return {"value": Fout / (ms / 1000.0), "unit": "faces/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
+            "path": "alsub_mesh_create(host) + alsub_refine + alsub_level_positions/topology(pinned host)"}
+
+
+def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, peak_src):
+    """Config 5: static-mode frames, armor50k CC level 4, 4096 frames sharded over ranks."""
+    import torch
+    from paper_1809_06047_b200 import Mesh
+    levels = 4
+    nframes = args.frames
+    mesh = mg.armor50k()
+    nb = 8
+    per_rank = nframes // world
+    f_lo = rank * per_rank
+    P0 = mesh["pos"]
+    # frame inputs resident in HBM: this rank's block of frames (V0 x 12 B each)
+    frames = torch.stack([torch.from_numpy(mg.frame_positions(P0, f_lo + t, nframes)) for t in range(per_rank)]).to(dev)
+    m = Mesh(mesh["face_off"], mesh["face_vtx"], P0, mesh["crease"], mesh["sigma"])
+    m.refine("cc", levels)
+    cnt = level_counts(m, levels)
+    Vout, Fout = cnt[-1]["V"], cnt[-1]["F"]
+    outs = [torch.empty((nb, Vout, 3), dtype=torch.float32, device=dev) for _ in range(2)]
+    nsteps = per_rank // nb
+    for i in range(min(args.warmup, nsteps)):
+        m.eval_frames(frames[i * nb:(i + 1) * nb], levels, out=outs[i % 2])
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(dev.index)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        e0.record(stream)
+        for i in range(nsteps):
+            m.eval_frames(frames[i * nb:(i + 1) * nb], levels, out=outs[i % 2])
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    total_frames = nsteps * nb * world
+    value = total_frames * Fout / (ms / 1000.0)
+    bytes_per_frame = sum(12 * cnt[l]["V"] + 12 * cnt[l + 1]["V"] for l in range(levels))
+    gbps = nsteps * nb * bytes_per_frame / (ms * 1e6 / 1.0) if ms else None
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "faces/s", "n_gpus": world, "steps": nsteps,
+                "warmup": args.warmup, "ms_per_step": ms / nsteps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"armor50k_cc_L{levels}_frames{nframes} (SURVEY config 5)",
+                           "frames": total_frames, "batch": nb, "faces_per_frame": Fout,
+                           "l2": "inputs and outputs far larger than L2",
+                           "parallelism": f"frames sharded over {world} GPUs"},
+                "roofline": {"bound": "hbm", "achieved": gbps, "peak": peak, "unit": "GB/s",
+                             "frac": gbps / peak if gbps else None, "traffic": None,
+                             "kernel": "whole static eval (position bytes only)", "peak_source": peak_src},
+                "cpu_baseline": None, "e2e": None, "gpu_launches": int(m.last_launch_count * nsteps),
+                "clocks": sampler.summary()}
+        print(json.dumps(line), flush=True)
+    m.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="alsub", choices=["alsub", "reference"])
+    ap.add_argument("--config", type=int, default=3, choices=[3, 5])
+    ap.add_argument("--levels", type=int, default=6)
+    ap.add_argument("--frames", type=int, default=4096)
+    ap.add_argument("--ref-levels", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_alsub(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -90,16 +90,30 @@ alsub_status alsub_set_positions(alsub_mesh *mesh, const float *pos, void *strea
 /* Dynamic mode: rebuild everything from the level-0 mesh matrix (a1-a3 of
  * SURVEY.md 8(a)) and run `levels` build+eval iterations of `scheme`.  Fully asynchronous on
  * `stream` (no host synchronisation); the first call per (scheme, levels) allocates the level
- * tables and records a CUDA graph that later calls replay (env ALSUB_NO_GRAPH=1 disables).
+ * tables and launches eagerly, the second records a CUDA graph that later calls replay
+ * (env ALSUB_NO_GRAPH=1 disables graphs).
  * levels = 0 returns the input.  Errors: E_ARG, E_SCHEME, E_OVERFLOW, E_NOMEM, E_CUDA. */
 alsub_status alsub_refine(alsub_mesh *mesh, alsub_scheme scheme, int32_t levels, void *stream);
+
+/* Per-kernel timing of one eager refine (instrumentation; the paper reports "the sum of all
+ * kernel timings").  A CUDA event is recorded after every kernel launch on `stream`;
+ * entry i is the time between event i-1 (or the start event) and event i, i.e. the kernel plus
+ * any memset issued just before it.  Synchronises `stream`.  *n_out = number of kernels
+ * (entries beyond `cap` are dropped).  level = -1 for the level-0 build. */
+typedef struct {
+    char name[32];
+    int32_t level;
+    float ms;
+} alsub_kernel_time;
+alsub_status alsub_refine_profile(alsub_mesh *mesh, alsub_scheme scheme, int32_t levels, void *stream,
+                                  alsub_kernel_time *out, int32_t cap, int32_t *n_out);
 
 /* Host-only: counts of level `level` of the last refine (level 0 always available). */
 alsub_status alsub_level_counts(const alsub_mesh *mesh, int32_t level, alsub_counts *out);
 
 /* Export the topology of level `level` (0 .. last refine's levels).  Every output is nullable.
  *   face_vtx     [face_slots]       face_off [faces+1]
- *   edge_vtx     [edges][2] (lo,hi) in edge-id order      (levels < last, or CC/Loop last)
+ *   edge_vtx     [edges][2] (lo,hi) in edge-id order      (levels < last refined level)
  *   edge_face    [edges][2] face of lo->hi, face of hi->lo, -1 = none
  *   crease_pairs [creases_upper_bound][2] (lo,hi) ascending edge id; crease_sigma [...]
  *   num_creases  [1] int32: the exact number written (boundary edges are not listed)

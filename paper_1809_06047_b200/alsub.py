@@ -34,6 +34,10 @@ class _Counts(C.Structure):
                 ("edges_valid", C.c_int32)]
 
 
+class _KTime(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("level", C.c_int32), ("ms", C.c_float)]
+
+
 _ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 _FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 
@@ -58,6 +62,7 @@ def lib():
     L.alsub_set_positions.argtypes = [vp, vp, vp]
     L.alsub_refine.argtypes = [vp, C.c_int, i32, vp]
     L.alsub_level_counts.argtypes = [vp, i32, C.POINTER(_Counts)]
+    L.alsub_refine_profile.argtypes = [vp, C.c_int, i32, vp, C.POINTER(_KTime), i32, C.POINTER(i32)]
     L.alsub_level_topology.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp]
     L.alsub_level_positions.argtypes = [vp, i32, vp, vp]
     L.alsub_eval_frames.argtypes = [vp, i32, vp, i32, vp, vp]
@@ -67,7 +72,7 @@ def lib():
     L.alsub_mesh_destroy.restype = None
     L.alsub_last_error.restype = C.c_char_p
     L.alsub_version.restype = C.c_char_p
-    for f in ("alsub_mesh_create", "alsub_set_positions", "alsub_refine", "alsub_level_counts",
+    for f in ("alsub_mesh_create", "alsub_set_positions", "alsub_refine", "alsub_refine_profile", "alsub_level_counts",
               "alsub_level_topology", "alsub_level_positions", "alsub_eval_frames"):
         getattr(L, f).restype = C.c_int
     _lib = L
@@ -187,6 +192,15 @@ class Mesh:
         _check(self._lib.alsub_refine(self._h, sc, int(levels), _stream(stream)))
         self.scheme, self.levels = sc, int(levels)
         return self
+
+    def refine_profile(self, scheme, levels, stream=None, cap=4096):
+        """Eager refine with a CUDA event after every kernel: [(name, level, ms), ...]."""
+        sc = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
+        buf = (_KTime * cap)()
+        n = C.c_int32()
+        _check(self._lib.alsub_refine_profile(self._h, sc, int(levels), _stream(stream), buf, cap, C.byref(n)))
+        self.scheme, self.levels = sc, int(levels)
+        return [(buf[i].name.decode(), int(buf[i].level), float(buf[i].ms)) for i in range(min(n.value, cap))]
 
     def counts(self, level):
         c = _Counts()

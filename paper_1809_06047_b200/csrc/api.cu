@@ -88,6 +88,7 @@ struct alsub_mesh {
     std::vector<LevelHost> lv;
     cudaGraphExec_t gexec = nullptr;
     int64_t graph_launches = 0;
+    int64_t plan_runs = 0;  // refines run with the current plan (graph recorded from the 2nd on)
     cudaStream_t cap_stream = nullptr;
     int64_t last_launches = 0;
     // frames
@@ -413,6 +414,7 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
         return fail(ALSUB_E_NOMEM, "device allocation failed for the level tables");
     }
     m->lv = std::move(lv);
+    m->plan_runs = 0;
     m->scheme = scheme;
     m->levels = levels;
     return ALSUB_OK;
@@ -422,6 +424,7 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
 static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     const int scheme = m->scheme, levels = m->levels;
     // a1-a3: level-0 mesh matrix, M^T by radix sort, edge index, creases
+    L.level = -1;
     build0_count_edges(m->b0, s, L);
     build0_fill(m->b0, false, s, L);
     const bool special = scheme != ALSUB_SQRT3 && m->K0 > 0;
@@ -429,6 +432,7 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
         LevelHost &P = m->lv[l];
         LevelHost &C = m->lv[l + 1];
         const bool adj = l + 1 < levels;
+        L.level = l;
         LevelDev p = dev_of(P);
         p.sv_vtx = m->sv_vtx;
         ChildDev c = child_of(C);
@@ -470,7 +474,9 @@ extern "C" alsub_status alsub_refine(alsub_mesh *m, alsub_scheme scheme, int32_t
         if (st != ALSUB_OK) return st;
     }
     Launches L;
-    if (graphs_enabled()) {
+    const bool use_graph = graphs_enabled() && m->plan_runs >= 1;  // one-shot refines run eagerly
+    m->plan_runs++;
+    if (use_graph) {
         if (!m->gexec) {
             // the plan's allocations are stream-ordered on `s`: make the capture stream wait for them
             cudaEvent_t ev;
@@ -496,6 +502,46 @@ extern "C" alsub_status alsub_refine(alsub_mesh *m, alsub_scheme scheme, int32_t
         m->last_launches = L.n;
     }
     CU(cudaGetLastError());
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_refine_profile(alsub_mesh *m, alsub_scheme scheme, int32_t levels, void *stream,
+                                             alsub_kernel_time *out, int32_t cap, int32_t *n_out) {
+    if (!m || (cap > 0 && !out)) return fail(ALSUB_E_ARG, "null argument");
+    if (scheme < ALSUB_CATMULL_CLARK || scheme > ALSUB_SQRT3) return fail(ALSUB_E_ARG, "unknown scheme");
+    if (levels < 0 || levels > 16) return fail(ALSUB_E_ARG, "levels must be in [0, 16]");
+    alsub_status st = check_scheme(m, scheme);
+    if (st != ALSUB_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (m->scheme != scheme || m->levels != levels) {
+        st = make_plan(m, scheme, levels, s);
+        if (st != ALSUB_OK) return st;
+    }
+    Launches L;
+    L.timing = true;
+    cudaEvent_t start;
+    CU(cudaEventCreate(&start));
+    CU(cudaEventRecord(start, s));
+    enqueue_refine(m, s, L);
+    CU(cudaStreamSynchronize(s));
+    CU(cudaGetLastError());
+    const int32_t n = (int32_t)L.ev.size();
+    cudaEvent_t prev = start;
+    for (int32_t i = 0; i < n; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, prev, L.ev[i]);
+        if (i < cap) {
+            memset(out[i].name, 0, sizeof(out[i].name));
+            strncpy(out[i].name, L.name[i], sizeof(out[i].name) - 1);
+            out[i].level = L.lvl[i];
+            out[i].ms = ms;
+        }
+        prev = L.ev[i];
+    }
+    for (auto e : L.ev) cudaEventDestroy(e);
+    cudaEventDestroy(start);
+    if (n_out) *n_out = n;
+    m->last_launches = L.n;
     return ALSUB_OK;
 }
 

@@ -211,7 +211,7 @@ void build0_validate(Build0 &b, cudaStream_t s, Launches &L) {
     if (b.F > 0) {
         k_validate_faces<<<grid_for(b.F), kThreads, 0, s>>>(b.face_off, b.face_vtx, b.F, b.V, b.slot_face, b.sort_k,
                                                             b.sort_v, b.flags);
-        L.n += 1;
+        L.done("b0_validate", s);
     }
 }
 
@@ -229,7 +229,7 @@ void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L) {
     cudaMemcpyAsync(b.vtx_slot, b.sort_v, sizeof(int32_t) * (size_t)b.S, cudaMemcpyDeviceToDevice, s);
     if (b.V > 0) {
         k_edge_count<<<grid_for(b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V, b.edge_cnt);
-        L.n += 1;
+        L.done("b0_edge_count", s);
     }
     scan_exclusive(b.edge_cnt, b.edge_off, b.V, b.scalars + 0, b.scratch, s, L);
 }
@@ -244,15 +244,16 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
         k_edge_fill<<<grid_for(b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V, b.edge_off,
                                                        b.face_edge, b.face_twin, b.edge_slot, b.bnd_word, b.scalars,
                                                        b.flags);
+        L.done("b0_edge_fill", s);
         k_slot0<<<grid_for(b.V), kThreads, 0, s>>>(b.vtx_off, b.vtx_slot, b.V, b.vtx_slot0);
-        L.n += 2;
+        L.done("b0_slot0", s);
         if (check_fans) {
             k_check_fans<<<grid_for(b.V), kThreads, 0, s>>>(b.face_twin, b.vtx_off, b.vtx_slot0, tp, b.V, b.flags);
-            L.n += 1;
+            L.done("b0_check_fans", s);
         }
     }
     k_word_popc<<<grid_for(nw), kThreads, 0, s>>>(b.bnd_word, nw, b.bnd_wcnt);
-    L.n += 1;
+    L.done("b0_popc", s);
     scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, b.scratch, s, L);
     if (E > 0) {
         cudaMemsetAsync(b.edge_sigma, 0, sizeof(float) * E, s);
@@ -262,27 +263,27 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
         k_crease_lookup<<<grid_for(b.K_in), kThreads, 0, s>>>(b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off,
                                                               b.vtx_slot, b.face_edge, b.face_twin, b.edge_slot, tp,
                                                               b.V, b.edge_sigma, b.edge_cidx, b.flags);
-        L.n += 1;
+        L.done("b0_crease_lookup", s);
     }
     if (E > 0) {
         k_special_flag<<<grid_for(E), kThreads, 0, s>>>(b.edge_slot, b.face_twin, b.edge_sigma, E, b.sp_flag);
-        L.n += 1;
+        L.done("b0_special_flag", s);
     }
     scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, b.scratch, s, L);
     if (b.V > 0) cudaMemsetAsync(b.v_mark, 0, sizeof(int32_t) * b.V, s);
     if (E > 0 && b.sp) {
         k_special_fill<<<grid_for(E), kThreads, 0, s>>>(b.edge_slot, b.face_twin, b.face_vtx, b.edge_sigma, b.sp_flag,
                                                         b.sp_off, tp, E, b.sp, b.v_mark);
-        L.n += 1;
+        L.done("b0_special_fill", s);
     }
     scan_exclusive(b.v_mark, b.v_idx, b.V, b.scalars + 3, b.scratch, s, L);
     if (b.V > 0 && b.sv_vtx) {
         k_sv_fill<<<grid_for(b.V), kThreads, 0, s>>>(b.v_mark, b.v_idx, b.V, b.sv_vtx);
-        L.n += 1;
+        L.done("b0_sv_fill", s);
     }
     if (E > 0 && b.sp) {
         k_sp_index<<<grid_for(E), kThreads, 0, s>>>(b.sp, b.scalars + 2, b.v_idx, E);
-        L.n += 1;
+        L.done("b0_sp_index", s);
     }
 }
 

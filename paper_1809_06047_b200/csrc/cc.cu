@@ -183,15 +183,15 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bo
     if (p.F > 0) {
         if constexpr (ORDER == 4) k_cc_face_quad<ADJ, BND><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
         else k_cc_face_gen<ORDER, ADJ, BND><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
-        L.n += 1;
+        L.done("cc_face", s);
     }
     if (p.E > 0) {
         k_cc_edge<ORDER, ADJ, BND><<<grid_for(p.E), kThreads, 0, s>>>(p, c, fr, topo);
-        L.n += 1;
+        L.done("cc_edge", s);
     }
     if (p.V > 0) {
         k_cc_vertex<ORDER, ADJ><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr, topo);
-        L.n += 1;
+        L.done("cc_vertex", s);
     }
 }
 

@@ -76,10 +76,10 @@ void crease_eval(const LevelDev &p, const Frames &fr, int32_t ep_base, bool accu
     if (p.sp_cap <= 0) return;
     if (accumulate && p.sv_cap > 0) cudaMemsetAsync(p.sva, 0, sizeof(SvAcc) * (size_t)p.sv_cap, s);
     k_sp_edge<<<grid_for(p.sp_cap), kThreads, 0, s>>>(p, fr, ep_base, accumulate);
-    L.n += 1;
+    L.done("sp_edge", s);
     if (p.sv_cap > 0) {
         k_sp_vert<<<grid_for(p.sv_cap), kThreads, 0, s>>>(p, fr, accumulate);
-        L.n += 1;
+        L.done("sp_vert", s);
     }
 }
 
@@ -135,10 +135,11 @@ void crease_inherit(const LevelDev &p, const ChildDev &c, int scheme, int32_t ep
         return;
     }
     k_sp_count<<<grid_for(p.sp_cap), kThreads, 0, s>>>(p, cnt);
+    L.done("sp_count", s);
     scan_exclusive(cnt, off, p.sp_cap, c.sp_count, scratch, s, L);
     if (scheme == 0) k_sp_fill<0><<<grid_for(p.sp_cap), kThreads, 0, s>>>(p, c, ep_base, off);
     else k_sp_fill<1><<<grid_for(p.sp_cap), kThreads, 0, s>>>(p, c, ep_base, off);
-    L.n += 2;
+    L.done("sp_fill", s);
 }
 
 // ---------------- boundary-word prefix ----------------
@@ -150,7 +151,7 @@ __global__ void k_popc_words(const uint32_t *__restrict__ w, int32_t n, int32_t 
 void bnd_prefix(uint32_t *words, int32_t *wcnt, int32_t *wpre, int32_t nwords, void *scratch, cudaStream_t s,
                 Launches &L) {
     k_popc_words<<<grid_for(nwords), kThreads, 0, s>>>(words, nwords, wcnt);
-    L.n += 1;
+    L.done("popc_words", s);
     scan_exclusive(wcnt, wpre, nwords, nullptr, scratch, s, L);
 }
 
@@ -178,7 +179,7 @@ void export_edges(const LevelDev &p, int32_t *edge_vtx, int32_t *edge_face, cuda
     if (p.order == 4) k_export_edges<4><<<grid_for(p.E), kThreads, 0, s>>>(p, edge_vtx, edge_face);
     else if (p.order == 3) k_export_edges<3><<<grid_for(p.E), kThreads, 0, s>>>(p, edge_vtx, edge_face);
     else k_export_edges<0><<<grid_for(p.E), kThreads, 0, s>>>(p, edge_vtx, edge_face);
-    L.n += 1;
+    L.done("export_edges", s);
 }
 
 }  // namespace alsub

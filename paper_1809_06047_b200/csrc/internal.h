@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace alsub {
@@ -10,6 +12,23 @@ namespace alsub {
 // Counts kernel launches issued into a stream (reported by alsub_last_launch_count).
 struct Launches {
     int64_t n = 0;
+    // optional per-kernel timing (alsub_refine_profile): an event after every launch
+    bool timing = false;
+    int level = -1;
+    std::vector<cudaEvent_t> ev;
+    std::vector<const char *> name;
+    std::vector<int> lvl;
+    void done(const char *kname, cudaStream_t s) {
+        ++n;
+        if (timing) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, s);
+            ev.push_back(e);
+            name.push_back(kname);
+            lvl.push_back(level);
+        }
+    }
 };
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kThreads) k_loop_count(LevelDev p, int32_t *__
 void loop_edge_base(const LevelDev &p, int32_t *cnt, int32_t *base, void *scratch, cudaStream_t s, Launches &L) {
     if (p.E <= 0) return;
     k_loop_count<<<grid_for(p.E), kThreads, 0, s>>>(p, cnt);
-    L.n += 1;
+    L.done("loop_count", s);
     scan_exclusive(cnt, base, p.E, nullptr, scratch, s, L);
 }
 
@@ -214,17 +214,17 @@ void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool top
     if (topo && p.F > 0) {
         if (A) k_loop_face<true><<<grid_for(p.F), kThreads, 0, s>>>(p, c);
         else k_loop_face<false><<<grid_for(p.F), kThreads, 0, s>>>(p, c);
-        L.n += 1;
+        L.done("loop_face", s);
     }
     if (p.E > 0) {
         if (A) k_loop_edge<true><<<grid_for(p.E), kThreads, 0, s>>>(p, c, fr);
         else k_loop_edge<false><<<grid_for(p.E), kThreads, 0, s>>>(p, c, fr);
-        L.n += 1;
+        L.done("loop_edge", s);
     }
     if (p.V > 0) {
         if (A) k_loop_vertex<true><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
         else k_loop_vertex<false><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
-        L.n += 1;
+        L.done("loop_vertex", s);
     }
 }
 
@@ -299,12 +299,12 @@ void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool to
     if (p.F > 0) {
         if (A) k_s3_face<true><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
         else k_s3_face<false><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
-        L.n += 1;
+        L.done("s3_face", s);
     }
     if (p.V > 0) {
         if (A) k_s3_vertex<true><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
         else k_s3_vertex<false><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
-        L.n += 1;
+        L.done("s3_vertex", s);
     }
 }
 

@@ -123,7 +123,7 @@ void scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *total, 
     cudaMemsetAsync(scratch, 0, scan_scratch_bytes(n), s);
     int64_t tiles = ceil_div(n, kScanTile);
     k_scan<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, n, (unsigned long long *)scratch, total);
-    L.n += 1;
+    L.done("scan", s);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -204,9 +204,10 @@ void radix_sort_pairs(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *
     for (int p = 0; p < passes; ++p) {
         int shift = 8 * p;
         k_rs_hist<<<nblocks, kSortThreads, 0, s>>>(ka, n, shift, counts, nblocks);
+        L.done("rs_hist", s);
         scan_exclusive(counts, offs, cnt, nullptr, scan_scratch, s, L);
         k_rs_scatter<<<nblocks, kSortThreads, 0, s>>>(ka, va, n, shift, offs, nblocks, kb, vb);
-        L.n += 2;
+        L.done("rs_scatter", s);
         int32_t *t;
         t = ka; ka = kb; kb = t;
         t = va; va = vb; vb = t;
@@ -241,7 +242,7 @@ void offsets_from_sorted(const int32_t *keys, int64_t n, int32_t *off, int32_t n
         return;
     }
     k_offsets<<<grid_for(n), kThreads, 0, s>>>(keys, n, off, nkeys);
-    L.n += 1;
+    L.done("offsets", s);
 }
 
 }  // namespace alsub
