@@ -142,6 +142,25 @@ def dist_env():
     return rank, world, local
 
 
+def shard(n, world, rank):
+    """Contiguous block of n independent units (frames / meshes) owned by `rank`."""
+    per = n // world
+    extra = n % world
+    lo = rank * per + min(rank, extra)
+    return lo, lo + per + (1 if rank < extra else 0)
+
+
+def dist_max(x, device=None):
+    """Max of a scalar over all ranks (timing only; no data-path collective)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return x
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def cpu_oracle_baseline(mesh, levels, label):
     """The oracle as it stands, single-threaded, on this host: faces/s of the final level."""
     import oracle
@@ -203,11 +222,7 @@ def run_alsub(args):
             dist.barrier()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return dist_max(x, dev)
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     peak, peak_src = peaks()
@@ -367,8 +382,8 @@ def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, pea
     nframes = args.frames
     mesh = mg.armor50k()
     nb = 8
-    per_rank = nframes // world
-    f_lo = rank * per_rank
+    f_lo, f_hi = shard(nframes, world, rank)
+    per_rank = f_hi - f_lo
     P0 = mesh["pos"]
     # frame inputs resident in HBM: this rank's block of frames (V0 x 12 B each)
     frames = torch.stack([torch.from_numpy(mg.frame_positions(P0, f_lo + t, nframes)) for t in range(per_rank)]).to(dev)

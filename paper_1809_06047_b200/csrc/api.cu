@@ -51,17 +51,15 @@ struct LevelHost {
     int order = 4;
     bool edges_valid = true;
     int32_t *face_off = nullptr, *slot_face = nullptr, *face_vtx = nullptr, *face_edge = nullptr,
-            *face_twin = nullptr, *edge_slot = nullptr, *vtx_slot0 = nullptr;
+            *face_twin = nullptr, *vtx_slot0 = nullptr;
+    int2 *edge_hh = nullptr;
     uint32_t *bnd_word = nullptr;
-    int32_t *bnd_wcnt = nullptr, *bnd_wpre = nullptr;
+    int32_t *bnd_wpre = nullptr;
     int32_t *loop_cnt = nullptr, *loop_base = nullptr;
-    SpEdge *sp = nullptr;
-    int32_t sp_cap = 0;
-    int32_t *sp_count = nullptr;
-    int32_t sv_cap = 0;
-    int32_t *sv_count = nullptr;
-    SvAcc *sva = nullptr;
-    int32_t *inh_cnt = nullptr, *inh_off = nullptr;
+    SpEdge *sp = nullptr;       // special edges of this level [nsp]
+    int64_t nsp = 0;            // = 2^l K_0
+    int32_t *sv_list = nullptr; // [2 nsp] incident special edges of the special vertices
+    int64_t nsv = 0;            // special vertices of this level (prefix of the shared table)
     float *pos = nullptr;
 };
 
@@ -77,8 +75,8 @@ struct alsub_mesh {
     Build0 b0{};
     int32_t E0 = 0, B0 = 0, K0 = 0, NSV0 = 0;
     bool user_creases = false;
-    int32_t *d_counts = nullptr;  // per level: [2l] sp_count, [2l+1] sv_count
-    int32_t *sv_vtx = nullptr;
+    int32_t *sv_vtx = nullptr, *sv_off = nullptr;  // shared special-vertex table (prefix per level)
+    int32_t *sv_vtx_create = nullptr, *sv_off_create = nullptr;
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
     void *scratch_create = nullptr;
@@ -134,19 +132,18 @@ static LevelDev dev_of(const LevelHost &L) {
     p.V = (int32_t)L.V; p.F = (int32_t)L.F; p.S = (int32_t)L.S; p.E = (int32_t)L.E; p.B = (int32_t)L.B;
     p.order = L.order;
     p.face_off = L.face_off; p.slot_face = L.slot_face;
-    p.face_vtx = L.face_vtx; p.face_edge = L.face_edge; p.face_twin = L.face_twin; p.edge_slot = L.edge_slot;
+    p.face_vtx = L.face_vtx; p.face_edge = L.face_edge; p.face_twin = L.face_twin; p.edge_hh = L.edge_hh;
     p.vtx_slot0 = L.vtx_slot0; p.bnd_word = L.bnd_word; p.bnd_wpre = L.bnd_wpre; p.loop_base = L.loop_base;
-    p.sp = L.sp; p.sp_count = L.sp_count; p.sp_cap = L.sp_cap;
-    p.sv_count = L.sv_count; p.sva = L.sva; p.sv_cap = L.sv_cap;
+    p.sp = L.sp; p.nsp = (int32_t)L.nsp; p.sv_list = L.sv_list; p.nsv = (int32_t)L.nsv;
     return p;
 }
 
 static ChildDev child_of(const LevelHost &L) {
     ChildDev c{};
     c.V = (int32_t)L.V; c.F = (int32_t)L.F; c.S = (int32_t)L.S; c.E = (int32_t)L.E;
-    c.face_vtx = L.face_vtx; c.face_edge = L.face_edge; c.face_twin = L.face_twin; c.edge_slot = L.edge_slot;
-    c.vtx_slot0 = L.vtx_slot0; c.bnd_word = L.bnd_word; c.bnd_wcnt = L.bnd_wcnt; c.bnd_wpre = L.bnd_wpre;
-    c.sp = L.sp; c.sp_count = L.sp_count; c.sp_cap = L.sp_cap; c.sv_count = L.sv_count;
+    c.face_vtx = L.face_vtx; c.face_edge = L.face_edge; c.face_twin = L.face_twin; c.edge_hh = L.edge_hh;
+    c.vtx_slot0 = L.vtx_slot0; c.bnd_word = L.bnd_word; c.bnd_wpre = L.bnd_wpre;
+    c.sp = L.sp; c.sv_list = L.sv_list;
     return c;
 }
 
@@ -156,10 +153,9 @@ static void set_level0_view(alsub_mesh *m, LevelHost &L) {
     L.order = m->order0;
     L.face_off = m->in_face_off; L.slot_face = b.slot_face;
     L.face_vtx = m->in_face_vtx; L.face_edge = b.face_edge; L.face_twin = b.face_twin;
-    L.edge_slot = b.edge_slot; L.vtx_slot0 = b.vtx_slot0;
-    L.bnd_word = b.bnd_word; L.bnd_wcnt = b.bnd_wcnt; L.bnd_wpre = b.bnd_wpre;
-    L.sp = b.sp; L.sp_cap = m->K0; L.sp_count = b.scalars + 2;
-    L.sv_cap = m->NSV0; L.sv_count = b.scalars + 3;
+    L.edge_hh = b.edge_hh; L.vtx_slot0 = b.vtx_slot0;
+    L.bnd_word = b.bnd_word; L.bnd_wpre = b.bnd_wpre;
+    L.sp = b.sp; L.nsp = m->K0; L.sv_list = b.sv_list; L.nsv = m->NSV0;
     L.pos = m->pos0;
 }
 
@@ -237,6 +233,7 @@ extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t
     b.face_edge = A<int32_t>(m, S0, s, ML, ok);
     b.face_twin = A<int32_t>(m, S0, s, ML, ok);
     b.vtx_slot0 = A<int32_t>(m, num_verts, s, ML, ok);
+    b.vbnd = A<int32_t>(m, num_verts, s, ML, ok);
     b.v_mark = A<int32_t>(m, num_verts, s, ML, ok);
     b.v_idx = A<int32_t>(m, num_verts, s, ML, ok);
     b.flags = A<int32_t>(m, 8, s, ML, ok);
@@ -269,7 +266,7 @@ extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t
     m->E0 = E0;
     b.E = E0;
     const int64_t nw = ceil_div(E0 > 0 ? E0 : 1, 32);
-    b.edge_slot = A<int32_t>(m, E0, s, ML, ok);
+    b.edge_hh = A<int2>(m, E0, s, ML, ok);
     b.bnd_word = A<uint32_t>(m, nw, s, ML, ok);
     b.bnd_wcnt = A<int32_t>(m, nw, s, ML, ok);
     b.bnd_wpre = A<int32_t>(m, nw, s, ML, ok);
@@ -279,6 +276,12 @@ extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t
     b.sp_off = A<int32_t>(m, E0, s, ML, ok);
     b.sp = A<SpEdge>(m, E0, s, ML, ok);
     b.sv_vtx = A<int32_t>(m, num_verts, s, ML, ok);
+    b.sv_off = A<int32_t>(m, (int64_t)num_verts + 1, s, ML, ok);
+    b.sv_cnt = A<int32_t>(m, num_verts, s, ML, ok);
+    b.sv_cur = A<int32_t>(m, num_verts, s, ML, ok);
+    b.sv_list = A<int32_t>(m, 2 * (int64_t)E0, s, ML, ok);
+    m->sv_vtx = m->sv_vtx_create = b.sv_vtx;
+    m->sv_off = m->sv_off_create = b.sv_off;
     if (!ok) return bail(fail(ALSUB_E_NOMEM, "device allocation failed"));
     build0_fill(b, true, s, L);
     int32_t sc[8];
@@ -312,6 +315,8 @@ static void free_plan(alsub_mesh *m, cudaStream_t s) {
     free_list(m, m->mem_frames, s);
     m->scratch = m->scratch_create;
     m->scratch_bytes = m->scratch_create_bytes;
+    m->sv_vtx = m->b0.sv_vtx = m->sv_vtx_create;
+    m->sv_off = m->b0.sv_off = m->sv_off_create;
     m->b0.scratch = m->scratch;
     m->frame_buf.clear();
     m->frames_nb = 0;
@@ -349,16 +354,18 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
         if (c.V > INT32_MAX || c.S > INT32_MAX || c.E > INT32_MAX || 4 * c.S > INT32_MAX)
             return fail(ALSUB_E_OVERFLOW, "level " + std::to_string(l) + " exceeds int32 ids");
         if (special) {
-            c.sp_cap = (int32_t)std::min<int64_t>(2 * (int64_t)p.sp_cap, INT32_MAX / 2);
-            c.sv_cap = p.sv_cap + p.sp_cap;
+            c.nsp = 2 * p.nsp;
+            c.nsv = p.nsv + p.nsp;
+            if (2 * c.nsp > INT32_MAX || c.nsv > INT32_MAX) return fail(ALSUB_E_OVERFLOW, "special lists exceed int32");
         }
     }
     bool ok = true;
     auto &ML = m->mem_plan;
-    const int64_t sv_total = special ? lv[levels].sv_cap : 1;
+    const int64_t sv_total = std::max<int64_t>(m->V0, special ? lv[levels].nsv : 0) + 1;
     m->sv_vtx = A<int32_t>(m, sv_total, s, ML, ok);
+    m->sv_off = A<int32_t>(m, sv_total, s, ML, ok);
     m->b0.sv_vtx = m->sv_vtx;
-    m->d_counts = A<int32_t>(m, 2 * ((int64_t)levels + 1), s, ML, ok);
+    m->b0.sv_off = m->sv_off;
     int64_t max_scan = std::max<int64_t>(m->V0, m->S0) + 1;
     for (int l = 0; l <= levels; ++l) {
         LevelHost &c = lv[l];
@@ -369,35 +376,26 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
             c.pos = A<float>(m, 3 * c.V, s, ML, ok);
             if (has_child) {
                 c.face_twin = A<int32_t>(m, c.S, s, ML, ok);
-                c.vtx_slot0 = A<int32_t>(m, c.V, s, ML, ok);
+                if (scheme != ALSUB_CATMULL_CLARK) c.vtx_slot0 = A<int32_t>(m, c.V, s, ML, ok);
                 if (scheme != ALSUB_SQRT3) {
                     c.face_edge = A<int32_t>(m, c.S, s, ML, ok);
-                    c.edge_slot = A<int32_t>(m, c.E, s, ML, ok);
+                    c.edge_hh = A<int2>(m, c.E, s, ML, ok);
                 }
                 if (scheme == ALSUB_CATMULL_CLARK && c.B > 0) {
                     const int64_t nw = ceil_div(c.E, 32);
                     c.bnd_word = A<uint32_t>(m, nw, s, ML, ok);
-                    c.bnd_wcnt = A<int32_t>(m, nw, s, ML, ok);
                     c.bnd_wpre = A<int32_t>(m, nw, s, ML, ok);
-                    max_scan = std::max<int64_t>(max_scan, nw);
                 }
             }
             if (special) {
-                c.sp = A<SpEdge>(m, c.sp_cap, s, ML, ok);
-                c.sp_count = m->d_counts + 2 * l;
-                c.sv_count = m->d_counts + 2 * l + 1;
+                c.sp = A<SpEdge>(m, c.nsp, s, ML, ok);
+                c.sv_list = A<int32_t>(m, 2 * c.nsp, s, ML, ok);
             }
         }
         if (scheme == ALSUB_LOOP && has_child && (adj || special)) {
             c.loop_cnt = A<int32_t>(m, c.E, s, ML, ok);
             c.loop_base = A<int32_t>(m, c.E, s, ML, ok);
             max_scan = std::max<int64_t>(max_scan, c.E);
-        }
-        if (special && has_child) {
-            c.sva = A<SvAcc>(m, c.sv_cap, s, ML, ok);
-            c.inh_cnt = A<int32_t>(m, c.sp_cap, s, ML, ok);
-            c.inh_off = A<int32_t>(m, c.sp_cap, s, ML, ok);
-            max_scan = std::max<int64_t>(max_scan, c.sp_cap);
         }
         (void)adj;
     }
@@ -421,6 +419,24 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
 }
 
 // ---------------- the level loop ----------------
+// vertex-id segments of CC level l (see VSegs in internal.h)
+static VSegs make_segs(alsub_mesh *m, int l) {
+    VSegs g{};
+    g.level = l;
+    int n = 0;
+    g.start[n] = 0; g.len[n] = m->V0; g.type[n] = 0; g.birth[n] = 0; ++n;
+    for (int k = 1; k <= l; ++k) {
+        const LevelHost &q = m->lv[k - 1];
+        g.start[n] = (int32_t)q.V; g.len[n] = (int32_t)q.F; g.type[n] = 1; g.birth[n] = (int8_t)k; ++n;
+        g.start[n] = (int32_t)(q.V + q.F); g.len[n] = (int32_t)q.E; g.type[n] = 2; g.birth[n] = (int8_t)k; ++n;
+        g.ehh[k - 1] = q.edge_hh;
+    }
+    g.nseg = n;
+    g.vtx_off0 = m->b0.vtx_off; g.vtx_list0 = m->b0.vtx_slot; g.face_off0 = m->in_face_off;
+    g.slot_face0 = m->b0.slot_face; g.vbnd0 = m->b0.vbnd;
+    return g;
+}
+
 static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     const int scheme = m->scheme, levels = m->levels;
     // a1-a3: level-0 mesh matrix, M^T by radix sort, edge index, creases
@@ -435,22 +451,19 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
         L.level = l;
         LevelDev p = dev_of(P);
         p.sv_vtx = m->sv_vtx;
+        p.sv_off = m->sv_off;
         ChildDev c = child_of(C);
         c.sv_vtx = m->sv_vtx;
+        c.sv_off = m->sv_off;
         Frames fr{P.pos, C.pos, 3 * P.V, 3 * C.V, 1};
         if (scheme == ALSUB_CATMULL_CLARK) {
-            cc_level(p, c, fr, true, adj, m->scratch, s, L);
-            if (special) {
-                crease_eval(p, fr, (int32_t)(P.V + P.F), true, s, L);
-                crease_inherit(p, c, 0, (int32_t)(P.V + P.F), P.inh_cnt, P.inh_off, m->scratch, s, L);
-            }
+            VSegs g = make_segs(m, l);
+            cc_level(p, c, fr, true, adj, g, s, L);
+            if (special) crease_level(p, c, fr, (int32_t)(P.V + P.F), 0, true, s, L);
         } else if (scheme == ALSUB_LOOP) {
             if (adj || special) loop_edge_base(p, P.loop_cnt, P.loop_base, m->scratch, s, L);
             loop_level(p, c, fr, true, adj, m->scratch, s, L);
-            if (special) {
-                crease_eval(p, fr, (int32_t)P.V, true, s, L);
-                crease_inherit(p, c, 1, (int32_t)P.V, P.inh_cnt, P.inh_off, m->scratch, s, L);
-            }
+            if (special) crease_level(p, c, fr, (int32_t)P.V, 1, true, s, L);
         } else {
             sqrt3_level(p, c, fr, true, adj, m->scratch, s, L);
         }
@@ -564,7 +577,7 @@ extern "C" alsub_status alsub_level_counts(const alsub_mesh *m, int32_t level, a
     const LevelHost *L = level_of(m, level);
     if (!L) return fail(ALSUB_E_ARG, "level not built (call alsub_refine first)");
     out->verts = L->V; out->faces = L->F; out->edges = L->E; out->boundary_edges = L->B; out->face_slots = L->S;
-    out->creases_upper_bound = L->sp_cap; out->face_order = L->order;
+    out->creases_upper_bound = L->nsp; out->face_order = L->order;
     out->edges_valid = (L->edges_valid && level < m->levels) ? 1 : 0;
     return ALSUB_OK;
 }
@@ -610,7 +623,7 @@ extern "C" alsub_status alsub_level_topology(const alsub_mesh *mc, int32_t level
         }
     }
     if (edge_vtx || edge_face) {
-        const bool have = L->edges_valid && (level == 0 || level < m->levels) && L->edge_slot && L->face_twin;
+        const bool have = L->edges_valid && (level == 0 || level < m->levels) && L->edge_hh;
         if (!have) { free_list(m, tmp, s); return fail(ALSUB_E_ARG, "edge tables are not kept for this level"); }
         int32_t *dv = edge_vtx && !is_device_ptr(edge_vtx) ? A<int32_t>(m, 2 * L->E, s, tmp, ok) : edge_vtx;
         int32_t *df = edge_face && !is_device_ptr(edge_face) ? A<int32_t>(m, 2 * L->E, s, tmp, ok) : edge_face;
@@ -620,19 +633,17 @@ extern "C" alsub_status alsub_level_topology(const alsub_mesh *mc, int32_t level
         if (df != edge_face) CU(copy_out(edge_face, df, sizeof(int32_t) * 2 * (size_t)L->E, s));
     }
     if (crease_pairs || crease_sigma || num_creases) {
-        int32_t cnt = 0;
+        int32_t cnt = (int32_t)L->nsp;
         std::vector<SpEdge> sp;
-        if (L->sp && L->sp_count) {
-            CU(cudaMemcpyAsync(&cnt, L->sp_count, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-            CU(cudaStreamSynchronize(s));
+        if (L->sp && cnt > 0) {
             sp.resize((size_t)cnt);
-            if (cnt > 0) CU(cudaMemcpyAsync(sp.data(), L->sp, sizeof(SpEdge) * cnt, cudaMemcpyDeviceToHost, s));
+            CU(cudaMemcpyAsync(sp.data(), L->sp, sizeof(SpEdge) * cnt, cudaMemcpyDeviceToHost, s));
             CU(cudaStreamSynchronize(s));
         }
         std::vector<int32_t> pairs;
         std::vector<float> sig;
         for (const SpEdge &e : sp) {
-            if (e.flags & kSpBoundary) continue;
+            if ((e.flags & kSpBoundary) || !(e.sigma > 0.0f)) continue;
             pairs.push_back(e.a);
             pairs.push_back(e.b);
             sig.push_back(e.sigma);
@@ -710,14 +721,16 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
             float *Pn = (l + 1 == levels) ? Pout_final : m->frame_buf[l + 1];
             LevelDev p = dev_of(Pl);
             p.sv_vtx = m->sv_vtx;
+            p.sv_off = m->sv_off;
             ChildDev c{};
             Frames fr{P, Pn, 3 * Pl.V, 3 * m->lv[l + 1].V, n};
             if (scheme == ALSUB_CATMULL_CLARK) {
-                cc_level(p, c, fr, false, false, m->scratch, s, L);
-                if (special) crease_eval(p, fr, (int32_t)(Pl.V + Pl.F), false, s, L);
+                VSegs g = make_segs(m, l);
+                cc_level(p, c, fr, false, false, g, s, L);
+                if (special) crease_level(p, c, fr, (int32_t)(Pl.V + Pl.F), 0, false, s, L);
             } else if (scheme == ALSUB_LOOP) {
                 loop_level(p, c, fr, false, false, m->scratch, s, L);
-                if (special) crease_eval(p, fr, (int32_t)Pl.V, false, s, L);
+                if (special) crease_level(p, c, fr, (int32_t)Pl.V, 1, false, s, L);
             } else {
                 sqrt3_level(p, c, fr, false, false, m->scratch, s, L);
             }

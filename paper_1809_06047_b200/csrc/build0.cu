@@ -74,8 +74,9 @@ __global__ void k_edge_count(const int32_t *__restrict__ face_vtx, const int32_t
 __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t *__restrict__ vtx_off,
                             const int32_t *__restrict__ vtx_slot, T0 tp, int32_t V,
                             const int32_t *__restrict__ edge_off, int32_t *__restrict__ face_edge,
-                            int32_t *__restrict__ face_twin, int32_t *__restrict__ edge_slot,
-                            uint32_t *__restrict__ bnd_word, int32_t *__restrict__ scalars, int32_t *flags) {
+                            int32_t *__restrict__ face_twin, int2 *__restrict__ edge_hh,
+                            uint32_t *__restrict__ bnd_word, int32_t *__restrict__ vbnd,
+                            int32_t *__restrict__ scalars, int32_t *flags) {
     int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= V) return;
     Cand cd{face_vtx, vtx_slot, tp, vtx_off[j]};
@@ -101,10 +102,13 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
         if (s_ij >= 0) { face_edge[s_ij] = e; face_twin[s_ij] = s_ji; }
         if (s_ji >= 0) { face_edge[s_ji] = e; face_twin[s_ji] = s_ij; }
         int32_t own = s_ij < 0 ? s_ji : (s_ji < 0 ? s_ij : min(s_ij, s_ji));
-        edge_slot[e] = own;
-        if (s_ij < 0 || s_ji < 0) {
+        int32_t oth = s_ij < 0 || s_ji < 0 ? -1 : max(s_ij, s_ji);
+        edge_hh[e] = make_int2(own, oth);
+        if (oth < 0) {
             atomicOr(bnd_word + (e >> 5), 1u << (e & 31));
             atomicAdd(scalars + 1, 1);
+            vbnd[i] = 1;
+            vbnd[j] = 1;
         }
     }
 }
@@ -142,7 +146,7 @@ __global__ void k_word_popc(const uint32_t *__restrict__ w, int32_t n, int32_t *
 __global__ void k_crease_lookup(const int32_t *__restrict__ crease, const float *__restrict__ sigma, int32_t K,
                                 const int32_t *__restrict__ face_vtx, const int32_t *__restrict__ vtx_off,
                                 const int32_t *__restrict__ vtx_slot, const int32_t *__restrict__ face_edge,
-                                const int32_t *__restrict__ face_twin, const int32_t *__restrict__ edge_slot, T0 tp,
+                                const int2 *__restrict__ edge_hh, T0 tp,
                                 int32_t V, float *__restrict__ edge_sigma, int32_t *__restrict__ edge_cidx,
                                 int32_t *flags) {
     int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -159,26 +163,26 @@ __global__ void k_crease_lookup(const int32_t *__restrict__ crease, const float 
     }
     if (e < 0) { atomicOr(flags, kFlagCrease); return; }
     if (atomicCAS(edge_cidx + e, -1, k) != -1) { atomicOr(flags, kFlagCrease); return; }
-    bool bnd = face_twin[edge_slot[e]] < 0;
+    bool bnd = edge_hh[e].y < 0;
     if (sg > 0.0f && !bnd) edge_sigma[e] = sg;  // boundary edges are infinitely sharp anyway
 }
 
-__global__ void k_special_flag(const int32_t *__restrict__ edge_slot, const int32_t *__restrict__ face_twin,
-                               const float *__restrict__ edge_sigma, int32_t E, int32_t *__restrict__ flag) {
+__global__ void k_special_flag(const int2 *__restrict__ edge_hh, const float *__restrict__ edge_sigma, int32_t E,
+                               int32_t *__restrict__ flag) {
     int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
-    flag[e] = (face_twin[edge_slot[e]] < 0 || edge_sigma[e] > 0.0f) ? 1 : 0;
+    flag[e] = (edge_hh[e].y < 0 || edge_sigma[e] > 0.0f) ? 1 : 0;
 }
 
-__global__ void k_special_fill(const int32_t *__restrict__ edge_slot, const int32_t *__restrict__ face_twin,
-                               const int32_t *__restrict__ face_vtx, const float *__restrict__ edge_sigma,
-                               const int32_t *__restrict__ flag, const int32_t *__restrict__ off, T0 tp, int32_t E,
-                               SpEdge *__restrict__ sp, int32_t *__restrict__ v_mark) {
+__global__ void k_special_fill(const int2 *__restrict__ edge_hh, const int32_t *__restrict__ face_vtx,
+                               const float *__restrict__ edge_sigma, const int32_t *__restrict__ flag,
+                               const int32_t *__restrict__ off, T0 tp, int32_t E, SpEdge *__restrict__ sp,
+                               int32_t *__restrict__ v_mark) {
     int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E || !flag[e]) return;
-    int32_t h = edge_slot[e];
+    int32_t h = edge_hh[e].x;
     int32_t va = face_vtx[h], vb = face_vtx[tp.next(h)];
-    bool bnd = face_twin[h] < 0;
+    bool bnd = edge_hh[e].y < 0;
     SpEdge s;
     s.e = e;
     s.a = min(va, vb);
@@ -199,11 +203,37 @@ __global__ void k_sv_fill(const int32_t *__restrict__ v_mark, const int32_t *__r
 }
 
 __global__ void k_sp_index(SpEdge *__restrict__ sp, const int32_t *__restrict__ count,
-                           const int32_t *__restrict__ v_idx, int32_t cap) {
+                           const int32_t *__restrict__ v_idx, int32_t cap, int32_t *__restrict__ sv_cnt) {
     int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= cap || j >= *count) return;
-    sp[j].ia = v_idx[sp[j].a];
-    sp[j].ib = v_idx[sp[j].b];
+    const int32_t ia = v_idx[sp[j].a], ib = v_idx[sp[j].b];
+    sp[j].ia = ia;
+    sp[j].ib = ib;
+    atomicAdd(sv_cnt + ia, 1);
+    atomicAdd(sv_cnt + ib, 1);
+}
+
+// special-vertex CSR: incident special edges of every special vertex, ascending
+__global__ void k_sv_list(const SpEdge *__restrict__ sp, const int32_t *__restrict__ count, int32_t cap,
+                          const int32_t *__restrict__ sv_off, int32_t *__restrict__ sv_cur, int32_t *__restrict__ sv_list) {
+    int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cap || j >= *count) return;
+    const int32_t ia = sp[j].ia, ib = sp[j].ib;
+    sv_list[sv_off[ia] + atomicAdd(sv_cur + ia, 1)] = j;
+    sv_list[sv_off[ib] + atomicAdd(sv_cur + ib, 1)] = j;
+}
+
+__global__ void k_sv_sort(const int32_t *__restrict__ nsv, int32_t cap, const int32_t *__restrict__ sv_off,
+                          int32_t *__restrict__ sv_list) {
+    int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cap || i >= *nsv) return;
+    const int32_t o = sv_off[i], n = sv_off[i + 1] - o;
+    for (int32_t a = 1; a < n; ++a) {
+        const int32_t x = sv_list[o + a];
+        int32_t b = a - 1;
+        while (b >= 0 && sv_list[o + b] > x) { sv_list[o + b + 1] = sv_list[o + b]; --b; }
+        sv_list[o + b + 1] = x;
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -240,10 +270,11 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     const int32_t nw = (int32_t)ceil_div(E > 0 ? E : 1, 32);
     cudaMemsetAsync(b.scalars + 1, 0, 3 * sizeof(int32_t), s);
     cudaMemsetAsync(b.bnd_word, 0, sizeof(uint32_t) * nw, s);
+    if (b.V > 0) cudaMemsetAsync(b.vbnd, 0, sizeof(int32_t) * b.V, s);
     if (b.V > 0) {
         k_edge_fill<<<grid_for(b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V, b.edge_off,
-                                                       b.face_edge, b.face_twin, b.edge_slot, b.bnd_word, b.scalars,
-                                                       b.flags);
+                                                       b.face_edge, b.face_twin, b.edge_hh, b.bnd_word, b.vbnd,
+                                                       b.scalars, b.flags);
         L.done("b0_edge_fill", s);
         k_slot0<<<grid_for(b.V), kThreads, 0, s>>>(b.vtx_off, b.vtx_slot, b.V, b.vtx_slot0);
         L.done("b0_slot0", s);
@@ -261,19 +292,19 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     }
     if (b.K_in > 0) {
         k_crease_lookup<<<grid_for(b.K_in), kThreads, 0, s>>>(b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off,
-                                                              b.vtx_slot, b.face_edge, b.face_twin, b.edge_slot, tp,
+                                                              b.vtx_slot, b.face_edge, b.edge_hh, tp,
                                                               b.V, b.edge_sigma, b.edge_cidx, b.flags);
         L.done("b0_crease_lookup", s);
     }
     if (E > 0) {
-        k_special_flag<<<grid_for(E), kThreads, 0, s>>>(b.edge_slot, b.face_twin, b.edge_sigma, E, b.sp_flag);
+        k_special_flag<<<grid_for(E), kThreads, 0, s>>>(b.edge_hh, b.edge_sigma, E, b.sp_flag);
         L.done("b0_special_flag", s);
     }
     scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, b.scratch, s, L);
     if (b.V > 0) cudaMemsetAsync(b.v_mark, 0, sizeof(int32_t) * b.V, s);
     if (E > 0 && b.sp) {
-        k_special_fill<<<grid_for(E), kThreads, 0, s>>>(b.edge_slot, b.face_twin, b.face_vtx, b.edge_sigma, b.sp_flag,
-                                                        b.sp_off, tp, E, b.sp, b.v_mark);
+        k_special_fill<<<grid_for(E), kThreads, 0, s>>>(b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp,
+                                                        E, b.sp, b.v_mark);
         L.done("b0_special_fill", s);
     }
     scan_exclusive(b.v_mark, b.v_idx, b.V, b.scalars + 3, b.scratch, s, L);
@@ -281,9 +312,22 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
         k_sv_fill<<<grid_for(b.V), kThreads, 0, s>>>(b.v_mark, b.v_idx, b.V, b.sv_vtx);
         L.done("b0_sv_fill", s);
     }
-    if (E > 0 && b.sp) {
-        k_sp_index<<<grid_for(E), kThreads, 0, s>>>(b.sp, b.scalars + 2, b.v_idx, E);
+    if (b.V > 0) {
+        cudaMemsetAsync(b.sv_cnt, 0, sizeof(int32_t) * b.V, s);
+        cudaMemsetAsync(b.sv_cur, 0, sizeof(int32_t) * b.V, s);
+    }
+    if (E > 0) {
+        k_sp_index<<<grid_for(E), kThreads, 0, s>>>(b.sp, b.scalars + 2, b.v_idx, E, b.sv_cnt);
         L.done("b0_sp_index", s);
+    }
+    scan_exclusive(b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V, b.scratch, s, L);
+    if (E > 0) {
+        k_sv_list<<<grid_for(E), kThreads, 0, s>>>(b.sp, b.scalars + 2, E, b.sv_off, b.sv_cur, b.sv_list);
+        L.done("b0_sv_list", s);
+    }
+    if (b.V > 0) {
+        k_sv_sort<<<grid_for(b.V), kThreads, 0, s>>>(b.scalars + 3, b.V, b.sv_off, b.sv_list);
+        L.done("b0_sv_sort", s);
     }
 }
 

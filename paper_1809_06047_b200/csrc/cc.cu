@@ -62,7 +62,6 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
             cft[t] = make_int4(tw[t] >= 0 ? 4 * twn + 3 : -1, 4 * (h0 + tn) + 2, 4 * hp + 1,
                                tw[tp] >= 0 ? 4 * tw[tp] : -1);
         }
-        c.vtx_slot0[V + r] = 4 * h0 + 2;
     }
 }
 
@@ -99,17 +98,17 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_gen(LevelDev p, ChildDev c
                 make_int4(twt >= 0 ? 4 * tp.next(twt) + 3 : -1, 4 * hn + 2, 4 * hp + 1, twp >= 0 ? 4 * twp : -1);
         }
     }
-    if constexpr (ADJ) c.vtx_slot0[V + r] = 4 * o + 2;
 }
 
 // ---------------- edge kernel ----------------
+// per parent edge e with pair (h = smallest slot, tw = the other or -1)
 template <int ORDER, bool ADJ, bool BND>
 __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Frames fr, bool topo) {
     const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= p.E) return;
     const Topo<ORDER> tp{p.face_off, p.slot_face};
-    const int32_t h = __ldg(p.edge_slot + e);
-    const int32_t tw = __ldg(p.face_twin + h);
+    const int2 hh = __ldg(p.edge_hh + e);
+    const int32_t h = hh.x, tw = hh.y;
     const int32_t hn = tp.next(h);
     const int32_t va = __ldg(p.face_vtx + h), vb = __ldg(p.face_vtx + hn);
     const int32_t V = p.V, F = p.F;
@@ -126,60 +125,160 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
     }
     if constexpr (ADJ) {
         if (!topo) return;
-        const int32_t base = cc_base<BND>(p.bnd_word, p.bnd_wpre, e);
+        // structured child edge ids: block [base, base + 4 - bnd) = (lo,ep), (hi,ep), (fp_min,ep), (fp_max,ep)
+        const int32_t bp = BND ? bprefix(p.bnd_word, p.bnd_wpre, e) : 0;
+        const int32_t base = 4 * e - bp;
         const int32_t h_ab = va < vb ? h : tw, h_ba = va < vb ? tw : h;
-        int32_t o0 = INT32_MAX, o1 = INT32_MAX;
-        if (h_ab >= 0) { o0 = 4 * h_ab; o1 = 4 * tp.next(h_ab) + 3; }
-        if (h_ba >= 0) { o0 = min(o0, 4 * tp.next(h_ba) + 3); o1 = min(o1, 4 * h_ba); }
-        c.edge_slot[base + 0] = o0;
-        c.edge_slot[base + 1] = o1;
-        c.edge_slot[base + 2] = min(4 * h + 1, 4 * hn + 2);
-        if (tw >= 0) c.edge_slot[base + 3] = min(4 * tw + 1, 4 * tp.next(tw) + 2);
-        c.vtx_slot0[V + F + e] = 4 * h + 1;
+        // child half-edges: (lo,ep): lo->ep = 4 h_ab, ep->lo = 4 next(h_ba) + 3; (hi,ep) symmetric
+        const int32_t a0 = h_ab >= 0 ? 4 * h_ab : -1, a1 = h_ba >= 0 ? 4 * tp.next(h_ba) + 3 : -1;
+        const int32_t b0 = h_ba >= 0 ? 4 * h_ba : -1, b1 = h_ab >= 0 ? 4 * tp.next(h_ab) + 3 : -1;
+        auto pair = [](int32_t x, int32_t y) {
+            if (x < 0) return make_int2(y, -1);
+            if (y < 0) return make_int2(x, -1);
+            return make_int2(min(x, y), max(x, y));
+        };
+        c.edge_hh[base + 0] = pair(a0, a1);
+        c.edge_hh[base + 1] = pair(b0, b1);
+        c.edge_hh[base + 2] = pair(4 * h + 1, 4 * hn + 2);  // (fp of face(h), ep); h < tw
+        if (tw >= 0) c.edge_hh[base + 3] = pair(4 * tw + 1, 4 * tp.next(tw) + 2);
         if constexpr (BND) {
+            // child boundary bits and, in closed form, the child per-word prefix:
+            // bprefix'(base + k) = 2 bprefix(e) + bnd_e min(k, 2)
+            const int32_t nch = tw < 0 ? 3 : 4;
             if (tw < 0) {
                 atomicOr(c.bnd_word + (base >> 5), 1u << (base & 31));
                 atomicOr(c.bnd_word + ((base + 1) >> 5), 1u << ((base + 1) & 31));
+            }
+            const int32_t w = (base + 31) >> 5;
+            if (32 * w < base + nch) {
+                const int32_t k = 32 * w - base;
+                c.bnd_wpre[w] = 2 * bp + (tw < 0 ? min(k, 2) : 0);
             }
         }
     }
 }
 
-// ---------------- vertex kernel: 1-ring walk ----------------
-template <int ORDER, bool ADJ>
-__global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, ChildDev c, Frames fr, bool topo) {
-    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= p.V) return;
-    const Topo<ORDER> tp{p.face_off, p.slot_face};
-    const int32_t h0 = __ldg(p.vtx_slot0 + v);
-    if constexpr (ADJ) {
-        if (topo) c.vtx_slot0[v] = h0 >= 0 ? 4 * h0 : -1;  // corner 0 of child face h0
+// ---------------- vertex kernel: class-structured incident slots ----------------
+// S(p) = (1 - 2/n) p + 1/n^2 sum_{incident slots x} (p_{v(next(x))} + f_{face(x)})
+// (Eq. pos_update split: s2 = F P and s3 = M f as gathers over M's row of p).
+// The row of M of a level-l vertex is closed-form from the level it was born at (VSegs):
+//   level-0 vertex v : 4^l x its level-0 slots (M^T from the radix sort)
+//   face point of face r of level m-1 : 4^(l-m) x {4 (off_r + t) + 2}
+//   edge point of edge (h, tw) of level m-1 : 4^(l-m) x {4h+1, 4 next(h)+3, 4tw+1, 4 next(tw)+3}
+// so no twin walk (no dependent chain) is needed; all loads of a vertex are issued together.
+template <int ORDER>
+struct VtxCtx {
+    const int32_t *face_vtx;
+    Topo<ORDER> tl;
+    int32_t V;
+};
+
+// accumulate the smooth point of v over nx slots for every frame
+template <int ORDER, int N>
+ALSUB_D void smooth_fixed(const VtxCtx<ORDER> &x, const Frames &fr, int32_t v, const int32_t (&sl)[N]) {
+    int32_t nb[N], fc[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        nb[k] = __ldg(x.face_vtx + x.tl.next(sl[k]));
+        fc[k] = x.V + x.tl.face(sl[k]);
     }
-    const int32_t V = p.V;
+    constexpr float inv = 1.0f / (float)N;
     for (int f = 0; f < fr.nb; ++f) {
         const float *P = fr.P + f * fr.Pstride;
         float *Pn = fr.Pn + f * fr.Pnstride;
-        const P3 pv = ld3(P, v);
-        if (h0 < 0) { st3(Pn, v, pv); continue; }
+        P3 acc = ld3(P, nb[0]) + ld3c(Pn, fc[0]);
+#pragma unroll
+        for (int k = 1; k < N; ++k) acc = acc + ld3(P, nb[k]) + ld3c(Pn, fc[k]);
+        st3(Pn, v, (1.0f - 2.0f * inv) * ld3(P, v) + (inv * inv) * acc);
+    }
+}
+
+template <int ORDER>
+ALSUB_D void smooth_list(const VtxCtx<ORDER> &x, const Frames &fr, int32_t v, const int32_t *list, int32_t n,
+                         int shift, bool quad_fp, int32_t off) {
+    for (int f = 0; f < fr.nb; ++f) {
+        const float *P = fr.P + f * fr.Pstride;
+        float *Pn = fr.Pn + f * fr.Pnstride;
         P3 acc = p3zero();
-        int32_t h = h0, n = 0;
-        bool bnd = false;
-        do {
-            acc = acc + ld3(P, __ldg(p.face_vtx + tp.next(h))) + ld3c(Pn, V + tp.face(h));
-            ++n;
-            h = __ldg(p.face_twin + tp.prev(h));
-            if (h < 0) { bnd = true; break; }
-        } while (h != h0 && n < p.S);
-        if (bnd) { st3(Pn, v, pv); continue; }  // boundary: set by the crease/boundary override
+        for (int32_t k = 0; k < n; ++k) {
+            const int32_t s = quad_fp ? ((4 * (off + k) + 2) << shift) : (__ldg(list + k) << shift);
+            acc = acc + ld3(P, __ldg(x.face_vtx + x.tl.next(s))) + ld3c(Pn, x.V + x.tl.face(s));
+        }
+        const P3 pv = ld3(P, v);
+        if (n == 0) { st3(Pn, v, pv); continue; }
         const float inv = 1.0f / (float)n;
         st3(Pn, v, (1.0f - 2.0f * inv) * pv + (inv * inv) * acc);
     }
 }
 
+ALSUB_D void copy_point(const Frames &fr, int32_t v) {
+    for (int f = 0; f < fr.nb; ++f) st3(fr.Pn + f * fr.Pnstride, v, ld3(fr.P + f * fr.Pstride, v));
+}
+
+template <int ORDER>
+__global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, VSegs g) {
+    __shared__ int32_t s_lo[kMaxSeg], s_pre[kMaxSeg + 1];
+    const int64_t nblk = gridDim.x, b = blockIdx.x;
+    if (threadIdx.x < g.nseg) {
+        const int64_t len = g.len[threadIdx.x];
+        s_lo[threadIdx.x] = (int32_t)(b * len / nblk);
+        s_pre[threadIdx.x] = (int32_t)((b + 1) * len / nblk) - (int32_t)(b * len / nblk);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t acc = 0;
+        for (int s = 0; s < g.nseg; ++s) {
+            const int32_t c = s_pre[s];
+            s_pre[s] = acc;
+            acc += c;
+        }
+        s_pre[g.nseg] = acc;
+    }
+    __syncthreads();
+    const VtxCtx<ORDER> x{p.face_vtx, Topo<ORDER>{p.face_off, p.slot_face}, p.V};
+    const int32_t total = s_pre[g.nseg];
+    int s = 0;
+    for (int32_t i = threadIdx.x; i < total; i += blockDim.x) {
+        while (s_pre[s + 1] <= i) ++s;  // items ascend: the segment index only moves forward
+        const int32_t j = s_lo[s] + (i - s_pre[s]);
+        const int32_t v = g.start[s] + j;
+        const int shift = 2 * (g.level - g.birth[s]);
+        const int type = g.type[s];
+        const int m1 = g.birth[s] - 1;
+        if (type == 2) {  // edge point born at level m1 + 1
+            const int2 hh = __ldg(g.ehh[m1] + j);
+            if (hh.y < 0) { copy_point(fr, v); continue; }  // boundary: crease module
+            int32_t nh, nt;
+            if (m1 == 0) {
+                const Topo<0> t0{g.face_off0, g.slot_face0};
+                nh = t0.next(hh.x);
+                nt = t0.next(hh.y);
+            } else {
+                nh = (hh.x & ~3) | ((hh.x + 1) & 3);
+                nt = (hh.y & ~3) | ((hh.y + 1) & 3);
+            }
+            const int32_t sl[4] = {(4 * hh.x + 1) << shift, (4 * nh + 3) << shift, (4 * hh.y + 1) << shift,
+                                   (4 * nt + 3) << shift};
+            smooth_fixed<ORDER, 4>(x, fr, v, sl);
+        } else if (type == 1 && m1 > 0) {  // face point of a quad
+            const int32_t sl[4] = {(16 * j + 2) << shift, (16 * j + 6) << shift, (16 * j + 10) << shift,
+                                   (16 * j + 14) << shift};
+            smooth_fixed<ORDER, 4>(x, fr, v, sl);
+        } else if (type == 1) {  // face point of a level-0 face (any order)
+            const int32_t off = __ldg(g.face_off0 + j), cnt = __ldg(g.face_off0 + j + 1) - off;
+            smooth_list<ORDER>(x, fr, v, nullptr, cnt, shift, true, off);
+        } else {  // level-0 vertex
+            if (__ldg(g.vbnd0 + j)) { copy_point(fr, v); continue; }
+            const int32_t o = __ldg(g.vtx_off0 + j), cnt = __ldg(g.vtx_off0 + j + 1) - o;
+            smooth_list<ORDER>(x, fr, v, g.vtx_list0 + o, cnt, shift, false, 0);
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 template <int ORDER, bool ADJ, bool BND>
-static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, cudaStream_t s,
-                      Launches &L) {
+static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, const VSegs &g,
+                      cudaStream_t s, Launches &L) {
     if (p.F > 0) {
         if constexpr (ORDER == 4) k_cc_face_quad<ADJ, BND><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
         else k_cc_face_gen<ORDER, ADJ, BND><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
@@ -190,38 +289,35 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bo
         L.done("cc_edge", s);
     }
     if (p.V > 0) {
-        k_cc_vertex<ORDER, ADJ><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr, topo);
+        const unsigned nblk = grid_for(p.V, 4 * kThreads);
+        if constexpr (ORDER == 4) k_cc_vertex<4><<<nblk, kThreads, 0, s>>>(p, fr, g);
+        else k_cc_vertex<0><<<nblk, kThreads, 0, s>>>(p, fr, g);
         L.done("cc_vertex", s);
     }
 }
 
 template <int ORDER>
-static void cc_dispatch(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, cudaStream_t s,
-                        Launches &L) {
+static void cc_dispatch(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &g,
+                        cudaStream_t s, Launches &L) {
     const bool bnd = p.B > 0;
     if (adj && topo) {
-        if (bnd) cc_launch<ORDER, true, true>(p, c, fr, topo, s, L);
-        else cc_launch<ORDER, true, false>(p, c, fr, topo, s, L);
+        if (bnd) cc_launch<ORDER, true, true>(p, c, fr, topo, g, s, L);
+        else cc_launch<ORDER, true, false>(p, c, fr, topo, g, s, L);
     } else {
-        cc_launch<ORDER, false, false>(p, c, fr, topo, s, L);
+        cc_launch<ORDER, false, false>(p, c, fr, topo, g, s, L);
     }
 }
 
-void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
+void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &g,
               cudaStream_t s, Launches &L) {
-    (void)scratch;
-    const bool need_mask = adj && topo && p.B > 0;
-    if (need_mask) {
+    if (adj && topo && p.B > 0) {
         const int32_t nw = (int32_t)ceil_div(c.E > 0 ? c.E : 1, 32);
         cudaMemsetAsync(c.bnd_word, 0, sizeof(uint32_t) * nw, s);
     }
-    if (p.order == 4) cc_dispatch<4>(p, c, fr, topo, adj, s, L);
-    else if (p.order == 3) cc_dispatch<3>(p, c, fr, topo, adj, s, L);
-    else cc_dispatch<0>(p, c, fr, topo, adj, s, L);
-    if (need_mask) {
-        const int32_t nw = (int32_t)ceil_div(c.E > 0 ? c.E : 1, 32);
-        bnd_prefix(c.bnd_word, c.bnd_wcnt, c.bnd_wpre, nw, scratch, s, L);
-    }
+    // level-0 meshes of uniform order use the generic kernels too (their M^T comes from the sort);
+    // levels >= 1 are reduced quad matrices
+    if (p.order == 4 && p.face_off == nullptr) cc_dispatch<4>(p, c, fr, topo, adj, g, s, L);
+    else cc_dispatch<0>(p, c, fr, topo, adj, g, s, L);
 }
 
 }  // namespace alsub

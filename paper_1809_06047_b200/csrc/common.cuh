@@ -7,9 +7,10 @@
 //   and a slot_face[S] table.
 //   face_edge[h]  id of the edge v(h) -> v(next(h))       (E's enumeration)
 //   face_twin[h]  slot of the reverse directed edge or -1 (F(j,i) of Eq. F)
-//   edge_slot[e]  smallest slot carrying edge e
-//   vtx_slot0[v]  one slot at vertex v (-1 = isolated); the 1-ring is walked with
-//                 next-around(h) = twin(prev(h))  (the rows of M, i.e. M^T's CSR, on demand)
+//   edge_hh[e]    (smallest slot carrying edge e, the other slot or -1 on a boundary)
+//   vtx_slot0[v]  (Loop / sqrt3) one slot at vertex v; the 1-ring is walked with
+//                 next-around(h) = twin(prev(h)).  CC derives each vertex's row of M in closed
+//                 form from the level the vertex was born at (VSegs in internal.h).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -83,28 +84,22 @@ ALSUB_D int32_t bprefix(const uint32_t *__restrict__ words, const int32_t *__res
 }
 
 // Special (boundary or creased) edge of a level: boundary edges are infinitely sharp creases
-// (reading R6).  Sorted by edge id.  ia/ib index the level's special-vertex table.
+// (reading R6).  Level l's list has K_l = 2^l K_0 entries in edge-id order; entry j's children
+// are entries 2j (endpoint a) and 2j + 1 (endpoint b) of the next level -- dead children keep
+// sigma = 0, so the list never needs compaction and every index is closed-form.
 struct SpEdge {
-    int32_t e, a, b, ia, ib;   // a < b
-    float sigma;               // > 0, +inf for boundary / infinitely sharp
-    int32_t flags;             // bit 0: boundary
+    int32_t e, a, b;   // edge id, endpoints a < b
+    int32_t ia, ib;    // special-vertex indices of a and b
+    float sigma;       // 0 = dead, > 0, +inf for boundary / infinitely sharp
+    int32_t flags;     // bit 0: boundary
     int32_t pad;
 };
 constexpr int32_t kSpBoundary = 1;
 
-// Per special vertex accumulators: crease valency k and sharpness s (Eqs. CC_crease_valency /
-// CC_crease_vsharpness, fused as in P:L676-681), the first two sharp neighbours,
-// and the finite-crease sums used by sharpness inheritance (reading R8).
-struct SvAcc {
-    int32_t k;
-    int32_t nfin;
-    float finsum;
-    float sum;
-    int32_t inf;
-    int32_t nb0, nb1;
-    float s;
-};
-
+// Special-vertex table of a level: vertex ids sv_vtx[i] with their incident special edges
+// sv_list[sv_off[i] .. sv_off[i+1]) (CSR).  The next level keeps the same vertices with the same
+// list lengths (entry j -> 2j + (vertex is b_j)) and appends one vertex per special edge (its edge
+// point) with the two entries {2j, 2j + 1}.
 // Device-side status flags written by the level-0 build (read back by alsub_mesh_create).
 enum : int32_t {
     kFlagMesh = 1, kFlagNonManifold = 2, kFlagCrease = 4, kFlagOrder = 8,

@@ -64,7 +64,9 @@ struct Build0 {
     int32_t *sort_k, *sort_v, *sort_k2, *sort_v2;  // [S]
     int32_t *vtx_off, *vtx_slot;  // [V+1], [S] (M^T in CSR)
     int32_t *edge_cnt, *edge_off; // [V], [V]
-    int32_t *face_edge, *face_twin, *edge_slot, *vtx_slot0;  // [S], [S], [E], [V]
+    int32_t *face_edge, *face_twin, *vtx_slot0;  // [S], [S], [V]
+    int2 *edge_hh;                // [E] (smallest slot of the edge, the other slot or -1)
+    int32_t *vbnd;                // [V] 1 = vertex on a boundary edge
     uint32_t *bnd_word;           // [ceil(E/32)]
     int32_t *bnd_wcnt, *bnd_wpre; // [ceil(E/32)]
     float *edge_sigma;            // [E]
@@ -73,6 +75,7 @@ struct Build0 {
     int32_t *v_mark, *v_idx;      // [V]
     SpEdge *sp;                   // [cap] special edges
     int32_t *sv_vtx;              // [cap] special vertices
+    int32_t *sv_cnt, *sv_off, *sv_cur, *sv_list;  // special-vertex CSR (level 0)
     int32_t *flags;               // device status flags
     int32_t *scalars;             // device scalars: [0] E, [1] B, [2] K special, [3] NSV
     int32_t E;                    // host-known after the count pass (create) or plan (refine)
@@ -87,29 +90,25 @@ struct LevelDev {
     int32_t V, F, S, E, B;  // parent counts
     int order;              // 0, 3, 4
     const int32_t *face_off, *slot_face;  // order 0
-    const int32_t *face_vtx, *face_edge, *face_twin, *edge_slot, *vtx_slot0;
+    const int32_t *face_vtx, *face_edge, *face_twin, *vtx_slot0;
+    const int2 *edge_hh;       // [E] (owner slot = smallest, twin slot or -1)
     const uint32_t *bnd_word;
     const int32_t *bnd_wpre;
     const int32_t *loop_base;  // Loop: [E] exclusive scan of child-edge counts
-    // special lists of the parent level
+    // special lists of the parent level (host-known sizes)
     const SpEdge *sp;
-    const int32_t *sp_count;   // device scalar
-    int32_t sp_cap;
-    const int32_t *sv_vtx;     // shared growing table
-    const int32_t *sv_count;   // device scalar (this level)
-    SvAcc *sva;                // [sv_cap] accumulators of this level
-    int32_t sv_cap;
+    int32_t nsp;
+    const int32_t *sv_vtx, *sv_off, *sv_list;
+    int32_t nsv;
 };
 struct ChildDev {
     int32_t V, F, S, E;  // child counts
-    int32_t *face_vtx, *face_edge, *face_twin, *edge_slot, *vtx_slot0;
+    int32_t *face_vtx, *face_edge, *face_twin, *vtx_slot0;
+    int2 *edge_hh;
     uint32_t *bnd_word;
-    int32_t *bnd_wcnt, *bnd_wpre;
+    int32_t *bnd_wpre;
     SpEdge *sp;
-    int32_t *sp_count;
-    int32_t sp_cap;
-    int32_t *sv_vtx;
-    int32_t *sv_count;
+    int32_t *sv_vtx, *sv_off, *sv_list;
 };
 
 // positions: P [nb][V][3] (frame stride Pstride floats), Pn [nb][V'][3]
@@ -120,26 +119,37 @@ struct Frames {
     int nb;
 };
 
+// Vertex-id segments of a CC level: level-l vertex ids are
+// [orig V0 | fp(1) F0 | ep(1) E0 | fp(2) F1 | ep(2) E1 | ... | fp(l) F_{l-1} | ep(l) E_{l-1}].
+// A vertex born at level m has its level-l incident slots = 4^(l-m) x its level-m slots, which
+// are closed-form in the level-(m-1) tables.  The vertex kernel interleaves all segments so a
+// block touches one spatial band of the mesh.
+constexpr int kMaxLevels = 16;
+constexpr int kMaxSeg = 2 * kMaxLevels + 1;
+struct VSegs {
+    int32_t nseg, level;
+    int32_t start[kMaxSeg], len[kMaxSeg];
+    int8_t type[kMaxSeg];   // 0 = level-0 vertex, 1 = face point, 2 = edge point
+    int8_t birth[kMaxSeg];  // level m at which the vertex was created
+    const int2 *ehh[kMaxLevels];  // ehh[m-1] = edge pairs of level m-1
+    const int32_t *vtx_off0, *vtx_list0, *face_off0, *slot_face0, *vbnd0;
+};
+
 // mode: adj = emit child adjacency (not the last level); topo = emit child faces;
 //       acc = accumulate crease valency/sharpness (refine) vs reuse stored (eval_frames)
-void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
+void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &segs,
               cudaStream_t s, Launches &L);
 void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
                 cudaStream_t s, Launches &L);
 void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
                  cudaStream_t s, Launches &L);
-// crease / boundary overrides and inheritance (crease.cu); ep_base = first edge-point id.
-void crease_eval(const LevelDev &p, const Frames &fr, int32_t ep_base, bool accumulate, cudaStream_t s,
-                 Launches &L);
-void crease_inherit(const LevelDev &p, const ChildDev &c, int scheme, int32_t ep_base, int32_t *cnt,
-                    int32_t *off, void *scratch, cudaStream_t s, Launches &L);
+// crease / boundary module (crease.cu): ONE kernel per level -- edge and vertex overrides and
+// (inherit) the child special lists.  ep_base = first edge-point id; scheme 0 CC, 1 Loop.
+void crease_level(const LevelDev &p, const ChildDev &c, const Frames &fr, int32_t ep_base, int scheme, bool inherit,
+                  cudaStream_t s, Launches &L);
 // Loop child-edge counts -> loop_base (scan); cnt [E] scratch
 void loop_edge_base(const LevelDev &p, int32_t *cnt, int32_t *base, void *scratch, cudaStream_t s, Launches &L);
-// Boundary-edge word prefix of a level (bnd_wcnt -> bnd_wpre)
-void bnd_prefix(uint32_t *words, int32_t *wcnt, int32_t *wpre, int32_t nwords, void *scratch, cudaStream_t s,
-                Launches &L);
-
-// topology export helper: edge_vtx / edge_face from edge_slot + face_twin
+// topology export helper: edge_vtx / edge_face from the edge pairs
 void export_edges(const LevelDev &p, int32_t *edge_vtx, int32_t *edge_face, cudaStream_t s, Launches &L);
 
 }  // namespace alsub

@@ -56,7 +56,8 @@ ALSUB_D void other_edges(const int32_t *face_edge, int32_t h, int32_t &x, int32_
 __global__ void __launch_bounds__(kThreads) k_loop_count(LevelDev p, int32_t *__restrict__ cnt) {
     const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= p.E) return;
-    const int32_t h = __ldg(p.edge_slot + e), tw = __ldg(p.face_twin + h);
+    const int2 hh = __ldg(p.edge_hh + e);
+    const int32_t h = hh.x, tw = hh.y;
     int32_t n[4];
     other_edges(p.face_edge, h, n[0], n[1]);
     n[2] = n[3] = INT32_MAX;
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) k_loop_face(LevelDev p, ChildDev c) 
             cft[3 * t + 0] = a >= 0 ? 3 * (4 * (a / 3) + (a % 3 + 1) % 3) + 2 : -1;
             cft[3 * t + 1] = 3 * (4 * r + 3) + tp;
             cft[3 * t + 2] = b >= 0 ? 3 * (4 * (b / 3) + b % 3) + 0 : -1;
-            c.edge_slot[inner_t_tm1[t]] = 12 * r + 3 * t + 1;
+            c.edge_hh[inner_t_tm1[t]] = make_int2(12 * r + 3 * t + 1, 3 * (4 * r + 3) + tp);
         }
         cfe[9] = in01;
         cfe[10] = in12;
@@ -158,7 +159,8 @@ template <bool ADJ>
 __global__ void __launch_bounds__(kThreads) k_loop_edge(LevelDev p, ChildDev c, Frames fr) {
     const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= p.E) return;
-    const int32_t h = __ldg(p.edge_slot + e), tw = __ldg(p.face_twin + h);
+    const int2 hh = __ldg(p.edge_hh + e);
+    const int32_t h = hh.x, tw = hh.y;
     const int32_t va = __ldg(p.face_vtx + h), vb = __ldg(p.face_vtx + tri_next(h));
     const int32_t g1 = __ldg(p.face_vtx + tri_prev(h));
     const int32_t g2 = tw >= 0 ? __ldg(p.face_vtx + tri_prev(tw)) : -1;
@@ -172,11 +174,14 @@ __global__ void __launch_bounds__(kThreads) k_loop_edge(LevelDev p, ChildDev c, 
     if constexpr (ADJ) {
         const int32_t base = __ldg(p.loop_base + e);
         const int32_t h_ab = va < vb ? h : tw, h_ba = va < vb ? tw : h;
-        int32_t o0 = INT32_MAX, o1 = INT32_MAX;
-        if (h_ab >= 0) { o0 = loop_c0(h_ab); o1 = loop_c2next(h_ab); }
-        if (h_ba >= 0) { o0 = min(o0, loop_c2next(h_ba)); o1 = min(o1, loop_c0(h_ba)); }
-        c.edge_slot[base + 0] = o0;
-        c.edge_slot[base + 1] = o1;
+        auto pair = [](int32_t x, int32_t y) {
+            if (x < 0) return make_int2(y, -1);
+            if (y < 0) return make_int2(x, -1);
+            return make_int2(min(x, y), max(x, y));
+        };
+        // (lo,ep): lo->ep in the child of h_ab, ep->lo in the child after h_ba; (hi,ep) symmetric
+        c.edge_hh[base + 0] = pair(h_ab >= 0 ? loop_c0(h_ab) : -1, h_ba >= 0 ? loop_c2next(h_ba) : -1);
+        c.edge_hh[base + 1] = pair(h_ba >= 0 ? loop_c0(h_ba) : -1, h_ab >= 0 ? loop_c2next(h_ab) : -1);
         c.vtx_slot0[V + e] = loop_c0(h) + 1;
     }
 }
