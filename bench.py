@@ -51,22 +51,27 @@ def level_counts(m, levels):
     out = []
     for l in range(levels + 1):
         c = m.counts(l)
-        out.append(dict(V=c["verts"], F=c["faces"], S=c["face_slots"], E=c["edges"]))
+        out.append(dict(V=c["verts"], F=c["faces"], S=c["face_slots"], E=c["edges"], level=l))
     return out
 
 
-def kernel_bytes_cc(name, c, adj):
-    """Algorithmic bytes of one launch of a CC level kernel; c = parent counts."""
+def kernel_bytes_cc(name, c, adj, prev=None):
+    """Algorithmic bytes of one launch of a CC level kernel: every array the
+    kernel reads or writes, counted once.  c = counts of the parent level l, prev = level l-1."""
     V, F, S, E = c["V"], c["F"], c["S"], c["E"]
+    Fp = prev["F"] if prev else 0           # face points born at level l (smoothed by cc_face, l >= 2)
+    Ep = prev["E"] if prev else 0
+    fpv = prev is not None and c.get("level", 0) >= 2
     if name == "cc_face":
-        rd = 4 * S + 4 * S + 12 * V + (4 * S if adj else 0)            # face_vtx, face_edge, P (+face_twin)
-        wr = 12 * F + 16 * S + ((16 * S + 16 * S + 4 * F) if adj else 0)  # f, child faces (+face_edge', face_twin', slot0')
+        rd = 4 * S + 4 * S + 12 * V + (4 * S if adj else 0)               # face_vtx, face_edge, P (+face_twin)
+        wr = 12 * F + 16 * S + ((16 * S + 16 * S) if adj else 0)          # f, child faces (+face_edge', face_twin')
+        wr += 12 * Fp if fpv else 0                                          # vertex points of the new face points
     elif name == "cc_edge":
-        rd = 4 * E + 4 * S + 4 * E + 12 * V + 12 * F                     # edge_slot, face_vtx, face_twin[owner], P, f
-        wr = 12 * E + ((4 * (2 * E + S) + 4 * E) if adj else 0)           # e (+edge_slot', slot0')
+        rd = 8 * E + 4 * S + 12 * V + 12 * F                                # edge pairs, face_vtx rows, P, f
+        wr = 12 * E + (8 * (2 * E + S) if adj else 0)                        # e (+ child edge pairs)
     elif name == "cc_vertex":
-        rd = 4 * V + 4 * S + 4 * S + 12 * V + 12 * F                     # slot0, face_vtx, face_twin, P, f
-        wr = 12 * V + (4 * V if adj else 0)
+        rd = 4 * S + 12 * V + 12 * F + 8 * Ep                               # face_vtx, P, f, birth edge pairs
+        wr = 12 * (V - (Fp if fpv else 0))
     else:
         return None
     return rd + wr
@@ -285,14 +290,15 @@ def run_alsub(args):
             row["survey_frac"] = row["survey_GBps"] / peak if row["survey_GBps"] else None
             kk = {}
             for n, t in ks.items():
-                b = kernel_bytes_cc(n, c, not final)
+                b = kernel_bytes_cc(n, c, not final, cnt[lvl - 1] if lvl > 0 else None)
                 kk[n] = {"ms": t, "alg_bytes": b, "GBps": (b / (t * 1e6)) if b else None,
                          "frac": (b / (t * 1e6) / peak) if b else None}
             row["kernels"] = kk
         per_level.append(row)
     # dominant kernel = the largest share of the step
     (dname, dlvl), dms = max(kt.items(), key=lambda kv: kv[1])
-    dbytes = kernel_bytes_cc(dname, cnt[dlvl], dlvl < levels - 1) if dlvl >= 0 else None
+    dbytes = kernel_bytes_cc(dname, cnt[dlvl], dlvl < levels - 1, cnt[dlvl - 1] if dlvl > 0 else None) \
+        if dlvl >= 0 else None
     achieved = dbytes / (dms * 1e6) if dbytes else None
     traffic = None
     prof_sum = os.path.join(ROOT, "profiles", "ncu_summary.json")

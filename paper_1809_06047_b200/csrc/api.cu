@@ -427,7 +427,9 @@ static VSegs make_segs(alsub_mesh *m, int l) {
     g.start[n] = 0; g.len[n] = m->V0; g.type[n] = 0; g.birth[n] = 0; ++n;
     for (int k = 1; k <= l; ++k) {
         const LevelHost &q = m->lv[k - 1];
-        g.start[n] = (int32_t)q.V; g.len[n] = (int32_t)q.F; g.type[n] = 1; g.birth[n] = (int8_t)k; ++n;
+        // face points born at this level (k == l >= 2) are smoothed inside the face kernel
+        g.start[n] = (int32_t)q.V; g.len[n] = (k == l && l >= 2) ? 0 : (int32_t)q.F; g.type[n] = 1;
+        g.birth[n] = (int8_t)k; ++n;
         g.start[n] = (int32_t)(q.V + q.F); g.len[n] = (int32_t)q.E; g.type[n] = 2; g.birth[n] = (int8_t)k; ++n;
         g.ehh[k - 1] = q.edge_hh;
     }

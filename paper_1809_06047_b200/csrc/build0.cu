@@ -54,20 +54,72 @@ struct Cand {
     }
 };
 
+// Warp-per-vertex collision processing: lane q < 2n holds candidate q of vertex j (slot q/2,
+// neighbour next (q even) or prev (q odd)); duplicates are found with __match_any_sync and the
+// rank of a distinct neighbour among the distinct neighbours < j with a ballot per lane.
+// Vertices with more than 16 incident faces fall back to a serial loop on lane 0.
+struct WarpCand {
+    int32_t x;     // neighbour vertex (INT32_MAX = none)
+    int32_t slot;  // the slot of the directed edge (j -> x for next, x -> j for prev)
+    bool first;    // first occurrence of x among the candidates
+    unsigned peers;
+};
+
+ALSUB_D WarpCand warp_cand(const int32_t *face_vtx, const int32_t *vtx_slot, T0 tp, int32_t o0, int32_t n, int lane) {
+    WarpCand c{INT32_MAX, -1, false, 0u};
+    if (lane < 2 * n) {
+        const int32_t h = __ldg(vtx_slot + o0 + (lane >> 1));
+        if (lane & 1) {
+            const int32_t hp = tp.prev(h);
+            c.x = __ldg(face_vtx + hp);
+            c.slot = hp;
+        } else {
+            c.x = __ldg(face_vtx + tp.next(h));
+            c.slot = h;
+        }
+    }
+    c.peers = __match_any_sync(0xffffffffu, c.x);
+    c.first = c.x != INT32_MAX && (__ffs(c.peers) - 1) == lane;
+    return c;
+}
+
 // symbolic pass: number of distinct neighbours i < j of vertex j (non-zeros of E's column j above
 // the diagonal)
 __global__ void k_edge_count(const int32_t *__restrict__ face_vtx, const int32_t *__restrict__ vtx_off,
                              const int32_t *__restrict__ vtx_slot, T0 tp, int32_t V, int32_t *__restrict__ cnt) {
-    int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t j = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (j >= V) return;
-    Cand cd{face_vtx, vtx_slot, tp, vtx_off[j]};
-    int32_t nq = 2 * (vtx_off[j + 1] - cd.o0);
-    int32_t c = 0;
-    for (int32_t q = 0; q < nq; ++q) {
-        int32_t x = cd.vert(q);
-        if (x < j && cd.first(q, x)) ++c;
+    const int32_t o0 = vtx_off[j], n = vtx_off[j + 1] - o0;
+    if (n <= 16) {
+        const WarpCand c = warp_cand(face_vtx, vtx_slot, tp, o0, n, lane);
+        const unsigned b = __ballot_sync(0xffffffffu, c.first && c.x < j);
+        if (lane == 0) cnt[j] = __popc(b);
+        return;
     }
-    cnt[j] = c;
+    if (lane != 0) return;
+    Cand cd{face_vtx, vtx_slot, tp, o0};
+    int32_t k = 0;
+    for (int32_t q = 0; q < 2 * n; ++q) {
+        int32_t x = cd.vert(q);
+        if (x < j && cd.first(q, x)) ++k;
+    }
+    cnt[j] = k;
+}
+
+ALSUB_D void emit_edge(int32_t e, int32_t s_ij, int32_t s_ji, int32_t i, int32_t j, int32_t *face_edge, int32_t *face_twin,
+                       int2 *edge_hh, uint32_t *bnd_word, int32_t *vbnd, int32_t *scalars) {
+    if (s_ij >= 0) { face_edge[s_ij] = e; face_twin[s_ij] = s_ji; }
+    if (s_ji >= 0) { face_edge[s_ji] = e; face_twin[s_ji] = s_ij; }
+    const int32_t own = s_ij < 0 ? s_ji : (s_ji < 0 ? s_ij : min(s_ij, s_ji));
+    const int32_t oth = s_ij < 0 || s_ji < 0 ? -1 : max(s_ij, s_ji);
+    edge_hh[e] = make_int2(own, oth);
+    if (oth < 0) {
+        atomicOr(bnd_word + (e >> 5), 1u << (e & 31));
+        atomicAdd(scalars + 1, 1);
+        vbnd[i] = 1;
+        vbnd[j] = 1;
+    }
 }
 
 // numeric pass: ids, F(i,j) / F(j,i) as twin slots, multiplicity checks, boundary bits
@@ -77,20 +129,42 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
                             int32_t *__restrict__ face_twin, int2 *__restrict__ edge_hh,
                             uint32_t *__restrict__ bnd_word, int32_t *__restrict__ vbnd,
                             int32_t *__restrict__ scalars, int32_t *flags) {
-    int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t j = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (j >= V) return;
-    Cand cd{face_vtx, vtx_slot, tp, vtx_off[j]};
-    const int32_t n = vtx_off[j + 1] - cd.o0, nq = 2 * n;
+    const int32_t o0 = vtx_off[j], n = vtx_off[j + 1] - o0;
+    if (n <= 16) {
+        const WarpCand c = warp_cand(face_vtx, vtx_slot, tp, o0, n, lane);
+        const bool mine = c.first && c.x < j;
+        int32_t rank = 0;
+        for (int k = 0; k < 32; ++k) {
+            const int32_t xk = __shfl_sync(0xffffffffu, c.x, k);
+            const unsigned b = __ballot_sync(0xffffffffu, c.first && c.x < xk);
+            if (lane == k) rank = __popc(b);
+        }
+        // the directed slots of the edge among the candidate lanes: even lanes carry j -> x,
+        // odd lanes x -> j; two of a kind = orientation error / non-manifold edge (E(i,j) > 2)
+        const unsigned ev = c.peers & 0x55555555u, od = c.peers & 0xAAAAAAAAu;
+        const int32_t s_ji = __shfl_sync(0xffffffffu, c.slot, ev ? __ffs(ev) - 1 : 0);
+        const int32_t s_ij = __shfl_sync(0xffffffffu, c.slot, od ? __ffs(od) - 1 : 0);
+        if (mine) {
+            if (__popc(ev) > 1 || __popc(od) > 1) atomicOr(flags, kFlagNonManifold);
+            emit_edge(edge_off[j] + rank, od ? s_ij : -1, ev ? s_ji : -1, c.x, j, face_edge, face_twin, edge_hh,
+                      bnd_word, vbnd, scalars);
+        }
+        return;
+    }
+    if (lane != 0) return;
+    Cand cd{face_vtx, vtx_slot, tp, o0};
+    const int32_t nq = 2 * n;
     for (int32_t q = 0; q < nq; ++q) {
         int32_t i = cd.vert(q);
         if (i >= j || !cd.first(q, i)) continue;
-        // rank of i among the distinct neighbours < j
         int32_t rank = 0;
         for (int32_t p = 0; p < nq; ++p) {
             int32_t x = cd.vert(p);
             if (x < i && cd.first(p, x)) ++rank;
         }
-        const int32_t e = edge_off[j] + rank;
         int32_t s_ji = -1, s_ij = -1, m_ji = 0, m_ij = 0;
         for (int32_t a = 0; a < n; ++a) {
             int32_t h = cd.slot(2 * a);
@@ -99,17 +173,7 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
             if (__ldg(face_vtx + hp) == i) { s_ij = hp; ++m_ij; }
         }
         if (m_ji > 1 || m_ij > 1) atomicOr(flags, kFlagNonManifold);
-        if (s_ij >= 0) { face_edge[s_ij] = e; face_twin[s_ij] = s_ji; }
-        if (s_ji >= 0) { face_edge[s_ji] = e; face_twin[s_ji] = s_ij; }
-        int32_t own = s_ij < 0 ? s_ji : (s_ji < 0 ? s_ij : min(s_ij, s_ji));
-        int32_t oth = s_ij < 0 || s_ji < 0 ? -1 : max(s_ij, s_ji);
-        edge_hh[e] = make_int2(own, oth);
-        if (oth < 0) {
-            atomicOr(bnd_word + (e >> 5), 1u << (e & 31));
-            atomicAdd(scalars + 1, 1);
-            vbnd[i] = 1;
-            vbnd[j] = 1;
-        }
+        emit_edge(edge_off[j] + rank, s_ij, s_ji, i, j, face_edge, face_twin, edge_hh, bnd_word, vbnd, scalars);
     }
 }
 
@@ -258,7 +322,8 @@ void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L) {
     offsets_from_sorted(b.sort_k, b.S, b.vtx_off, b.V, s, L);
     cudaMemcpyAsync(b.vtx_slot, b.sort_v, sizeof(int32_t) * (size_t)b.S, cudaMemcpyDeviceToDevice, s);
     if (b.V > 0) {
-        k_edge_count<<<grid_for(b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V, b.edge_cnt);
+        k_edge_count<<<grid_for(32 * (int64_t)b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
+                                                                        b.edge_cnt);
         L.done("b0_edge_count", s);
     }
     scan_exclusive(b.edge_cnt, b.edge_off, b.V, b.scalars + 0, b.scratch, s, L);
@@ -272,7 +337,7 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     cudaMemsetAsync(b.bnd_word, 0, sizeof(uint32_t) * nw, s);
     if (b.V > 0) cudaMemsetAsync(b.vbnd, 0, sizeof(int32_t) * b.V, s);
     if (b.V > 0) {
-        k_edge_fill<<<grid_for(b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V, b.edge_off,
+        k_edge_fill<<<grid_for(32 * (int64_t)b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V, b.edge_off,
                                                        b.face_edge, b.face_twin, b.edge_hh, b.bnd_word, b.vbnd,
                                                        b.scalars, b.flags);
         L.done("b0_edge_fill", s);

@@ -12,6 +12,8 @@
 //   k_cc_vertex  per parent vertex: S(p) = (1 - 2/n) p + 1/n^2 sum_{incident slots}(p_next + f)
 //                = s1 + s2 + s3 of P:L332-357 (s2 = F P, s3 = M f) via a 1-ring walk.
 // Boundary vertices and creases are overwritten afterwards by crease.cu (boundary = inf crease).
+#include <algorithm>
+
 #include "internal.h"
 
 namespace alsub {
@@ -24,17 +26,34 @@ ALSUB_D int32_t cc_base(const uint32_t *w, const int32_t *wp, int32_t e) {
 }
 
 // ---------------- face kernel: reduced quad matrix (levels >= 1, or all-quad input) --------
-template <bool ADJ, bool BND>
-__global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev c, Frames fr, bool topo) {
+template <bool ADJ, bool BND, int NBC>
+__global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev c, Frames fr, bool topo, bool fpv) {
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= p.F) return;
     const int4 fv = __ldg(reinterpret_cast<const int4 *>(p.face_vtx) + r);
     const int32_t v[4] = {fv.x, fv.y, fv.z, fv.w};
     const int32_t V = p.V, F = p.F;
-    for (int f = 0; f < fr.nb; ++f) {
+    const int nb = NBC ? NBC : fr.nb;
+    const unsigned mask = __activemask();  // sibling quads 4R..4R+3 are active together
+    for (int f = 0; f < nb; ++f) {
         const float *P = fr.P + f * fr.Pstride;
-        P3 s = ld3(P, v[0]) + ld3(P, v[1]) + ld3(P, v[2]) + ld3(P, v[3]);
-        st3(fr.Pn + f * fr.Pnstride, V + r, 0.25f * s);
+        float *Pn = fr.Pn + f * fr.Pnstride;
+        const P3 p0 = ld3(P, v[0]), p1 = ld3(P, v[1]), p2 = ld3(P, v[2]), p3 = ld3(P, v[3]);
+        const P3 fc = 0.25f * (p0 + p1 + p2 + p3);
+        st3(Pn, V + r, fc);
+        if (fpv) {
+            // corner 2 of the four children of a quad is the parent's face point (born at this
+            // level, valence 4): its vertex point needs exactly these four faces' f and their
+            // corner-3 vertices -- reduce over the 4 sibling lanes (no gather, no vertex pass)
+            P3 acc = p3 + fc;
+            acc.x += __shfl_xor_sync(mask, acc.x, 1);
+            acc.y += __shfl_xor_sync(mask, acc.y, 1);
+            acc.z += __shfl_xor_sync(mask, acc.z, 1);
+            acc.x += __shfl_xor_sync(mask, acc.x, 2);
+            acc.y += __shfl_xor_sync(mask, acc.y, 2);
+            acc.z += __shfl_xor_sync(mask, acc.z, 2);
+            if ((r & 3) == 0) st3(Pn, v[2], 0.5f * p2 + 0.0625f * acc);
+        }
     }
     if (!topo) return;
     const int4 fe = __ldg(reinterpret_cast<const int4 *>(p.face_edge) + r);
@@ -66,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
 }
 
 // ---------------- face kernel: general matrix (level 0: mixed orders or triangles) ---------
-template <int ORDER, bool ADJ, bool BND>
+template <int ORDER, bool ADJ, bool BND, int NBC>
 __global__ void __launch_bounds__(kThreads) k_cc_face_gen(LevelDev p, ChildDev c, Frames fr, bool topo) {
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= p.F) return;
@@ -74,7 +93,8 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_gen(LevelDev p, ChildDev c
     const int32_t o = tp.first(r), n = tp.order(r);
     const int32_t V = p.V, F = p.F;
     const float inv = 1.0f / (float)n;
-    for (int f = 0; f < fr.nb; ++f) {
+    const int nb = NBC ? NBC : fr.nb;
+    for (int f = 0; f < nb; ++f) {
         const float *P = fr.P + f * fr.Pstride;
         P3 s = p3zero();
         for (int32_t t = 0; t < n; ++t) s = s + ld3(P, __ldg(p.face_vtx + o + t));
@@ -101,58 +121,94 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_gen(LevelDev p, ChildDev c
 }
 
 // ---------------- edge kernel ----------------
-// per parent edge e with pair (h = smallest slot, tw = the other or -1)
-template <int ORDER, bool ADJ, bool BND>
+// per parent edge e with pair (h = smallest slot, tw = the other or -1).  IT edges per thread
+// with all loads of a stage issued before any is consumed (memory-level parallelism: the kernel
+// is a chain edge pair -> face row -> positions).  NBC = compile-time frame count (0 = runtime).
+template <int ORDER>
+ALSUB_D void edge_ends(const LevelDev &p, const Topo<ORDER> &tp, int32_t h, int32_t &va, int32_t &vb, int32_t &hn) {
+    if constexpr (ORDER == 4) {
+        const int4 row = __ldg(reinterpret_cast<const int4 *>(p.face_vtx) + (h >> 2));
+        const int t = h & 3;
+        const int32_t r[4] = {row.x, row.y, row.z, row.w};
+        va = r[t];
+        vb = r[(t + 1) & 3];
+        hn = (h & ~3) | ((h + 1) & 3);
+    } else {
+        hn = tp.next(h);
+        va = __ldg(p.face_vtx + h);
+        vb = __ldg(p.face_vtx + hn);
+    }
+}
+
+template <int ORDER, bool ADJ, bool BND, int NBC, int IT>
 __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Frames fr, bool topo) {
-    const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= p.E) return;
     const Topo<ORDER> tp{p.face_off, p.slot_face};
-    const int2 hh = __ldg(p.edge_hh + e);
-    const int32_t h = hh.x, tw = hh.y;
-    const int32_t hn = tp.next(h);
-    const int32_t va = __ldg(p.face_vtx + h), vb = __ldg(p.face_vtx + hn);
+    const int32_t e0 = blockIdx.x * (kThreads * IT) + threadIdx.x;
     const int32_t V = p.V, F = p.F;
-    const int32_t fr_r = V + tp.face(h);
-    const int32_t fr_s = tw >= 0 ? V + tp.face(tw) : -1;
-    for (int f = 0; f < fr.nb; ++f) {
+    const int nb = NBC ? NBC : fr.nb;
+    int32_t hv[IT], tv[IT], va[IT], vb[IT], hn[IT];
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+        const int32_t e = e0 + k * kThreads;
+        const int2 hh = e < p.E ? __ldg(p.edge_hh + e) : make_int2(0, -1);
+        hv[k] = hh.x;
+        tv[k] = hh.y;
+    }
+#pragma unroll
+    for (int k = 0; k < IT; ++k) edge_ends<ORDER>(p, tp, hv[k], va[k], vb[k], hn[k]);
+    for (int f = 0; f < nb; ++f) {
         const float *P = fr.P + f * fr.Pstride;
         float *Pn = fr.Pn + f * fr.Pnstride;
-        const P3 ab = ld3(P, va) + ld3(P, vb);
-        P3 out;
-        if (tw < 0) out = 0.5f * ab;
-        else out = 0.25f * (ab + ld3c(Pn, fr_r) + ld3c(Pn, fr_s));
-        st3(Pn, (int64_t)V + F + e, out);
+        P3 ab[IT], fs[IT];
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            ab[k] = ld3(P, va[k]) + ld3(P, vb[k]);
+            fs[k] = tv[k] >= 0 ? ld3c(Pn, V + tp.face(hv[k])) + ld3c(Pn, V + tp.face(tv[k])) : p3zero();
+        }
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int32_t e = e0 + k * kThreads;
+            if (e >= p.E) continue;
+            st3(Pn, (int64_t)V + F + e, tv[k] < 0 ? 0.5f * ab[k] : 0.25f * (ab[k] + fs[k]));
+        }
     }
     if constexpr (ADJ) {
         if (!topo) return;
-        // structured child edge ids: block [base, base + 4 - bnd) = (lo,ep), (hi,ep), (fp_min,ep), (fp_max,ep)
-        const int32_t bp = BND ? bprefix(p.bnd_word, p.bnd_wpre, e) : 0;
-        const int32_t base = 4 * e - bp;
-        const int32_t h_ab = va < vb ? h : tw, h_ba = va < vb ? tw : h;
-        // child half-edges: (lo,ep): lo->ep = 4 h_ab, ep->lo = 4 next(h_ba) + 3; (hi,ep) symmetric
-        const int32_t a0 = h_ab >= 0 ? 4 * h_ab : -1, a1 = h_ba >= 0 ? 4 * tp.next(h_ba) + 3 : -1;
-        const int32_t b0 = h_ba >= 0 ? 4 * h_ba : -1, b1 = h_ab >= 0 ? 4 * tp.next(h_ab) + 3 : -1;
-        auto pair = [](int32_t x, int32_t y) {
-            if (x < 0) return make_int2(y, -1);
-            if (y < 0) return make_int2(x, -1);
-            return make_int2(min(x, y), max(x, y));
-        };
-        c.edge_hh[base + 0] = pair(a0, a1);
-        c.edge_hh[base + 1] = pair(b0, b1);
-        c.edge_hh[base + 2] = pair(4 * h + 1, 4 * hn + 2);  // (fp of face(h), ep); h < tw
-        if (tw >= 0) c.edge_hh[base + 3] = pair(4 * tw + 1, 4 * tp.next(tw) + 2);
-        if constexpr (BND) {
-            // child boundary bits and, in closed form, the child per-word prefix:
-            // bprefix'(base + k) = 2 bprefix(e) + bnd_e min(k, 2)
-            const int32_t nch = tw < 0 ? 3 : 4;
-            if (tw < 0) {
-                atomicOr(c.bnd_word + (base >> 5), 1u << (base & 31));
-                atomicOr(c.bnd_word + ((base + 1) >> 5), 1u << ((base + 1) & 31));
-            }
-            const int32_t w = (base + 31) >> 5;
-            if (32 * w < base + nch) {
-                const int32_t k = 32 * w - base;
-                c.bnd_wpre[w] = 2 * bp + (tw < 0 ? min(k, 2) : 0);
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int32_t e = e0 + k * kThreads;
+            if (e >= p.E) continue;
+            const int32_t h = hv[k], tw = tv[k];
+            // structured child edge ids: block [base, base + 4 - bnd) = (lo,ep), (hi,ep), (fp_min,ep), (fp_max,ep)
+            const int32_t bp = BND ? bprefix(p.bnd_word, p.bnd_wpre, e) : 0;
+            const int32_t base = 4 * e - bp;
+            const bool fwd = va[k] < vb[k];
+            const int32_t h_ab = fwd ? h : tw, h_ba = fwd ? tw : h;
+            // child half-edges: (lo,ep): lo->ep = 4 h_ab, ep->lo = 4 next(h_ba) + 3; (hi,ep) symmetric
+            const int32_t a0 = h_ab >= 0 ? 4 * h_ab : -1, a1 = h_ba >= 0 ? 4 * tp.next(h_ba) + 3 : -1;
+            const int32_t b0 = h_ba >= 0 ? 4 * h_ba : -1, b1 = h_ab >= 0 ? 4 * tp.next(h_ab) + 3 : -1;
+            auto pair = [](int32_t x, int32_t y) {
+                if (x < 0) return make_int2(y, -1);
+                if (y < 0) return make_int2(x, -1);
+                return make_int2(min(x, y), max(x, y));
+            };
+            c.edge_hh[base + 0] = pair(a0, a1);
+            c.edge_hh[base + 1] = pair(b0, b1);
+            c.edge_hh[base + 2] = pair(4 * h + 1, 4 * hn[k] + 2);  // (fp of face(h), ep); h < tw
+            if (tw >= 0) c.edge_hh[base + 3] = pair(4 * tw + 1, 4 * tp.next(tw) + 2);
+            if constexpr (BND) {
+                // child boundary bits and, in closed form, the child per-word prefix:
+                // bprefix'(base + k) = 2 bprefix(e) + bnd_e min(k, 2)
+                const int32_t nch = tw < 0 ? 3 : 4;
+                if (tw < 0) {
+                    atomicOr(c.bnd_word + (base >> 5), 1u << (base & 31));
+                    atomicOr(c.bnd_word + ((base + 1) >> 5), 1u << ((base + 1) & 31));
+                }
+                const int32_t w = (base + 31) >> 5;
+                if (32 * w < base + nch) {
+                    const int32_t kk = 32 * w - base;
+                    c.bnd_wpre[w] = 2 * bp + (tw < 0 ? min(kk, 2) : 0);
+                }
             }
         }
     }
@@ -279,17 +335,29 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
 template <int ORDER, bool ADJ, bool BND>
 static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, const VSegs &g,
                       cudaStream_t s, Launches &L) {
+    const bool fpv = g.level >= 2;  // face points born at this level are smoothed by the face kernel
     if (p.F > 0) {
-        if constexpr (ORDER == 4) k_cc_face_quad<ADJ, BND><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
-        else k_cc_face_gen<ORDER, ADJ, BND><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+        const bool one = fr.nb == 1;
+        if constexpr (ORDER == 4) {
+            if (one) k_cc_face_quad<ADJ, BND, 1><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo, fpv);
+            else k_cc_face_quad<ADJ, BND, 0><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo, fpv);
+        } else {
+            if (one) k_cc_face_gen<ORDER, ADJ, BND, 1><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+            else k_cc_face_gen<ORDER, ADJ, BND, 0><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+        }
         L.done("cc_face", s);
     }
     if (p.E > 0) {
-        k_cc_edge<ORDER, ADJ, BND><<<grid_for(p.E), kThreads, 0, s>>>(p, c, fr, topo);
+        constexpr int IT = 2;
+        const unsigned g = grid_for(p.E, kThreads * IT);
+        if (fr.nb == 1) k_cc_edge<ORDER, ADJ, BND, 1, IT><<<g, kThreads, 0, s>>>(p, c, fr, topo);
+        else k_cc_edge<ORDER, ADJ, BND, 0, IT><<<g, kThreads, 0, s>>>(p, c, fr, topo);
         L.done("cc_edge", s);
     }
     if (p.V > 0) {
-        const unsigned nblk = grid_for(p.V, 4 * kThreads);
+        // >= 2 waves of 148 SMs for small levels, 4 vertices per thread for large ones
+        const unsigned nblk = (unsigned)std::max<int64_t>(grid_for(p.V, 4 * kThreads),
+                                                          std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
         if constexpr (ORDER == 4) k_cc_vertex<4><<<nblk, kThreads, 0, s>>>(p, fr, g);
         else k_cc_vertex<0><<<nblk, kThreads, 0, s>>>(p, fr, g);
         L.done("cc_vertex", s);
