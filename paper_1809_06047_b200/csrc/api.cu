@@ -77,6 +77,8 @@ struct alsub_mesh {
     bool user_creases = false;
     int32_t *sv_vtx = nullptr, *sv_off = nullptr;  // shared special-vertex table (prefix per level)
     int32_t *sv_vtx_create = nullptr, *sv_off_create = nullptr;
+    float *hs = nullptr;          // half ring sums (CC, levels >= 2), [3 * max F_l] floats
+    int64_t hs_elems = 0;
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
     void *scratch_create = nullptr;
@@ -92,6 +94,7 @@ struct alsub_mesh {
     // frames
     int frames_nb = 0;
     std::vector<float *> frame_buf;
+    float *frame_hs = nullptr;
 };
 
 // ---------------- memory ----------------
@@ -227,7 +230,9 @@ extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t
     b.sort_k2 = A<int32_t>(m, S0, s, ML, ok);
     b.sort_v2 = A<int32_t>(m, S0, s, ML, ok);
     b.vtx_off = A<int32_t>(m, (int64_t)num_verts + 1, s, ML, ok);
-    b.vtx_slot = A<int32_t>(m, S0, s, ML, ok);
+    b.vtx_slot = b.sort_v;  // the radix sort's value output is M^T's row index array
+    b.vtx_cnt = A<int32_t>(m, (int64_t)num_verts + 1, s, ML, ok);
+    b.digits = A<int32_t>(m, 4 * 256, s, ML, ok);
     b.edge_cnt = A<int32_t>(m, num_verts, s, ML, ok);
     b.edge_off = A<int32_t>(m, num_verts, s, ML, ok);
     b.face_edge = A<int32_t>(m, S0, s, ML, ok);
@@ -238,9 +243,7 @@ extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t
     b.v_idx = A<int32_t>(m, num_verts, s, ML, ok);
     b.flags = A<int32_t>(m, 8, s, ML, ok);
     b.scalars = A<int32_t>(m, 8, s, ML, ok);
-    m->scratch_bytes = sort_scratch_bytes(S0);
-    size_t sb = scan_scratch_bytes(std::max<int64_t>(num_verts, S0) + 1);
-    if (sb > m->scratch_bytes) m->scratch_bytes = sb;
+    m->scratch_bytes = build0_scratch_bytes(num_verts, S0);
     m->scratch = dev_alloc(m, m->scratch_bytes, s, ML);
     b.scratch = m->scratch;
     m->scratch_create = m->scratch;
@@ -250,7 +253,7 @@ extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t
     cudaMemsetAsync(b.scalars, 0, 8 * sizeof(int32_t), s);
     init_scheme_tables(s);
     Launches L;
-    // stage 1: face validation
+    // stage 1: face validation (+ the sort input and histograms)
     build0_validate(b, s, L);
     int32_t flags = 0;
     if (cudaMemcpyAsync(&flags, b.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -364,6 +367,10 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
     const int64_t sv_total = std::max<int64_t>(m->V0, special ? lv[levels].nsv : 0) + 1;
     m->sv_vtx = A<int32_t>(m, sv_total, s, ML, ok);
     m->sv_off = A<int32_t>(m, sv_total, s, ML, ok);
+    m->hs_elems = 0;
+    if (scheme == ALSUB_CATMULL_CLARK)
+        for (int l = 2; l < levels; ++l) m->hs_elems = std::max<int64_t>(m->hs_elems, 3 * lv[l].F);
+    m->hs = m->hs_elems ? A<float>(m, m->hs_elems, s, ML, ok) : nullptr;
     m->b0.sv_vtx = m->sv_vtx;
     m->b0.sv_off = m->sv_off;
     int64_t max_scan = std::max<int64_t>(m->V0, m->S0) + 1;
@@ -399,7 +406,7 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
         }
         (void)adj;
     }
-    size_t need = std::max(sort_scratch_bytes(m->S0), scan_scratch_bytes(max_scan));
+    size_t need = std::max(build0_scratch_bytes(m->V0, m->S0), scan_scratch_bytes(max_scan));
     if (need > m->scratch_bytes) {
         void *p = dev_alloc(m, need, s, ML);
         if (!p) ok = false;
@@ -434,6 +441,7 @@ static VSegs make_segs(alsub_mesh *m, int l) {
         g.ehh[k - 1] = q.edge_hh;
     }
     g.nseg = n;
+    g.hs_seg = l >= 2 ? n - 1 : -1;  // the last segment = edge points born at level l
     g.vtx_off0 = m->b0.vtx_off; g.vtx_list0 = m->b0.vtx_slot; g.face_off0 = m->in_face_off;
     g.slot_face0 = m->b0.slot_face; g.vbnd0 = m->b0.vbnd;
     return g;
@@ -443,6 +451,7 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     const int scheme = m->scheme, levels = m->levels;
     // a1-a3: level-0 mesh matrix, M^T by radix sort, edge index, creases
     L.level = -1;
+    build0_validate(m->b0, s, L);
     build0_count_edges(m->b0, s, L);
     build0_fill(m->b0, false, s, L);
     const bool special = scheme != ALSUB_SQRT3 && m->K0 > 0;
@@ -457,7 +466,7 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
         ChildDev c = child_of(C);
         c.sv_vtx = m->sv_vtx;
         c.sv_off = m->sv_off;
-        Frames fr{P.pos, C.pos, 3 * P.V, 3 * C.V, 1};
+        Frames fr{P.pos, C.pos, 3 * P.V, 3 * C.V, 1, m->hs, 0};
         if (scheme == ALSUB_CATMULL_CLARK) {
             VSegs g = make_segs(m, l);
             cc_level(p, c, fr, true, adj, g, s, L);
@@ -704,6 +713,7 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
         bool ok = true;
         for (int l = 0; l <= m->levels; ++l)
             m->frame_buf[l] = A<float>(m, 3 * m->lv[l].V * nb, s, m->mem_frames, ok);
+        m->frame_hs = m->hs_elems ? A<float>(m, m->hs_elems * nb, s, m->mem_frames, ok) : nullptr;
         if (!ok) return fail(ALSUB_E_NOMEM, "frame batch buffers");
         m->frames_nb = nb;
     }
@@ -725,7 +735,7 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
             p.sv_vtx = m->sv_vtx;
             p.sv_off = m->sv_off;
             ChildDev c{};
-            Frames fr{P, Pn, 3 * Pl.V, 3 * m->lv[l + 1].V, n};
+            Frames fr{P, Pn, 3 * Pl.V, 3 * m->lv[l + 1].V, n, m->frame_hs, m->hs_elems};
             if (scheme == ALSUB_CATMULL_CLARK) {
                 VSegs g = make_segs(m, l);
                 cc_level(p, c, fr, false, false, g, s, L);

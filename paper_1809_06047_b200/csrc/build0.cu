@@ -12,28 +12,44 @@
 //     (F(i,j) and F(j,i)) and the multiplicity checks (E(i,j) in {1, 2}).
 // Then the crease matrix C is attached to edge ids and the special-edge list
 // (boundary edges = infinitely sharp creases, reading R6) and special-vertex table are built.
+#include <algorithm>
+
 #include "internal.h"
 
 namespace alsub {
 
 using T0 = Topo<0>;
 
-__global__ void k_validate_faces(const int32_t *__restrict__ face_off, const int32_t *__restrict__ face_vtx,
-                                 int32_t F, int32_t V, int32_t *__restrict__ slot_face, int32_t *__restrict__ sk,
-                                 int32_t *__restrict__ sv, int32_t *flags) {
-    int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= F) return;
-    int32_t o = face_off[r], c = face_off[r + 1] - o;
-    if (c < 3) { atomicOr(flags, kFlagMesh); return; }
-    for (int32_t t = 0; t < c; ++t) {
-        int32_t v = face_vtx[o + t];
-        slot_face[o + t] = r;
-        sk[o + t] = v;
-        sv[o + t] = o + t;
-        if (v < 0 || v >= V) { atomicOr(flags, kFlagMesh); sk[o + t] = 0; continue; }
-        for (int32_t u = 0; u < t; ++u)
-            if (face_vtx[o + u] == v) atomicOr(flags, kFlagMesh);
+// a1 + the inputs of a2: validation, slot -> face, the (vertex, slot) sort input, the row
+// lengths of M^T (vertex valences n = M 1, Eq. vo) and the digit histograms of every radix pass.
+__global__ void __launch_bounds__(kThreads) k_b0_prep(const int32_t *__restrict__ face_off,
+                                                    const int32_t *__restrict__ face_vtx, int32_t F, int32_t V,
+                                                    int passes, int32_t *__restrict__ slot_face,
+                                                    int32_t *__restrict__ sk, int32_t *__restrict__ sv,
+                                                    int32_t *__restrict__ vtx_cnt, int32_t *__restrict__ digits,
+                                                    int32_t *flags) {
+    __shared__ int h[4][256];
+    for (int p = 0; p < passes; ++p) h[p][threadIdx.x] = 0;
+    __syncthreads();
+    const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < F) {
+        const int32_t o = face_off[r], c = face_off[r + 1] - o;
+        if (c < 3) atomicOr(flags, kFlagMesh);
+        for (int32_t t = 0; t < c; ++t) {
+            int32_t v = face_vtx[o + t];
+            slot_face[o + t] = r;
+            sv[o + t] = o + t;
+            if (v < 0 || v >= V) { atomicOr(flags, kFlagMesh); v = 0; }
+            sk[o + t] = v;
+            atomicAdd(vtx_cnt + v, 1);
+            for (int p = 0; p < passes; ++p) atomicAdd(&h[p][((uint32_t)v >> (8 * p)) & 255u], 1);
+            for (int32_t u = 0; u < t; ++u)
+                if (face_vtx[o + u] == face_vtx[o + t]) atomicOr(flags, kFlagMesh);
+        }
     }
+    __syncthreads();
+    for (int p = 0; p < passes; ++p)
+        if (h[p][threadIdx.x]) atomicAdd(digits + 256 * p + threadIdx.x, h[p][threadIdx.x]);
 }
 
 // Candidate q of vertex j's collision list: slot vtx_slot[o0 + q/2], neighbour next (q even) or prev.
@@ -128,11 +144,12 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
                             const int32_t *__restrict__ edge_off, int32_t *__restrict__ face_edge,
                             int32_t *__restrict__ face_twin, int2 *__restrict__ edge_hh,
                             uint32_t *__restrict__ bnd_word, int32_t *__restrict__ vbnd,
-                            int32_t *__restrict__ scalars, int32_t *flags) {
+                            int32_t *__restrict__ scalars, int32_t *flags, int32_t *__restrict__ slot0) {
     const int32_t j = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (j >= V) return;
     const int32_t o0 = vtx_off[j], n = vtx_off[j + 1] - o0;
+    if (lane == 0) slot0[j] = n > 0 ? vtx_slot[o0] : -1;
     if (n <= 16) {
         const WarpCand c = warp_cand(face_vtx, vtx_slot, tp, o0, n, lane);
         const bool mine = c.first && c.x < j;
@@ -177,14 +194,6 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
     }
 }
 
-__global__ void k_slot0(const int32_t *__restrict__ vtx_off, const int32_t *__restrict__ vtx_slot, int32_t V,
-                        int32_t *__restrict__ slot0) {
-    int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= V) return;
-    int32_t o = vtx_off[v];
-    slot0[v] = vtx_off[v + 1] > o ? vtx_slot[o] : -1;
-}
-
 // a vertex whose interior faces form a closed fan that misses some incident face is non-manifold
 // (reading R18); open fans (bowties) are allowed and end up as corners.
 __global__ void k_check_fans(const int32_t *__restrict__ face_twin, const int32_t *__restrict__ vtx_off,
@@ -202,96 +211,96 @@ __global__ void k_check_fans(const int32_t *__restrict__ face_twin, const int32_
     if (h == h0 && n != deg) atomicOr(flags, kFlagNonManifold);
 }
 
-__global__ void k_word_popc(const uint32_t *__restrict__ w, int32_t n, int32_t *__restrict__ c) {
-    int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) c[i] = __popc(w[i]);
-}
 
-__global__ void k_crease_lookup(const int32_t *__restrict__ crease, const float *__restrict__ sigma, int32_t K,
-                                const int32_t *__restrict__ face_vtx, const int32_t *__restrict__ vtx_off,
-                                const int32_t *__restrict__ vtx_slot, const int32_t *__restrict__ face_edge,
-                                const int2 *__restrict__ edge_hh, T0 tp,
-                                int32_t V, float *__restrict__ edge_sigma, int32_t *__restrict__ edge_cidx,
-                                int32_t *flags) {
-    int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= K) return;
-    int32_t a = crease[2 * k], b = crease[2 * k + 1];
-    float sg = sigma[k];
+
+
+
+
+
+
+
+// ------------------------------------------------------------------------------------------
+// Level-0 special lists.  The level-0 special-vertex table is the identity over all V0 vertices
+// (sv_vtx[v] = v; non-special vertices get empty lists), so no vertex compaction is needed.
+// ------------------------------------------------------------------------------------------
+// crease matrix C: pairs -> edge ids and the special flags (boundary = inf crease,
+// reading R6); also the popcounts of the boundary words
+__global__ void __launch_bounds__(kThreads) k_b0_flags(const int32_t *__restrict__ crease, const float *__restrict__ sigma,
+                                                     int32_t K, const int32_t *__restrict__ face_vtx,
+                                                     const int32_t *__restrict__ vtx_off,
+                                                     const int32_t *__restrict__ vtx_slot,
+                                                     const int32_t *__restrict__ face_edge, const int2 *__restrict__ edge_hh,
+                                                     T0 tp, int32_t V, int32_t E, const uint32_t *__restrict__ bnd_word,
+                                                     int32_t nw, float *__restrict__ edge_sigma,
+                                                     int32_t *__restrict__ edge_cidx, int32_t *__restrict__ flag,
+                                                     int32_t *__restrict__ wcnt, int32_t *flags) {
+    const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < E && edge_hh[t].y < 0) atomicOr(flag + t, 1);
+    if (t < nw) wcnt[t] = __popc(bnd_word[t]);
+    if (t >= K) return;
+    const int32_t a = crease[2 * t], b = crease[2 * t + 1];
+    const float sg = sigma[t];
     if (a < 0 || a >= V || b < 0 || b >= V || a == b || !(sg >= 0.0f)) { atomicOr(flags, kFlagCrease); return; }
-    int32_t j = max(a, b), i = min(a, b), e = -1;
+    const int32_t j = max(a, b), i = min(a, b);
+    int32_t e = -1;
     for (int32_t p = vtx_off[j]; p < vtx_off[j + 1]; ++p) {
-        int32_t h = vtx_slot[p];
+        const int32_t h = vtx_slot[p];
         if (face_vtx[tp.next(h)] == i) { e = face_edge[h]; break; }
-        int32_t hp = tp.prev(h);
+        const int32_t hp = tp.prev(h);
         if (face_vtx[hp] == i) { e = face_edge[hp]; break; }
     }
     if (e < 0) { atomicOr(flags, kFlagCrease); return; }
-    if (atomicCAS(edge_cidx + e, -1, k) != -1) { atomicOr(flags, kFlagCrease); return; }
-    bool bnd = edge_hh[e].y < 0;
-    if (sg > 0.0f && !bnd) edge_sigma[e] = sg;  // boundary edges are infinitely sharp anyway
+    if (atomicCAS(edge_cidx + e, -1, t) != -1) { atomicOr(flags, kFlagCrease); return; }
+    if (sg > 0.0f && edge_hh[e].y >= 0) {  // boundary edges are infinitely sharp anyway (R19)
+        edge_sigma[e] = sg;
+        atomicOr(flag + e, 1);
+    }
 }
 
-__global__ void k_special_flag(const int2 *__restrict__ edge_hh, const float *__restrict__ edge_sigma, int32_t E,
-                               int32_t *__restrict__ flag) {
-    int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= E) return;
-    flag[e] = (edge_hh[e].y < 0 || edge_sigma[e] > 0.0f) ? 1 : 0;
-}
-
-__global__ void k_special_fill(const int2 *__restrict__ edge_hh, const int32_t *__restrict__ face_vtx,
-                               const float *__restrict__ edge_sigma, const int32_t *__restrict__ flag,
-                               const int32_t *__restrict__ off, T0 tp, int32_t E, SpEdge *__restrict__ sp,
-                               int32_t *__restrict__ v_mark) {
-    int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+// special-edge list in ascending edge id (compaction by the scanned flags) + list lengths
+__global__ void __launch_bounds__(kThreads) k_b0_special(const int2 *__restrict__ edge_hh, const int32_t *__restrict__ face_vtx,
+                                                       const float *__restrict__ edge_sigma,
+                                                       const int32_t *__restrict__ flag, const int32_t *__restrict__ off,
+                                                       T0 tp, int32_t E, SpEdge *__restrict__ sp,
+                                                       int32_t *__restrict__ sv_cnt) {
+    const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E || !flag[e]) return;
-    int32_t h = edge_hh[e].x;
-    int32_t va = face_vtx[h], vb = face_vtx[tp.next(h)];
-    bool bnd = edge_hh[e].y < 0;
-    SpEdge s;
-    s.e = e;
-    s.a = min(va, vb);
-    s.b = max(va, vb);
-    s.ia = s.ib = -1;
-    s.sigma = bnd ? __int_as_float(0x7f800000) : edge_sigma[e];
-    s.flags = bnd ? kSpBoundary : 0;
-    s.pad = 0;
-    sp[off[e]] = s;
-    v_mark[s.a] = 1;
-    v_mark[s.b] = 1;
+    const int2 hh = edge_hh[e];
+    const int32_t va = face_vtx[hh.x], vb = face_vtx[tp.next(hh.x)];
+    const bool bnd = hh.y < 0;
+    SpEdge x;
+    x.e = e;
+    x.a = min(va, vb);
+    x.b = max(va, vb);
+    x.ia = x.a;  // identity special-vertex table at level 0
+    x.ib = x.b;
+    x.sigma = bnd ? __int_as_float(0x7f800000) : edge_sigma[e];
+    x.flags = bnd ? kSpBoundary : 0;
+    x.pad = 0;
+    sp[off[e]] = x;
+    atomicAdd(sv_cnt + x.a, 1);
+    atomicAdd(sv_cnt + x.b, 1);
 }
 
-__global__ void k_sv_fill(const int32_t *__restrict__ v_mark, const int32_t *__restrict__ v_idx, int32_t V,
-                          int32_t *__restrict__ sv_vtx) {
-    int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < V && v_mark[v]) sv_vtx[v_idx[v]] = v;
-}
-
-__global__ void k_sp_index(SpEdge *__restrict__ sp, const int32_t *__restrict__ count,
-                           const int32_t *__restrict__ v_idx, int32_t cap, int32_t *__restrict__ sv_cnt) {
-    int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= cap || j >= *count) return;
-    const int32_t ia = v_idx[sp[j].a], ib = v_idx[sp[j].b];
-    sp[j].ia = ia;
-    sp[j].ib = ib;
-    atomicAdd(sv_cnt + ia, 1);
-    atomicAdd(sv_cnt + ib, 1);
-}
-
-// special-vertex CSR: incident special edges of every special vertex, ascending
-__global__ void k_sv_list(const SpEdge *__restrict__ sp, const int32_t *__restrict__ count, int32_t cap,
-                          const int32_t *__restrict__ sv_off, int32_t *__restrict__ sv_cur, int32_t *__restrict__ sv_list) {
-    int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kThreads) k_b0_svlist(const SpEdge *__restrict__ sp, const int32_t *__restrict__ count,
+                                                      int32_t cap, const int32_t *__restrict__ sv_off,
+                                                      int32_t *__restrict__ sv_cur, int32_t *__restrict__ sv_list) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= cap || j >= *count) return;
     const int32_t ia = sp[j].ia, ib = sp[j].ib;
     sv_list[sv_off[ia] + atomicAdd(sv_cur + ia, 1)] = j;
     sv_list[sv_off[ib] + atomicAdd(sv_cur + ib, 1)] = j;
 }
 
-__global__ void k_sv_sort(const int32_t *__restrict__ nsv, int32_t cap, const int32_t *__restrict__ sv_off,
-                          int32_t *__restrict__ sv_list) {
-    int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= cap || i >= *nsv) return;
-    const int32_t o = sv_off[i], n = sv_off[i + 1] - o;
+// ascending lists (= the oracle's edge-id order, so crease sums match bit for bit) + identity table
+__global__ void __launch_bounds__(kThreads) k_b0_svsort(int32_t V, const int32_t *__restrict__ sv_off,
+                                                      int32_t *__restrict__ sv_list, int32_t *__restrict__ sv_vtx,
+                                                      int32_t *__restrict__ scalars) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v == 0) scalars[3] = V;
+    if (v >= V) return;
+    sv_vtx[v] = v;
+    const int32_t o = sv_off[v], n = sv_off[v + 1] - o;
     for (int32_t a = 1; a < n; ++a) {
         const int32_t x = sv_list[o + a];
         int32_t b = a - 1;
@@ -301,26 +310,35 @@ __global__ void k_sv_sort(const int32_t *__restrict__ nsv, int32_t cap, const in
 }
 
 // ------------------------------------------------------------------------------------------
-void build0_validate(Build0 &b, cudaStream_t s, Launches &L) {
-    if (b.F > 0) {
-        k_validate_faces<<<grid_for(b.F), kThreads, 0, s>>>(b.face_off, b.face_vtx, b.F, b.V, b.slot_face, b.sort_k,
-                                                            b.sort_v, b.flags);
-        L.done("b0_validate", s);
-    }
-}
-
 static int bits_for(int32_t V) {
     int bits = 1;
     while (bits < 31 && (1ll << bits) < (long long)V) ++bits;
     return bits;
 }
 
+static int passes_for(int32_t V) { return (bits_for(V) + 7) / 8; }
+
+size_t build0_scratch_bytes(int32_t V, int32_t S) {
+    return std::max(onesweep_scratch_bytes(S, passes_for(V)), scan_scratch_bytes(std::max(V, S) + 1));
+}
+
+// a1: validation + sort input + M^T row lengths + radix digit histograms
+void build0_validate(Build0 &b, cudaStream_t s, Launches &L) {
+    cudaMemsetAsync(b.vtx_cnt, 0, sizeof(int32_t) * ((size_t)b.V + 1), s);
+    cudaMemsetAsync(b.digits, 0, sizeof(int32_t) * 256 * 4, s);
+    if (b.F > 0) {
+        k_b0_prep<<<grid_for(b.F), kThreads, 0, s>>>(b.face_off, b.face_vtx, b.F, b.V, passes_for(b.V), b.slot_face,
+                                                     b.sort_k, b.sort_v, b.vtx_cnt, b.digits, b.flags);
+        L.done("b0_prep", s);
+    }
+}
+
+// a2 + symbolic a3: M^T (run lengths scanned into vtx_off, slots sorted by vertex with the
+// one-sweep radix sort -> vtx_slot aliases sort_v), then the per-vertex upper-triangle counts of E
 void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L) {
     T0 tp{b.face_off, b.slot_face};
-    build0_validate(b, s, L);  // also (re)writes the sort input
-    radix_sort_pairs(b.sort_k, b.sort_v, b.sort_k2, b.sort_v2, b.S, bits_for(b.V), b.scratch, s, L);
-    offsets_from_sorted(b.sort_k, b.S, b.vtx_off, b.V, s, L);
-    cudaMemcpyAsync(b.vtx_slot, b.sort_v, sizeof(int32_t) * (size_t)b.S, cudaMemcpyDeviceToDevice, s);
+    scan_exclusive(b.vtx_cnt, b.vtx_off, (int64_t)b.V + 1, nullptr, b.scratch, s, L);
+    radix_sort_onesweep(b.sort_k, b.sort_v, b.sort_k2, b.sort_v2, b.S, bits_for(b.V), b.digits, true, b.scratch, s, L);
     if (b.V > 0) {
         k_edge_count<<<grid_for(32 * (int64_t)b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
                                                                         b.edge_cnt);
@@ -329,6 +347,7 @@ void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L) {
     scan_exclusive(b.edge_cnt, b.edge_off, b.V, b.scalars + 0, b.scratch, s, L);
 }
 
+// numeric a3 + crease matrix + special lists
 void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     T0 tp{b.face_off, b.slot_face};
     const int32_t E = b.E;
@@ -337,61 +356,44 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     cudaMemsetAsync(b.bnd_word, 0, sizeof(uint32_t) * nw, s);
     if (b.V > 0) cudaMemsetAsync(b.vbnd, 0, sizeof(int32_t) * b.V, s);
     if (b.V > 0) {
-        k_edge_fill<<<grid_for(32 * (int64_t)b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V, b.edge_off,
-                                                       b.face_edge, b.face_twin, b.edge_hh, b.bnd_word, b.vbnd,
-                                                       b.scalars, b.flags);
+        k_edge_fill<<<grid_for(32 * (int64_t)b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
+                                                                       b.edge_off, b.face_edge, b.face_twin, b.edge_hh,
+                                                                       b.bnd_word, b.vbnd, b.scalars, b.flags,
+                                                                       b.vtx_slot0);
         L.done("b0_edge_fill", s);
-        k_slot0<<<grid_for(b.V), kThreads, 0, s>>>(b.vtx_off, b.vtx_slot, b.V, b.vtx_slot0);
-        L.done("b0_slot0", s);
         if (check_fans) {
             k_check_fans<<<grid_for(b.V), kThreads, 0, s>>>(b.face_twin, b.vtx_off, b.vtx_slot0, tp, b.V, b.flags);
             L.done("b0_check_fans", s);
         }
     }
-    k_word_popc<<<grid_for(nw), kThreads, 0, s>>>(b.bnd_word, nw, b.bnd_wcnt);
-    L.done("b0_popc", s);
-    scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, b.scratch, s, L);
     if (E > 0) {
         cudaMemsetAsync(b.edge_sigma, 0, sizeof(float) * E, s);
         cudaMemsetAsync(b.edge_cidx, 0xff, sizeof(int32_t) * E, s);
-    }
-    if (b.K_in > 0) {
-        k_crease_lookup<<<grid_for(b.K_in), kThreads, 0, s>>>(b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off,
-                                                              b.vtx_slot, b.face_edge, b.edge_hh, tp,
-                                                              b.V, b.edge_sigma, b.edge_cidx, b.flags);
-        L.done("b0_crease_lookup", s);
-    }
-    if (E > 0) {
-        k_special_flag<<<grid_for(E), kThreads, 0, s>>>(b.edge_hh, b.edge_sigma, E, b.sp_flag);
-        L.done("b0_special_flag", s);
-    }
-    scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, b.scratch, s, L);
-    if (b.V > 0) cudaMemsetAsync(b.v_mark, 0, sizeof(int32_t) * b.V, s);
-    if (E > 0 && b.sp) {
-        k_special_fill<<<grid_for(E), kThreads, 0, s>>>(b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp,
-                                                        E, b.sp, b.v_mark);
-        L.done("b0_special_fill", s);
-    }
-    scan_exclusive(b.v_mark, b.v_idx, b.V, b.scalars + 3, b.scratch, s, L);
-    if (b.V > 0 && b.sv_vtx) {
-        k_sv_fill<<<grid_for(b.V), kThreads, 0, s>>>(b.v_mark, b.v_idx, b.V, b.sv_vtx);
-        L.done("b0_sv_fill", s);
+        cudaMemsetAsync(b.sp_flag, 0, sizeof(int32_t) * E, s);
     }
     if (b.V > 0) {
         cudaMemsetAsync(b.sv_cnt, 0, sizeof(int32_t) * b.V, s);
         cudaMemsetAsync(b.sv_cur, 0, sizeof(int32_t) * b.V, s);
     }
+    const int64_t nf = std::max<int64_t>(std::max<int64_t>(E, b.K_in), nw);
+    k_b0_flags<<<grid_for(nf), kThreads, 0, s>>>(b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
+                                                 b.face_edge, b.edge_hh, tp, b.V, E, b.bnd_word, nw, b.edge_sigma,
+                                                 b.edge_cidx, b.sp_flag, b.bnd_wcnt, b.flags);
+    L.done("b0_flags", s);
+    scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, b.scratch, s, L);
+    scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, b.scratch, s, L);
     if (E > 0) {
-        k_sp_index<<<grid_for(E), kThreads, 0, s>>>(b.sp, b.scalars + 2, b.v_idx, E, b.sv_cnt);
-        L.done("b0_sp_index", s);
+        k_b0_special<<<grid_for(E), kThreads, 0, s>>>(b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp, E,
+                                                      b.sp, b.sv_cnt);
+        L.done("b0_special", s);
     }
     scan_exclusive(b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V, b.scratch, s, L);
     if (E > 0) {
-        k_sv_list<<<grid_for(E), kThreads, 0, s>>>(b.sp, b.scalars + 2, E, b.sv_off, b.sv_cur, b.sv_list);
+        k_b0_svlist<<<grid_for(E), kThreads, 0, s>>>(b.sp, b.scalars + 2, E, b.sv_off, b.sv_cur, b.sv_list);
         L.done("b0_sv_list", s);
     }
     if (b.V > 0) {
-        k_sv_sort<<<grid_for(b.V), kThreads, 0, s>>>(b.scalars + 3, b.V, b.sv_off, b.sv_list);
+        k_b0_svsort<<<grid_for(b.V), kThreads, 0, s>>>(b.V, b.sv_off, b.sv_list, b.sv_vtx, b.scalars);
         L.done("b0_sv_sort", s);
     }
 }

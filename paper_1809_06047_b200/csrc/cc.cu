@@ -26,61 +26,97 @@ ALSUB_D int32_t cc_base(const uint32_t *w, const int32_t *wp, int32_t e) {
 }
 
 // ---------------- face kernel: reduced quad matrix (levels >= 1, or all-quad input) --------
+// Each thread owns one parent quad and produces 4 child rows (64 B) per output array; a warp's
+// 32 x 64 B = 2 KB are staged in shared memory and written back as 4 fully coalesced 512 B
+// stores (child rows 4 r0 .. 4 r0 + 127 are contiguous).
+ALSUB_D void warp_store_rows(int4 *stage, const int4 (&rows)[4], int4 *dst, int64_t row0, int64_t nrows, int lane) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) stage[lane * 4 + t] = rows[t];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t rr = row0 + k * 32 + lane;
+        if (rr < nrows) dst[rr] = stage[k * 32 + lane];
+    }
+    __syncwarp();
+}
+
 template <bool ADJ, bool BND, int NBC>
 __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev c, Frames fr, bool topo, bool fpv) {
+    __shared__ int4 s_stage[kThreads / 32][128];
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= p.F) return;
-    const int4 fv = __ldg(reinterpret_cast<const int4 *>(p.face_vtx) + r);
+    const bool valid = r < p.F;
+    const int lane = threadIdx.x & 31;
+    int4 *stage = s_stage[threadIdx.x >> 5];
+    const int4 fv = valid ? __ldg(reinterpret_cast<const int4 *>(p.face_vtx) + r) : make_int4(0, 0, 0, 0);
     const int32_t v[4] = {fv.x, fv.y, fv.z, fv.w};
     const int32_t V = p.V, F = p.F;
     const int nb = NBC ? NBC : fr.nb;
-    const unsigned mask = __activemask();  // sibling quads 4R..4R+3 are active together
     for (int f = 0; f < nb; ++f) {
         const float *P = fr.P + f * fr.Pstride;
         float *Pn = fr.Pn + f * fr.Pnstride;
         const P3 p0 = ld3(P, v[0]), p1 = ld3(P, v[1]), p2 = ld3(P, v[2]), p3 = ld3(P, v[3]);
         const P3 fc = 0.25f * (p0 + p1 + p2 + p3);
-        st3(Pn, V + r, fc);
+        if (valid) st3(Pn, V + r, fc);
         if (fpv) {
-            // corner 2 of the four children of a quad is the parent's face point (born at this
+            // (1) the edge point of parent slot r (born at this level) sits at corner 1 of child
+            // r and corner 3 of child r+1 (mod 4): its half ring sum from this parent face is
+            // (p2 + f_r) + (p0 + f_{r+1}); the vertex kernel adds the two halves of the edge
+            const P3 q = p0 + fc;
+            const int src = (lane & ~3) | ((lane + 1) & 3);
+            P3 qn;
+            qn.x = __shfl_sync(0xffffffffu, q.x, src);
+            qn.y = __shfl_sync(0xffffffffu, q.y, src);
+            qn.z = __shfl_sync(0xffffffffu, q.z, src);
+            if (valid) st3(fr.hs + f * fr.hsstride, r, p2 + fc + qn);
+            // (2) corner 2 of the four children of a quad is the parent's face point (born at this
             // level, valence 4): its vertex point needs exactly these four faces' f and their
             // corner-3 vertices -- reduce over the 4 sibling lanes (no gather, no vertex pass)
             P3 acc = p3 + fc;
-            acc.x += __shfl_xor_sync(mask, acc.x, 1);
-            acc.y += __shfl_xor_sync(mask, acc.y, 1);
-            acc.z += __shfl_xor_sync(mask, acc.z, 1);
-            acc.x += __shfl_xor_sync(mask, acc.x, 2);
-            acc.y += __shfl_xor_sync(mask, acc.y, 2);
-            acc.z += __shfl_xor_sync(mask, acc.z, 2);
-            if ((r & 3) == 0) st3(Pn, v[2], 0.5f * p2 + 0.0625f * acc);
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+            acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 1);
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+            acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 2);
+            if (valid && (r & 3) == 0) st3(Pn, v[2], 0.5f * p2 + 0.0625f * acc);
         }
     }
     if (!topo) return;
-    const int4 fe = __ldg(reinterpret_cast<const int4 *>(p.face_edge) + r);
+    const int4 fe = valid ? __ldg(reinterpret_cast<const int4 *>(p.face_edge) + r) : make_int4(0, 0, 0, 0);
     const int32_t e[4] = {fe.x, fe.y, fe.z, fe.w};
-    int4 *cfv = reinterpret_cast<int4 *>(c.face_vtx) + 4 * (int64_t)r;
+    const int64_t row0 = 4 * (int64_t)(r - lane), nrows = 4 * (int64_t)F;
+    {
+        int4 rows[4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
-        cfv[t] = make_int4(v[t], V + F + e[t], V + r, V + F + e[(t + 3) & 3]);
+        for (int t = 0; t < 4; ++t) rows[t] = make_int4(v[t], V + F + e[t], V + r, V + F + e[(t + 3) & 3]);
+        warp_store_rows(stage, rows, reinterpret_cast<int4 *>(c.face_vtx), row0, nrows, lane);
+    }
     if constexpr (ADJ) {
-        const int4 ft = __ldg(reinterpret_cast<const int4 *>(p.face_twin) + r);
+        const int4 ft = valid ? __ldg(reinterpret_cast<const int4 *>(p.face_twin) + r) : make_int4(-1, -1, -1, -1);
         const int32_t tw[4] = {ft.x, ft.y, ft.z, ft.w};
         int32_t base[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) base[t] = cc_base<BND>(p.bnd_word, p.bnd_wpre, e[t]);
-        int4 *cfe = reinterpret_cast<int4 *>(c.face_edge) + 4 * (int64_t)r;
-        int4 *cft = reinterpret_cast<int4 *>(c.face_twin) + 4 * (int64_t)r;
+        for (int t = 0; t < 4; ++t) base[t] = valid ? cc_base<BND>(p.bnd_word, p.bnd_wpre, e[t]) : 0;
         const int32_t h0 = 4 * r;
+        int4 rows[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const int tn = (t + 1) & 3, tp = (t + 3) & 3;
             const int32_t h = h0 + t, hp = h0 + tp;
-            cfe[t] = make_int4(base[t] + (v[t] > v[tn]), base[t] + 2 + (tw[t] >= 0 && tw[t] < h),
-                               base[tp] + 2 + (tw[tp] >= 0 && tw[tp] < hp), base[tp] + (v[t] > v[tp]));
-            const int32_t twn = tw[t] >= 0 ? ((tw[t] & ~3) | ((tw[t] + 1) & 3)) : -1;
-            cft[t] = make_int4(tw[t] >= 0 ? 4 * twn + 3 : -1, 4 * (h0 + tn) + 2, 4 * hp + 1,
-                               tw[tp] >= 0 ? 4 * tw[tp] : -1);
+            rows[t] = make_int4(base[t] + (v[t] > v[tn]), base[t] + 2 + (tw[t] >= 0 && tw[t] < h),
+                                base[tp] + 2 + (tw[tp] >= 0 && tw[tp] < hp), base[tp] + (v[t] > v[tp]));
         }
+        warp_store_rows(stage, rows, reinterpret_cast<int4 *>(c.face_edge), row0, nrows, lane);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int tn = (t + 1) & 3, tp = (t + 3) & 3;
+            const int32_t hp = h0 + tp;
+            const int32_t twn = tw[t] >= 0 ? ((tw[t] & ~3) | ((tw[t] + 1) & 3)) : -1;
+            rows[t] = make_int4(tw[t] >= 0 ? 4 * twn + 3 : -1, 4 * (h0 + tn) + 2, 4 * hp + 1,
+                                tw[tp] >= 0 ? 4 * tw[tp] : -1);
+        }
+        warp_store_rows(stage, rows, reinterpret_cast<int4 *>(c.face_twin), row0, nrows, lane);
     }
 }
 
@@ -273,12 +309,16 @@ ALSUB_D void copy_point(const Frames &fr, int32_t v) {
 
 template <int ORDER>
 __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, VSegs g) {
+    // Work unit = a warp task of 32 consecutive vertices of ONE segment (no divergence between
+    // vertex classes inside a warp); block b takes the same fraction [b/NB, (b+1)/NB) of every
+    // segment's tasks, so a block works on one spatial band of the mesh.
     __shared__ int32_t s_lo[kMaxSeg], s_pre[kMaxSeg + 1];
     const int64_t nblk = gridDim.x, b = blockIdx.x;
     if (threadIdx.x < g.nseg) {
-        const int64_t len = g.len[threadIdx.x];
-        s_lo[threadIdx.x] = (int32_t)(b * len / nblk);
-        s_pre[threadIdx.x] = (int32_t)((b + 1) * len / nblk) - (int32_t)(b * len / nblk);
+        const int64_t tasks = (g.len[threadIdx.x] + 31) >> 5;
+        const int32_t lo = (int32_t)(b * tasks / nblk), hi = (int32_t)((b + 1) * tasks / nblk);
+        s_lo[threadIdx.x] = lo;
+        s_pre[threadIdx.x] = hi - lo;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -292,16 +332,26 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
     }
     __syncthreads();
     const VtxCtx<ORDER> x{p.face_vtx, Topo<ORDER>{p.face_off, p.slot_face}, p.V};
-    const int32_t total = s_pre[g.nseg];
+    const int32_t ntask = s_pre[g.nseg];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
     int s = 0;
-    for (int32_t i = threadIdx.x; i < total; i += blockDim.x) {
-        while (s_pre[s + 1] <= i) ++s;  // items ascend: the segment index only moves forward
-        const int32_t j = s_lo[s] + (i - s_pre[s]);
+    for (int32_t task = warp; task < ntask; task += nwarp) {
+        while (s_pre[s + 1] <= task) ++s;  // tasks ascend: the segment index only moves forward
+        const int32_t j = ((s_lo[s] + (task - s_pre[s])) << 5) + lane;
+        if (j >= g.len[s]) continue;
         const int32_t v = g.start[s] + j;
         const int shift = 2 * (g.level - g.birth[s]);
         const int type = g.type[s];
         const int m1 = g.birth[s] - 1;
-        if (type == 2) {  // edge point born at level m1 + 1
+        if (s == g.hs_seg) {  // edge point born at this level: two half sums from the face kernel
+            const int2 hh = __ldg(g.ehh[m1] + j);
+            if (hh.y < 0) { copy_point(fr, v); continue; }
+            for (int f = 0; f < fr.nb; ++f) {
+                const float *hs = fr.hs + f * fr.hsstride;
+                const P3 acc = ld3c(hs, hh.x) + ld3c(hs, hh.y);
+                st3(fr.Pn + f * fr.Pnstride, v, 0.5f * ld3(fr.P + f * fr.Pstride, v) + 0.0625f * acc);
+            }
+        } else if (type == 2) {  // edge point born at level m1 + 1
             const int2 hh = __ldg(g.ehh[m1] + j);
             if (hh.y < 0) { copy_point(fr, v); continue; }  // boundary: crease module
             int32_t nh, nt;

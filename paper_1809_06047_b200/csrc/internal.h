@@ -48,6 +48,12 @@ void scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *total, 
 size_t sort_scratch_bytes(int64_t n);
 void radix_sort_pairs(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *vals_alt, int64_t n,
                       int bits, void *scratch, cudaStream_t s, Launches &L);
+// One-sweep LSD radix sort (one kernel per 8-bit pass, decoupled look-back per digit).
+// counts = [passes][256] digit histograms (computed here unless counts_ready).  Result in
+// keys/vals when the number of passes is even, else copied back.
+size_t onesweep_scratch_bytes(int64_t n, int passes);
+void radix_sort_onesweep(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *vals_alt, int64_t n, int bits,
+                         int32_t *counts, bool counts_ready, void *scratch, cudaStream_t s, Launches &L);
 // CSR offsets of sorted keys: off[v] = first i with key[i] >= v, v in [0, nkeys] (run-length).
 void offsets_from_sorted(const int32_t *keys, int64_t n, int32_t *off, int32_t nkeys, cudaStream_t s,
                          Launches &L);
@@ -62,7 +68,9 @@ struct Build0 {
     // outputs / work
     int32_t *slot_face;           // [S] (all orders: used for validation & mixed topology)
     int32_t *sort_k, *sort_v, *sort_k2, *sort_v2;  // [S]
-    int32_t *vtx_off, *vtx_slot;  // [V+1], [S] (M^T in CSR)
+    int32_t *vtx_off, *vtx_slot;  // [V+1], [S] (M^T in CSR; vtx_slot aliases sort_v)
+    int32_t *vtx_cnt;             // [V+1] row lengths of M^T
+    int32_t *digits;              // [4][256] radix digit histograms
     int32_t *edge_cnt, *edge_off; // [V], [V]
     int32_t *face_edge, *face_twin, *vtx_slot0;  // [S], [S], [V]
     int2 *edge_hh;                // [E] (smallest slot of the edge, the other slot or -1)
@@ -81,6 +89,7 @@ struct Build0 {
     int32_t E;                    // host-known after the count pass (create) or plan (refine)
     void *scratch;
 };
+size_t build0_scratch_bytes(int32_t V, int32_t S);
 void build0_validate(Build0 &b, cudaStream_t s, Launches &L);
 void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L);  // through edge_off + scalars[0]
 void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L);  // needs b.E
@@ -117,6 +126,10 @@ struct Frames {
     float *Pn;
     int64_t Pstride, Pnstride;
     int nb;
+    // CC levels >= 2: half ring sums of the edge points born at this level, one per parent slot
+    // (= per face of this level), written by the face kernel, read by the vertex kernel
+    float *hs = nullptr;
+    int64_t hsstride = 0;
 };
 
 // Vertex-id segments of a CC level: level-l vertex ids are
@@ -133,6 +146,7 @@ struct VSegs {
     int8_t birth[kMaxSeg];  // level m at which the vertex was created
     const int2 *ehh[kMaxLevels];  // ehh[m-1] = edge pairs of level m-1
     const int32_t *vtx_off0, *vtx_list0, *face_off0, *slot_face0, *vbnd0;
+    int32_t hs_seg;  // segment whose vertex points come from the half sums (-1 = none)
 };
 
 // mode: adj = emit child adjacency (not the last level); topo = emit child faces;

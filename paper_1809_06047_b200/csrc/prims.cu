@@ -5,6 +5,8 @@
 //  * radix_sort_pairs: stable LSD radix sort, 8-bit digits, histogram -> scan -> scatter per pass;
 //    the scatter ranks keys with warp match (__match_any_sync) so equal digits keep their order.
 //  * offsets_from_sorted: CSR column pointer of sorted keys ("segmented scan / run-length").
+#include <algorithm>
+
 #include "internal.h"
 
 namespace alsub {
@@ -208,6 +210,151 @@ void radix_sort_pairs(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *
         scan_exclusive(counts, offs, cnt, nullptr, scan_scratch, s, L);
         k_rs_scatter<<<nblocks, kSortThreads, 0, s>>>(ka, va, n, shift, offs, nblocks, kb, vb);
         L.done("rs_scatter", s);
+        int32_t *t;
+        t = ka; ka = kb; kb = t;
+        t = va; va = vb; vb = t;
+    }
+    if (ka != keys) {
+        cudaMemcpyAsync(keys, ka, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(vals, va, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// One-sweep LSD radix sort: digit histograms of every pass are computed up front (by the caller's
+// fused kernel or k_os_hist), then ONE kernel per pass ranks each tile stably (warp match) and
+// gets its per-digit offset by a decoupled look-back over the previous tiles (256 digits looked
+// back in parallel, one per thread).
+// ------------------------------------------------------------------------------------------
+constexpr int kOsThreads = 256;
+constexpr int kOsItems = 8;
+constexpr int kOsTile = kOsThreads * kOsItems;
+
+static int64_t os_tiles(int64_t n) { return ceil_div(n > 0 ? n : 1, kOsTile); }
+
+size_t onesweep_scratch_bytes(int64_t n, int passes) {
+    // per pass: tile counter (4 B, padded to 64) + ntiles x 256 status words
+    return (size_t)passes * (64 + (size_t)os_tiles(n) * 256 * 4);
+}
+
+__global__ void __launch_bounds__(kOsThreads) k_os_hist(const int32_t *__restrict__ keys, int64_t n, int passes,
+                                                      int32_t *__restrict__ counts) {
+    __shared__ int h[4][256];
+    for (int p = 0; p < passes; ++p) h[p][threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = (uint32_t)keys[i];
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1);
+    }
+    __syncthreads();
+    for (int p = 0; p < passes; ++p)
+        if (h[p][threadIdx.x]) atomicAdd(counts + 256 * p + threadIdx.x, h[p][threadIdx.x]);
+}
+
+constexpr uint32_t kOsAgg = 1u << 30, kOsInc = 2u << 30, kOsMask = (1u << 30) - 1;
+
+__global__ void __launch_bounds__(kOsThreads) k_os_pass(const int32_t *__restrict__ keys, const int32_t *__restrict__ vals,
+                                                      int64_t n, int shift, const int32_t *__restrict__ counts,
+                                                      uint32_t *status, unsigned *counter, int32_t *__restrict__ okeys,
+                                                      int32_t *__restrict__ ovals) {
+    __shared__ int s_tile;
+    __shared__ int s_base[256];       // global exclusive prefix of the digit + this tile's look-back
+    __shared__ int s_cnt[256];        // this tile's digit counts
+    __shared__ int wc[kOsThreads / 32][257];
+    __shared__ int s_run[256];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) s_tile = (int)atomicAdd(counter, 1u);
+    // global digit prefix (exclusive scan of the 256 pass counts; one warp-free serial-in-smem pass)
+    s_cnt[tid] = counts[tid];
+    __syncthreads();
+    if (tid == 0) {
+        int acc = 0;
+        for (int d = 0; d < 256; ++d) { const int c = s_cnt[d]; s_cnt[d] = acc; acc += c; }
+    }
+    __syncthreads();
+    s_base[tid] = s_cnt[tid];
+    s_run[tid] = 0;
+    s_cnt[tid] = 0;
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t base = (int64_t)tile * kOsTile;
+    int32_t key[kOsItems], val[kOsItems], rank[kOsItems];
+    unsigned dig[kOsItems];
+    // stable local ranks, round by round (element order = base + k * 256 + tid)
+    for (int k = 0; k < kOsItems; ++k) {
+        for (int w = 0; w < kOsThreads / 32; ++w) wc[w][tid] = 0;
+        __syncthreads();
+        const int64_t i = base + k * kOsThreads + tid;
+        const bool valid = i < n;
+        key[k] = valid ? keys[i] : 0;
+        val[k] = valid ? vals[i] : 0;
+        dig[k] = valid ? (((uint32_t)key[k] >> shift) & 255u) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, dig[k]);
+        const int r = __popc(peers & ((1u << lane) - 1u));
+        if (valid && (__ffs(peers) - 1) == lane) wc[warp][dig[k]] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            int pos = s_run[dig[k]] + r;
+            for (int w = 0; w < warp; ++w) pos += wc[w][dig[k]];
+            rank[k] = pos;
+        }
+        __syncthreads();
+        int add = 0;
+        for (int w = 0; w < kOsThreads / 32; ++w) add += wc[w][tid];
+        s_run[tid] += add;
+        __syncthreads();
+    }
+    // decoupled look-back, one digit per thread
+    {
+        const int d = tid;
+        const uint32_t mine = (uint32_t)s_run[d];
+        uint32_t *st = status + (int64_t)tile * 256 + d;
+        if (tile == 0) {
+            atomicExch(st, kOsInc | mine);
+        } else {
+            atomicExch(st, kOsAgg | mine);
+            uint32_t prefix = 0;
+            for (int p = tile - 1; p >= 0; --p) {
+                uint32_t w;
+                do {
+                    w = atomicAdd(status + (int64_t)p * 256 + d, 0u);
+                } while ((w >> 30) == 0);
+                prefix += w & kOsMask;
+                if ((w >> 30) == 2) break;
+            }
+            atomicExch(st, kOsInc | (prefix + mine));
+            s_base[d] += (int)prefix;
+        }
+    }
+    __syncthreads();
+    for (int k = 0; k < kOsItems; ++k) {
+        const int64_t i = base + k * kOsThreads + tid;
+        if (i < n) {
+            const int pos = s_base[dig[k]] + rank[k];
+            okeys[pos] = key[k];
+            ovals[pos] = val[k];
+        }
+    }
+}
+
+void radix_sort_onesweep(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *vals_alt, int64_t n, int bits,
+                         int32_t *counts, bool counts_ready, void *scratch, cudaStream_t s, Launches &L) {
+    int passes = (bits + 7) / 8;
+    if (passes < 1) passes = 1;
+    if (n <= 1) return;
+    if (!counts_ready) {
+        cudaMemsetAsync(counts, 0, sizeof(int32_t) * 256 * passes, s);
+        k_os_hist<<<(unsigned)std::min<int64_t>(ceil_div(n, kOsThreads), 4 * 148), kOsThreads, 0, s>>>(keys, n, passes, counts);
+        L.done("os_hist", s);
+    }
+    cudaMemsetAsync(scratch, 0, onesweep_scratch_bytes(n, passes), s);
+    const int64_t tiles = os_tiles(n);
+    int32_t *ka = keys, *va = vals, *kb = keys_alt, *vb = vals_alt;
+    for (int p = 0; p < passes; ++p) {
+        char *base = (char *)scratch + (size_t)p * (64 + (size_t)tiles * 256 * 4);
+        k_os_pass<<<(unsigned)tiles, kOsThreads, 0, s>>>(ka, va, n, 8 * p, counts + 256 * p, (uint32_t *)(base + 64),
+                                                         (unsigned *)base, kb, vb);
+        L.done("os_pass", s);
         int32_t *t;
         t = ka; ka = kb; kb = t;
         t = va; va = vb; vb = t;
