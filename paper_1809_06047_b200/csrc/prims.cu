@@ -280,15 +280,21 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(const int32_t *__restric
     const int64_t base = (int64_t)tile * kOsTile;
     int32_t key[kOsItems], val[kOsItems], rank[kOsItems];
     unsigned dig[kOsItems];
-    // stable local ranks, round by round (element order = base + k * 256 + tid)
+    // load the whole tile first (all loads in flight together), then rank from registers
+#pragma unroll
     for (int k = 0; k < kOsItems; ++k) {
-        for (int w = 0; w < kOsThreads / 32; ++w) wc[w][tid] = 0;
-        __syncthreads();
         const int64_t i = base + k * kOsThreads + tid;
         const bool valid = i < n;
         key[k] = valid ? keys[i] : 0;
         val[k] = valid ? vals[i] : 0;
         dig[k] = valid ? (((uint32_t)key[k] >> shift) & 255u) : 256u;
+    }
+    // stable local ranks, round by round (element order = base + k * 256 + tid)
+#pragma unroll
+    for (int k = 0; k < kOsItems; ++k) {
+        for (int w = 0; w < kOsThreads / 32; ++w) wc[w][tid] = 0;
+        __syncthreads();
+        const bool valid = dig[k] < 256u;
         const unsigned peers = __match_any_sync(0xffffffffu, dig[k]);
         const int r = __popc(peers & ((1u << lane) - 1u));
         if (valid && (__ffs(peers) - 1) == lane) wc[warp][dig[k]] = __popc(peers);

@@ -1,5 +1,5 @@
 """Summarise an ncu --set full report (raw page) into a markdown table + JSON (per kernel launch)."""
-import csv, json, subprocess, sys
+import csv, json, os, subprocess, sys
 rep = sys.argv[1]
 out_md = sys.argv[2] if len(sys.argv) > 2 else None
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -36,3 +36,13 @@ print('\n'.join(lines))
 if out_md:
     json.dump(rows, open(out_md.replace('.md', '.json'), 'w'), indent=1)
     open(out_md, 'w').write('\n'.join(lines) + '\n')
+    # per (kernel family, level) DRAM bytes for bench.py's roofline.traffic; the CC level kernels of
+    # one refine are captured in launch order, so launch index == level for cc_face/cc_edge/cc_vertex
+    summ = {}
+    for d in rows:
+        base = d['kernel'].split('<')[0].replace('k_', '', 1)
+        fam = {'cc_face_quad': 'cc_face', 'cc_face_gen': 'cc_face'}.get(base, base)
+        key = f"{fam}@L{d['launch'] if fam != 'cc_face' else sum(1 for x in rows[:rows.index(d)] if x['kernel'].startswith(('k_cc_face',)))}"
+        summ[key] = {'dram_bytes': d['dram__bytes_read.sum'] + d['dram__bytes_write.sum'],
+                     'time_us': d['gpu__time_duration.sum'] * 1e6, 'kernel': d['kernel']}
+    json.dump({'source': rep, 'kernels': summ}, open(os.path.join(os.path.dirname(out_md), 'ncu_summary.json'), 'w'), indent=1)
