@@ -383,7 +383,7 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
             c.pos = A<float>(m, 3 * c.V, s, ML, ok);
             if (has_child) {
                 c.face_twin = A<int32_t>(m, c.S, s, ML, ok);
-                if (scheme != ALSUB_CATMULL_CLARK) c.vtx_slot0 = A<int32_t>(m, c.V, s, ML, ok);
+                if (scheme == ALSUB_LOOP) c.vtx_slot0 = A<int32_t>(m, c.V, s, ML, ok);
                 if (scheme != ALSUB_SQRT3) {
                     c.face_edge = A<int32_t>(m, c.S, s, ML, ok);
                     c.edge_hh = A<int2>(m, c.E, s, ML, ok);
@@ -426,6 +426,29 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
 }
 
 // ---------------- the level loop ----------------
+// vertex-id segments of sqrt3 level l: [V0 | F0 | F1 | ... | F_{l-1}]
+static VSegs make_segs_s3(alsub_mesh *m, int l) {
+    VSegs g{};
+    g.level = l;
+    g.hs_seg = -1;
+    int n = 0;
+    int32_t mult = 1;
+    for (int k = 0; k < l; ++k) mult *= 3;
+    g.start[n] = 0; g.len[n] = m->V0; g.type[n] = 0; g.birth[n] = 0; g.mult[n] = mult; ++n;
+    for (int k = 1; k <= l; ++k) {
+        const LevelHost &q = m->lv[k - 1];
+        mult /= 3;
+        g.start[n] = (int32_t)q.V; g.len[n] = (int32_t)q.F; g.type[n] = 1; g.birth[n] = (int8_t)k; g.mult[n] = mult;
+        g.fvx[k - 1] = q.face_vtx;
+        g.ftw[k - 1] = q.face_twin;
+        ++n;
+    }
+    g.nseg = n;
+    g.vtx_off0 = m->b0.vtx_off; g.vtx_list0 = m->b0.vtx_slot; g.face_off0 = m->in_face_off;
+    g.slot_face0 = m->b0.slot_face; g.vbnd0 = m->b0.vbnd;
+    return g;
+}
+
 // vertex-id segments of CC level l (see VSegs in internal.h)
 static VSegs make_segs(alsub_mesh *m, int l) {
     VSegs g{};
@@ -476,7 +499,8 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
             loop_level(p, c, fr, true, adj, m->scratch, s, L);
             if (special) crease_level(p, c, fr, (int32_t)P.V, 1, true, s, L);
         } else {
-            sqrt3_level(p, c, fr, true, adj, m->scratch, s, L);
+            VSegs g = make_segs_s3(m, l);
+            sqrt3_level(p, c, fr, true, adj, g, s, L);
         }
     }
 }
@@ -744,7 +768,8 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
                 loop_level(p, c, fr, false, false, m->scratch, s, L);
                 if (special) crease_level(p, c, fr, (int32_t)Pl.V, 1, false, s, L);
             } else {
-                sqrt3_level(p, c, fr, false, false, m->scratch, s, L);
+                VSegs g = make_segs_s3(m, l);
+                sqrt3_level(p, c, fr, false, false, g, s, L);
             }
             P = Pn;
         }

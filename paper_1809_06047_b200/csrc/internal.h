@@ -147,6 +147,9 @@ struct VSegs {
     const int2 *ehh[kMaxLevels];  // ehh[m-1] = edge pairs of level m-1
     const int32_t *vtx_off0, *vtx_list0, *face_off0, *slot_face0, *vbnd0;
     int32_t hs_seg;  // segment whose vertex points come from the half sums (-1 = none)
+    // sqrt3: slot multiplier 3^(l-m) per segment and the level m-1 face rows
+    int32_t mult[kMaxSeg];
+    const int32_t *fvx[kMaxLevels], *ftw[kMaxLevels];
 };
 
 // mode: adj = emit child adjacency (not the last level); topo = emit child faces;
@@ -155,7 +158,7 @@ void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo,
               cudaStream_t s, Launches &L);
 void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
                 cudaStream_t s, Launches &L);
-void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
+void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &g,
                  cudaStream_t s, Launches &L);
 // crease / boundary module (crease.cu): ONE kernel per level -- edge and vertex overrides and
 // (inherit) the child special lists.  ep_base = first edge-point id; scheme 0 CC, 1 Loop.

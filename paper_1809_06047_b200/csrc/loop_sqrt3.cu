@@ -10,6 +10,8 @@
 //         distinct edges x < e sharing a triangle with e, ascending]; base_e = scan of counts.
 // sqrt3:  f = barycenters; S = (1 - alpha) p + alpha/n sum p_j (Eqs. sqrt2, alpha);
 //         child 3i+t = (p_k, fp_F(l,k), fp_i) (CCW reading R13); closed only.
+#include <algorithm>
+
 #include "internal.h"
 
 namespace alsub {
@@ -236,79 +238,175 @@ void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool top
 // ------------------------------------------------------------------------------------------
 // sqrt3
 // ------------------------------------------------------------------------------------------
-template <bool ADJ>
-__global__ void __launch_bounds__(kThreads) k_s3_face(LevelDev p, ChildDev c, Frames fr, bool topo) {
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= p.F) return;
-    const int32_t V = p.V;
-    int32_t v[3];
+// face kernel: barycenter (P:L1010 with (1,2,3) -> 1/3) and the three children (p_k, fp_F(l,k), fp_i)
+// (CCW reading R13) + child twins; a warp's 32 x 36 B of child rows are staged in
+// shared memory and written as 9 coalesced 128 B stores.
+ALSUB_D void warp_store_9(int32_t *stage, const int32_t (&v)[9], int32_t *dst, int64_t w0, int64_t n, int lane) {
 #pragma unroll
-    for (int t = 0; t < 3; ++t) v[t] = __ldg(p.face_vtx + 3 * i + t);
-    for (int f = 0; f < fr.nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
-        const P3 s = ld3(P, v[0]) + ld3(P, v[1]) + ld3(P, v[2]);
-        st3(fr.Pn + f * fr.Pnstride, (int64_t)V + i, (1.0f / 3.0f) * s);
+    for (int k = 0; k < 9; ++k) stage[lane * 9 + k] = v[k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        const int64_t o = w0 + k * 32 + lane;
+        if (o < n) dst[o] = stage[k * 32 + lane];
     }
-    if (!topo) return;
-    int32_t tw[3];
-#pragma unroll
-    for (int t = 0; t < 3; ++t) tw[t] = __ldg(p.face_twin + 3 * i + t);
-    int32_t *cfv = c.face_vtx + 9 * (int64_t)i;
+    __syncwarp();
+}
+
+template <bool ADJ, int NBC>
+__global__ void __launch_bounds__(kThreads) k_s3_face(LevelDev p, ChildDev c, Frames fr, bool topo) {
+    __shared__ int32_t s_stage[kThreads / 32][9 * 32];
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < p.F;
+    const int lane = threadIdx.x & 31;
+    const int32_t V = p.V;
+    int32_t v[3], tw[3];
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
-        cfv[3 * t + 0] = v[t];
-        cfv[3 * t + 1] = V + tw[t] / 3;
-        cfv[3 * t + 2] = V + i;
+        v[t] = valid ? __ldg(p.face_vtx + 3 * i + t) : 0;
+        tw[t] = valid ? __ldg(p.face_twin + 3 * i + t) : 0;
     }
+    const int nb = NBC ? NBC : fr.nb;
+    for (int f = 0; f < nb; ++f) {
+        const float *P = fr.P + f * fr.Pstride;
+        const P3 s = ld3(P, v[0]) + ld3(P, v[1]) + ld3(P, v[2]);
+        if (valid) st3(fr.Pn + f * fr.Pnstride, (int64_t)V + i, (1.0f / 3.0f) * s);
+    }
+    if (!topo) return;
+    int32_t *stage = s_stage[threadIdx.x >> 5];
+    const int64_t w0 = 9 * (int64_t)(i - lane), n = 9 * (int64_t)p.F;
+    int32_t rows[9];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        rows[3 * t + 0] = v[t];
+        rows[3 * t + 1] = V + tw[t] / 3;
+        rows[3 * t + 2] = V + i;
+    }
+    warp_store_9(stage, rows, c.face_vtx, w0, n, lane);
     if constexpr (ADJ) {
-        int32_t *cft = c.face_twin + 9 * (int64_t)i;
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
             const int32_t a = tw[t], b = tw[(t + 2) % 3];
-            const int32_t na = a / 3, ua = a % 3, nb = b / 3, wb = b % 3;
-            cft[3 * t + 0] = 3 * (3 * na + (ua + 1) % 3) + 2;
-            cft[3 * t + 1] = 3 * (3 * na + ua) + 1;
-            cft[3 * t + 2] = 3 * (3 * nb + wb) + 0;
+            const int32_t na = a / 3, ua = a % 3, nb2 = b / 3, wb = b % 3;
+            rows[3 * t + 0] = 3 * (3 * na + (ua + 1) % 3) + 2;
+            rows[3 * t + 1] = 3 * (3 * na + ua) + 1;
+            rows[3 * t + 2] = 3 * (3 * nb2 + wb) + 0;
         }
-        c.vtx_slot0[V + i] = 9 * i + 2;
+        warp_store_9(stage, rows, c.face_twin, w0, n, lane);
     }
 }
 
-template <bool ADJ>
-__global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, ChildDev c, Frames fr) {
-    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= p.V) return;
-    const int32_t h0 = __ldg(p.vtx_slot0 + v);
-    if constexpr (ADJ) c.vtx_slot0[v] = h0 >= 0 ? 3 * h0 : -1;
-    for (int f = 0; f < fr.nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
-        float *Pn = fr.Pn + f * fr.Pnstride;
-        const P3 pv = ld3(P, v);
-        if (h0 < 0) { st3(Pn, v, pv); continue; }
-        P3 acc = p3zero();
-        int32_t h = h0, n = 0;
-        do {
-            acc = acc + ld3(P, __ldg(p.face_vtx + tri_next(h)));
-            ++n;
-            h = __ldg(p.face_twin + tri_prev(h));
-        } while (h >= 0 && h != h0 && n < p.S);
-        const float alpha = sqrt3_alpha(n);
-        st3(Pn, v, (1.0f - alpha) * pv + (alpha / (float)n) * acc);
+// vertex kernel: S = (1 - alpha) p + alpha/n sum p_j (Eqs. sqrt2, alpha) over the closed-form row
+// of M of every vertex class: a vertex born at level m has level-l slots
+// 3^(l-m) x its level-m slots; a face point of face i (level m-1) has level-m slots
+// {9i + 3t + 2} u {3 tw_t + 1}; face points born at this level read their six neighbours straight
+// from the parent rows (the triangle's corners and the three neighbouring face points).
+template <int NBC>
+__global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, VSegs g) {
+    __shared__ int32_t s_lo[kMaxSeg], s_pre[kMaxSeg + 1];
+    const int64_t nblk = gridDim.x, b = blockIdx.x;
+    if (threadIdx.x < g.nseg) {
+        const int64_t tasks = (g.len[threadIdx.x] + 31) >> 5;
+        const int32_t lo = (int32_t)(b * tasks / nblk), hi = (int32_t)((b + 1) * tasks / nblk);
+        s_lo[threadIdx.x] = lo;
+        s_pre[threadIdx.x] = hi - lo;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t acc = 0;
+        for (int s = 0; s < g.nseg; ++s) {
+            const int32_t c = s_pre[s];
+            s_pre[s] = acc;
+            acc += c;
+        }
+        s_pre[g.nseg] = acc;
+    }
+    __syncthreads();
+    const int32_t ntask = s_pre[g.nseg];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    const int nb = NBC ? NBC : fr.nb;
+    int s = 0;
+    for (int32_t task = warp; task < ntask; task += nwarp) {
+        while (s_pre[s + 1] <= task) ++s;
+        const int32_t j = ((s_lo[s] + (task - s_pre[s])) << 5) + lane;
+        if (j >= g.len[s]) continue;
+        const int32_t v = g.start[s] + j;
+        const int32_t mult = g.mult[s];
+        if (g.type[s] == 1 && g.birth[s] == g.level) {
+            // face point of parent face j: neighbours = its corners + the 3 adjacent face points
+            const int m1 = g.birth[s] - 1;
+            int32_t nbv[6];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                nbv[t] = __ldg(g.fvx[m1] + 3 * j + t);
+                nbv[3 + t] = g.start[s] + __ldg(g.ftw[m1] + 3 * j + t) / 3;
+            }
+            constexpr float alpha = 1.0f / 3.0f;  // alpha_6 = (4 - 2 cos(pi/3)) / 9
+            for (int f = 0; f < nb; ++f) {
+                const float *P = fr.P + f * fr.Pstride;
+                P3 acc = ld3(P, nbv[0]);
+#pragma unroll
+                for (int k = 1; k < 6; ++k) acc = acc + ld3(P, nbv[k]);
+                st3(fr.Pn + f * fr.Pnstride, v, (1.0f - alpha) * ld3(P, v) + (alpha / 6.0f) * acc);
+            }
+            continue;
+        }
+        int32_t sl[6];
+        int32_t n = 0;
+        const int32_t *list = nullptr;
+        if (g.type[s] == 1) {
+            const int m1 = g.birth[s] - 1;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                sl[t] = (9 * j + 3 * t + 2) * mult;
+                sl[3 + t] = (3 * __ldg(g.ftw[m1] + 3 * j + t) + 1) * mult;
+            }
+            n = 6;
+        } else {
+            const int32_t o = __ldg(g.vtx_off0 + j);
+            n = __ldg(g.vtx_off0 + j + 1) - o;
+            list = g.vtx_list0 + o;
+        }
+        const float alpha = n > 0 ? sqrt3_alpha(n) : 0.0f;
+        for (int f = 0; f < nb; ++f) {
+            const float *P = fr.P + f * fr.Pstride;
+            float *Pn = fr.Pn + f * fr.Pnstride;
+            const P3 pv = ld3(P, v);
+            if (n == 0) { st3(Pn, v, pv); continue; }
+            P3 acc = p3zero();
+            if (list) {
+                for (int32_t k = 0; k < n; ++k) acc = acc + ld3(P, __ldg(p.face_vtx + tri_next(__ldg(list + k) * mult)));
+            } else {
+                int32_t nbv[6];
+#pragma unroll
+                for (int k = 0; k < 6; ++k) nbv[k] = __ldg(p.face_vtx + tri_next(sl[k]));
+#pragma unroll
+                for (int k = 0; k < 6; ++k) acc = acc + ld3(P, nbv[k]);
+            }
+            st3(Pn, v, (1.0f - alpha) * pv + (alpha / (float)n) * acc);
+        }
     }
 }
 
-void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
+void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &g,
                  cudaStream_t s, Launches &L) {
-    (void)scratch;
     const bool A = adj && topo;
+    const bool one = fr.nb == 1;
     if (p.F > 0) {
-        if (A) k_s3_face<true><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
-        else k_s3_face<false><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+        if (A) {
+            if (one) k_s3_face<true, 1><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+            else k_s3_face<true, 0><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+        } else {
+            if (one) k_s3_face<false, 1><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+            else k_s3_face<false, 0><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+        }
         L.done("s3_face", s);
     }
     if (p.V > 0) {
-        if (A) k_s3_vertex<true><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
-        else k_s3_vertex<false><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
+        const unsigned nblk = (unsigned)std::max<int64_t>(grid_for(p.V, 4 * kThreads),
+                                                          std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
+        if (one) k_s3_vertex<1><<<nblk, kThreads, 0, s>>>(p, fr, g);
+        else k_s3_vertex<0><<<nblk, kThreads, 0, s>>>(p, fr, g);
         L.done("s3_vertex", s);
     }
 }
