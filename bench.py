@@ -318,6 +318,14 @@ def run_alsub(args):
     if not args.no_e2e:
         e2e = run_e2e(args, mesh, levels, Fout, Vout, dev, flush)
 
+    others = None
+    frames = None
+    if rank == 0 and world == 1 and not args.no_other_configs:
+        others = other_configs(dev, flush, peak)
+        fa = argparse.Namespace(**vars(args))
+        fa.frames, fa.warmup = 64, 3
+        frames = run_frames(fa, 0, 1, dev, flush, lambda: None, lambda x: x, peak, peak_src, emit=False)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_baseline(mg.armor9k(), levels, "armor9k (config 3), the full workload")
@@ -336,12 +344,51 @@ def run_alsub(args):
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches_per_step * K), "launches_per_step": int(launches_per_step),
                 "clocks": sampler.summary(), "levels": per_level, "profile_step_ms": prof_step,
+                "other_configs": others, "frames_config5_sample": frames,
                 "paper_context": PAPER_CONTEXT}
         print(json.dumps(line), flush=True)
     m.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def other_configs(dev, flush, peak, reps=20):
+    """Graph-replayed timings of the other BASELINE configs:
+    refined faces/s of the final level and the SURVEY per-level compulsory-byte rate."""
+    import torch
+    from paper_1809_06047_b200 import Mesh
+    cases = [("config1_cube_cc_L3", mg.cube(), "cc", 3), ("config2a_ico_loop_L6", mg.icosahedron(), "loop", 6),
+             ("config2b_creased_tet_loop_L6", mg.tetrahedron(creased=True), "loop", 6),
+             ("config2b_creased_tet_cc_L6", mg.tetrahedron(creased=True), "cc", 6),
+             ("config4_torus100k_sqrt3_L5", mg.torus100k(), "sqrt3", 5)]
+    out = {}
+    stream = torch.cuda.current_stream()
+    for name, mesh, scheme, L in cases:
+        m = Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"])
+        for _ in range(4):
+            m.refine(scheme, L)
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            m.refine(scheme, L)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ts.sort()
+        ms = ts[len(ts) // 2]
+        c = m.counts(L)
+        cp = m.counts(L - 1)
+        row = {"scheme": scheme, "levels": L, "faces_out": c["faces"], "verts_out": c["verts"], "ms_median": ms,
+               "faces_per_s": c["faces"] / (ms / 1e3), "launches": m.last_launch_count}
+        if scheme == "sqrt3":  # final step bytes: read 12F + 12F (face rows, twins) + 12V, write 36F + 12V'
+            fb = 24 * cp["faces"] + 12 * cp["verts"] + 36 * cp["faces"] + 12 * c["verts"]
+            row["final_step_compulsory_bytes"] = fb
+        out[name] = row
+        m.close()
+    return out
 
 
 def run_e2e(args, mesh, levels, Fout, Vout, dev, flush):
@@ -380,7 +427,7 @@ def run_e2e(args, mesh, levels, Fout, Vout, dev, flush):
             "path": "alsub_mesh_create(host) + alsub_refine + alsub_level_positions/topology(pinned host)"}
 
 
-def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, peak_src):
+def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, peak_src, emit=True):
     """Config 5: static-mode frames, armor50k CC level 4, 4096 frames sharded over ranks."""
     import torch
     from paper_1809_06047_b200 import Mesh
@@ -418,6 +465,10 @@ def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, pea
     value = total_frames * Fout / (ms / 1000.0)
     bytes_per_frame = sum(12 * cnt[l]["V"] + 12 * cnt[l + 1]["V"] for l in range(levels))
     gbps = nsteps * nb * bytes_per_frame / (ms * 1e6 / 1.0) if ms else None
+    if not emit:
+        m.close()
+        return {"frames": total_frames, "faces_per_frame": Fout, "ms_per_batch_of_8": ms / nsteps,
+                "faces_per_s": value, "position_GBps": gbps, "position_frac": gbps / peak if gbps else None}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "faces/s", "n_gpus": world, "steps": nsteps,
                 "warmup": args.warmup, "ms_per_step": ms / nsteps, "higher_is_better": True, "scaling": "strong",
@@ -448,6 +499,7 @@ def main():
     ap.add_argument("--ref-levels", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

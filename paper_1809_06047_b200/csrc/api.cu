@@ -618,6 +618,7 @@ extern "C" alsub_status alsub_level_counts(const alsub_mesh *m, int32_t level, a
 }
 
 __global__ void k_iota_stride(int32_t *o, int64_t n, int32_t c) {
+    ALSUB_GRID_WAIT();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) o[i] = (int32_t)(c * i);
 }
@@ -653,7 +654,7 @@ extern "C" alsub_status alsub_level_topology(const alsub_mesh *mc, int32_t level
         } else {
             int32_t *d = is_device_ptr(face_off) ? face_off : A<int32_t>(m, L->F + 1, s, tmp, ok);
             if (!ok) return fail(ALSUB_E_NOMEM, "export buffer");
-            k_iota_stride<<<grid_for(L->F + 1), kThreads, 0, s>>>(d, L->F + 1, L->order);
+            launch(Ln, "iota", k_iota_stride, dim3(grid_for(L->F + 1)), dim3(kThreads), 0, s, d, (int64_t)(L->F + 1), (int32_t)L->order);
             if (d != face_off) CU(copy_out(face_off, d, sizeof(int32_t) * ((size_t)L->F + 1), s));
         }
     }
@@ -801,3 +802,14 @@ extern "C" void alsub_mesh_destroy(alsub_mesh *m) {
 
 extern "C" const char *alsub_last_error(void) { return g_err.c_str(); }
 extern "C" const char *alsub_version(void) { return "alsub-b200 0.1 (sm_100a)"; }
+
+namespace alsub {
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("ALSUB_NO_PDL");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1;
+}
+}  // namespace alsub

@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(kThreads) k_b0_prep(const int32_t *__restrict_
                                                     int32_t *__restrict__ sk, int32_t *__restrict__ sv,
                                                     int32_t *__restrict__ vtx_cnt, int32_t *__restrict__ digits,
                                                     int32_t *flags) {
+    ALSUB_GRID_WAIT();
     __shared__ int h[4][256];
     for (int p = 0; p < passes; ++p) h[p][threadIdx.x] = 0;
     __syncthreads();
@@ -103,6 +104,7 @@ ALSUB_D WarpCand warp_cand(const int32_t *face_vtx, const int32_t *vtx_slot, T0 
 // the diagonal)
 __global__ void k_edge_count(const int32_t *__restrict__ face_vtx, const int32_t *__restrict__ vtx_off,
                              const int32_t *__restrict__ vtx_slot, T0 tp, int32_t V, int32_t *__restrict__ cnt) {
+    ALSUB_GRID_WAIT();
     const int32_t j = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (j >= V) return;
@@ -145,6 +147,7 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
                             int32_t *__restrict__ face_twin, int2 *__restrict__ edge_hh,
                             uint32_t *__restrict__ bnd_word, int32_t *__restrict__ vbnd,
                             int32_t *__restrict__ scalars, int32_t *flags, int32_t *__restrict__ slot0) {
+    ALSUB_GRID_WAIT();
     const int32_t j = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (j >= V) return;
@@ -198,6 +201,7 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
 // (reading R18); open fans (bowties) are allowed and end up as corners.
 __global__ void k_check_fans(const int32_t *__restrict__ face_twin, const int32_t *__restrict__ vtx_off,
                              const int32_t *__restrict__ slot0, T0 tp, int32_t V, int32_t *flags) {
+    ALSUB_GRID_WAIT();
     int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= V) return;
     int32_t h0 = slot0[v];
@@ -234,23 +238,39 @@ __global__ void __launch_bounds__(kThreads) k_b0_flags(const int32_t *__restrict
                                                      int32_t nw, float *__restrict__ edge_sigma,
                                                      int32_t *__restrict__ edge_cidx, int32_t *__restrict__ flag,
                                                      int32_t *__restrict__ wcnt, int32_t *flags) {
-    const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    ALSUB_GRID_WAIT();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < E && edge_hh[t].y < 0) atomicOr(flag + t, 1);
     if (t < nw) wcnt[t] = __popc(bnd_word[t]);
-    if (t >= K) return;
-    const int32_t a = crease[2 * t], b = crease[2 * t + 1];
-    const float sg = sigma[t];
-    if (a < 0 || a >= V || b < 0 || b >= V || a == b || !(sg >= 0.0f)) { atomicOr(flags, kFlagCrease); return; }
-    const int32_t j = max(a, b), i = min(a, b);
-    int32_t e = -1;
-    for (int32_t p = vtx_off[j]; p < vtx_off[j + 1]; ++p) {
-        const int32_t h = vtx_slot[p];
-        if (face_vtx[tp.next(h)] == i) { e = face_edge[h]; break; }
-        const int32_t hp = tp.prev(h);
-        if (face_vtx[hp] == i) { e = face_edge[hp]; break; }
+    // one warp per crease pair: the lanes test the incident slots of max(a, b) in parallel
+    const int64_t k = t >> 5;
+    const int lane = threadIdx.x & 31;
+    if (k >= K) return;
+    const int32_t a = crease[2 * k], b = crease[2 * k + 1];
+    const float sg = sigma[k];
+    if (a < 0 || a >= V || b < 0 || b >= V || a == b || !(sg >= 0.0f)) {
+        if (lane == 0) atomicOr(flags, kFlagCrease);
+        return;
     }
+    const int32_t j = max(a, b), i = min(a, b);
+    const int32_t o0 = vtx_off[j], n = vtx_off[j + 1] - o0;
+    int32_t e = -1;
+    for (int32_t q0 = 0; q0 < n; q0 += 32) {
+        int32_t cand = -1;
+        if (q0 + lane < n) {
+            const int32_t h = vtx_slot[o0 + q0 + lane];
+            if (face_vtx[tp.next(h)] == i) cand = face_edge[h];
+            else {
+                const int32_t hp = tp.prev(h);
+                if (face_vtx[hp] == i) cand = face_edge[hp];
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, cand >= 0);
+        if (m) { e = __shfl_sync(0xffffffffu, cand, __ffs(m) - 1); break; }
+    }
+    if (lane != 0) return;
     if (e < 0) { atomicOr(flags, kFlagCrease); return; }
-    if (atomicCAS(edge_cidx + e, -1, t) != -1) { atomicOr(flags, kFlagCrease); return; }
+    if (atomicCAS(edge_cidx + e, -1, (int32_t)k) != -1) { atomicOr(flags, kFlagCrease); return; }
     if (sg > 0.0f && edge_hh[e].y >= 0) {  // boundary edges are infinitely sharp anyway (R19)
         edge_sigma[e] = sg;
         atomicOr(flag + e, 1);
@@ -263,6 +283,7 @@ __global__ void __launch_bounds__(kThreads) k_b0_special(const int2 *__restrict_
                                                        const int32_t *__restrict__ flag, const int32_t *__restrict__ off,
                                                        T0 tp, int32_t E, SpEdge *__restrict__ sp,
                                                        int32_t *__restrict__ sv_cnt) {
+    ALSUB_GRID_WAIT();
     const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E || !flag[e]) return;
     const int2 hh = edge_hh[e];
@@ -285,6 +306,7 @@ __global__ void __launch_bounds__(kThreads) k_b0_special(const int2 *__restrict_
 __global__ void __launch_bounds__(kThreads) k_b0_svlist(const SpEdge *__restrict__ sp, const int32_t *__restrict__ count,
                                                       int32_t cap, const int32_t *__restrict__ sv_off,
                                                       int32_t *__restrict__ sv_cur, int32_t *__restrict__ sv_list) {
+    ALSUB_GRID_WAIT();
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= cap || j >= *count) return;
     const int32_t ia = sp[j].ia, ib = sp[j].ib;
@@ -296,6 +318,7 @@ __global__ void __launch_bounds__(kThreads) k_b0_svlist(const SpEdge *__restrict
 __global__ void __launch_bounds__(kThreads) k_b0_svsort(int32_t V, const int32_t *__restrict__ sv_off,
                                                       int32_t *__restrict__ sv_list, int32_t *__restrict__ sv_vtx,
                                                       int32_t *__restrict__ scalars) {
+    ALSUB_GRID_WAIT();
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v == 0) scalars[3] = V;
     if (v >= V) return;
@@ -327,9 +350,8 @@ void build0_validate(Build0 &b, cudaStream_t s, Launches &L) {
     cudaMemsetAsync(b.vtx_cnt, 0, sizeof(int32_t) * ((size_t)b.V + 1), s);
     cudaMemsetAsync(b.digits, 0, sizeof(int32_t) * 256 * 4, s);
     if (b.F > 0) {
-        k_b0_prep<<<grid_for(b.F), kThreads, 0, s>>>(b.face_off, b.face_vtx, b.F, b.V, passes_for(b.V), b.slot_face,
+        launch(L, "b0_prep", k_b0_prep, dim3(grid_for(b.F)), dim3(kThreads), 0, s, b.face_off, b.face_vtx, b.F, b.V, passes_for(b.V), b.slot_face,
                                                      b.sort_k, b.sort_v, b.vtx_cnt, b.digits, b.flags);
-        L.done("b0_prep", s);
     }
 }
 
@@ -340,9 +362,8 @@ void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L) {
     scan_exclusive(b.vtx_cnt, b.vtx_off, (int64_t)b.V + 1, nullptr, b.scratch, s, L);
     radix_sort_onesweep(b.sort_k, b.sort_v, b.sort_k2, b.sort_v2, b.S, bits_for(b.V), b.digits, true, b.scratch, s, L);
     if (b.V > 0) {
-        k_edge_count<<<grid_for(32 * (int64_t)b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
+        launch(L, "b0_edge_count", k_edge_count, dim3(grid_for(32 * (int64_t)b.V)), dim3(kThreads), 0, s, b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
                                                                         b.edge_cnt);
-        L.done("b0_edge_count", s);
     }
     scan_exclusive(b.edge_cnt, b.edge_off, b.V, b.scalars + 0, b.scratch, s, L);
 }
@@ -356,14 +377,12 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     cudaMemsetAsync(b.bnd_word, 0, sizeof(uint32_t) * nw, s);
     if (b.V > 0) cudaMemsetAsync(b.vbnd, 0, sizeof(int32_t) * b.V, s);
     if (b.V > 0) {
-        k_edge_fill<<<grid_for(32 * (int64_t)b.V), kThreads, 0, s>>>(b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
+        launch(L, "b0_edge_fill", k_edge_fill, dim3(grid_for(32 * (int64_t)b.V)), dim3(kThreads), 0, s, b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
                                                                        b.edge_off, b.face_edge, b.face_twin, b.edge_hh,
                                                                        b.bnd_word, b.vbnd, b.scalars, b.flags,
                                                                        b.vtx_slot0);
-        L.done("b0_edge_fill", s);
         if (check_fans) {
-            k_check_fans<<<grid_for(b.V), kThreads, 0, s>>>(b.face_twin, b.vtx_off, b.vtx_slot0, tp, b.V, b.flags);
-            L.done("b0_check_fans", s);
+            launch(L, "b0_check_fans", k_check_fans, dim3(grid_for(b.V)), dim3(kThreads), 0, s, b.face_twin, b.vtx_off, b.vtx_slot0, tp, b.V, b.flags);
         }
     }
     if (E > 0) {
@@ -375,26 +394,22 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
         cudaMemsetAsync(b.sv_cnt, 0, sizeof(int32_t) * b.V, s);
         cudaMemsetAsync(b.sv_cur, 0, sizeof(int32_t) * b.V, s);
     }
-    const int64_t nf = std::max<int64_t>(std::max<int64_t>(E, b.K_in), nw);
-    k_b0_flags<<<grid_for(nf), kThreads, 0, s>>>(b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
+    const int64_t nf = std::max<int64_t>(std::max<int64_t>(E, 32 * (int64_t)b.K_in), nw);
+    launch(L, "b0_flags", k_b0_flags, dim3(grid_for(nf)), dim3(kThreads), 0, s, b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
                                                  b.face_edge, b.edge_hh, tp, b.V, E, b.bnd_word, nw, b.edge_sigma,
                                                  b.edge_cidx, b.sp_flag, b.bnd_wcnt, b.flags);
-    L.done("b0_flags", s);
     scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, b.scratch, s, L);
     scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, b.scratch, s, L);
     if (E > 0) {
-        k_b0_special<<<grid_for(E), kThreads, 0, s>>>(b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp, E,
+        launch(L, "b0_special", k_b0_special, dim3(grid_for(E)), dim3(kThreads), 0, s, b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp, E,
                                                       b.sp, b.sv_cnt);
-        L.done("b0_special", s);
     }
     scan_exclusive(b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V, b.scratch, s, L);
     if (E > 0) {
-        k_b0_svlist<<<grid_for(E), kThreads, 0, s>>>(b.sp, b.scalars + 2, E, b.sv_off, b.sv_cur, b.sv_list);
-        L.done("b0_sv_list", s);
+        launch(L, "b0_sv_list", k_b0_svlist, dim3(grid_for(E)), dim3(kThreads), 0, s, b.sp, b.scalars + 2, E, b.sv_off, b.sv_cur, b.sv_list);
     }
     if (b.V > 0) {
-        k_b0_svsort<<<grid_for(b.V), kThreads, 0, s>>>(b.V, b.sv_off, b.sv_list, b.sv_vtx, b.scalars);
-        L.done("b0_sv_sort", s);
+        launch(L, "b0_sv_sort", k_b0_svsort, dim3(grid_for(b.V)), dim3(kThreads), 0, s, b.V, b.sv_off, b.sv_list, b.sv_vtx, b.scalars);
     }
 }
 

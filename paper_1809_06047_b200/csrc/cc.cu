@@ -43,6 +43,7 @@ ALSUB_D void warp_store_rows(int4 *stage, const int4 (&rows)[4], int4 *dst, int6
 
 template <bool ADJ, bool BND, int NBC>
 __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev c, Frames fr, bool topo, bool fpv) {
+    ALSUB_GRID_WAIT();
     __shared__ int4 s_stage[kThreads / 32][128];
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = r < p.F;
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
 // ---------------- face kernel: general matrix (level 0: mixed orders or triangles) ---------
 template <int ORDER, bool ADJ, bool BND, int NBC>
 __global__ void __launch_bounds__(kThreads) k_cc_face_gen(LevelDev p, ChildDev c, Frames fr, bool topo) {
+    ALSUB_GRID_WAIT();
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= p.F) return;
     const Topo<ORDER> tp{p.face_off, p.slot_face};
@@ -178,6 +180,7 @@ ALSUB_D void edge_ends(const LevelDev &p, const Topo<ORDER> &tp, int32_t h, int3
 
 template <int ORDER, bool ADJ, bool BND, int NBC, int IT>
 __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Frames fr, bool topo) {
+    ALSUB_GRID_WAIT();
     const Topo<ORDER> tp{p.face_off, p.slot_face};
     const int32_t e0 = blockIdx.x * (kThreads * IT) + threadIdx.x;
     const int32_t V = p.V, F = p.F;
@@ -309,6 +312,7 @@ ALSUB_D void copy_point(const Frames &fr, int32_t v) {
 
 template <int ORDER>
 __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, VSegs g) {
+    ALSUB_GRID_WAIT();
     // Work unit = a warp task of 32 consecutive vertices of ONE segment (no divergence between
     // vertex classes inside a warp); block b takes the same fraction [b/NB, (b+1)/NB) of every
     // segment's tasks, so a block works on one spatial band of the mesh.
@@ -389,28 +393,25 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bo
     if (p.F > 0) {
         const bool one = fr.nb == 1;
         if constexpr (ORDER == 4) {
-            if (one) k_cc_face_quad<ADJ, BND, 1><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo, fpv);
-            else k_cc_face_quad<ADJ, BND, 0><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo, fpv);
+            if (one) launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 1>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv);
+            else launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 0>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv);
         } else {
-            if (one) k_cc_face_gen<ORDER, ADJ, BND, 1><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
-            else k_cc_face_gen<ORDER, ADJ, BND, 0><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+            if (one) launch(L, "cc_face", k_cc_face_gen<ORDER, ADJ, BND, 1>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo);
+            else launch(L, "cc_face", k_cc_face_gen<ORDER, ADJ, BND, 0>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo);
         }
-        L.done("cc_face", s);
     }
     if (p.E > 0) {
         constexpr int IT = 2;
         const unsigned g = grid_for(p.E, kThreads * IT);
-        if (fr.nb == 1) k_cc_edge<ORDER, ADJ, BND, 1, IT><<<g, kThreads, 0, s>>>(p, c, fr, topo);
-        else k_cc_edge<ORDER, ADJ, BND, 0, IT><<<g, kThreads, 0, s>>>(p, c, fr, topo);
-        L.done("cc_edge", s);
+        if (fr.nb == 1) launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 1, IT>, dim3(g), dim3(kThreads), 0, s, p, c, fr, topo);
+        else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT>, dim3(g), dim3(kThreads), 0, s, p, c, fr, topo);
     }
     if (p.V > 0) {
         // >= 2 waves of 148 SMs for small levels, 4 vertices per thread for large ones
         const unsigned nblk = (unsigned)std::max<int64_t>(grid_for(p.V, 4 * kThreads),
                                                           std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
-        if constexpr (ORDER == 4) k_cc_vertex<4><<<nblk, kThreads, 0, s>>>(p, fr, g);
-        else k_cc_vertex<0><<<nblk, kThreads, 0, s>>>(p, fr, g);
-        L.done("cc_vertex", s);
+        if constexpr (ORDER == 4) launch(L, "cc_vertex", k_cc_vertex<4>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
+        else launch(L, "cc_vertex", k_cc_vertex<0>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
     }
 }
 

@@ -17,6 +17,10 @@
 
 #define ALSUB_HD __host__ __device__ __forceinline__
 #define ALSUB_D __device__ __forceinline__
+// first statement of every kernel: wait for the predecessor grid (programmatic dependent launch)
+#define ALSUB_GRID_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+// let the next kernel in the stream begin launching (its blocks wait in ALSUB_GRID_WAIT)
+#define ALSUB_GRID_LAUNCH_NEXT() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
 
 namespace alsub {
 

@@ -46,6 +46,7 @@ __device__ __forceinline__ float sigma_bar(const LevelDev &p, int32_t ix, int32_
 }
 
 __global__ void __launch_bounds__(kThreads) k_crease(CreaseArgs A) {
+    ALSUB_GRID_WAIT();
     const LevelDev &p = A.p;
     const Frames &fr = A.fr;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -126,13 +127,13 @@ void crease_level(const LevelDev &p, const ChildDev &c, const Frames &fr, int32_
     const int64_t work = (int64_t)p.nsp + p.nsv;
     if (work <= 0) return;
     CreaseArgs A{p, c, fr, ep_base, scheme, inherit ? 1 : 0};
-    k_crease<<<grid_for(work), kThreads, 0, s>>>(A);
-    L.done("crease", s);
+    launch(L, "crease", k_crease, dim3(grid_for(work)), dim3(kThreads), 0, s, A);
 }
 
 // ---------------- topology export ----------------
 template <int ORDER>
 __global__ void k_export_edges(LevelDev p, int32_t *edge_vtx, int32_t *edge_face) {
+    ALSUB_GRID_WAIT();
     const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= p.E) return;
     const Topo<ORDER> tp{p.face_off, p.slot_face};
@@ -152,10 +153,9 @@ __global__ void k_export_edges(LevelDev p, int32_t *edge_vtx, int32_t *edge_face
 
 void export_edges(const LevelDev &p, int32_t *edge_vtx, int32_t *edge_face, cudaStream_t s, Launches &L) {
     if (p.E <= 0) return;
-    if (p.order == 4) k_export_edges<4><<<grid_for(p.E), kThreads, 0, s>>>(p, edge_vtx, edge_face);
-    else if (p.order == 3) k_export_edges<3><<<grid_for(p.E), kThreads, 0, s>>>(p, edge_vtx, edge_face);
-    else k_export_edges<0><<<grid_for(p.E), kThreads, 0, s>>>(p, edge_vtx, edge_face);
-    L.done("export_edges", s);
+    if (p.order == 4) launch(L, "export_edges", k_export_edges<4>, dim3(grid_for(p.E)), dim3(kThreads), 0, s, p, edge_vtx, edge_face);
+    else if (p.order == 3) launch(L, "export_edges", k_export_edges<3>, dim3(grid_for(p.E)), dim3(kThreads), 0, s, p, edge_vtx, edge_face);
+    else launch(L, "export_edges", k_export_edges<0>, dim3(grid_for(p.E)), dim3(kThreads), 0, s, p, edge_vtx, edge_face);
 }
 
 }  // namespace alsub

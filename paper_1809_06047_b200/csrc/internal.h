@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -32,6 +33,27 @@ struct Launches {
 };
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Programmatic dependent launch (sm_90+): every kernel starts with griddepcontrol.wait, so it may
+// be launched while its predecessor drains; inside the CUDA graph this overlaps the launch latency
+// of each level kernel with the tail of the previous one.  ALSUB_NO_PDL=1 disables it.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch(Launches &L, const char *name, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                   cudaStream_t s, Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+    L.done(name, s);
+}
 inline unsigned grid_for(int64_t n, int threads = kThreads) {
     int64_t g = ceil_div(n > 0 ? n : 1, threads);
     return (unsigned)g;

@@ -56,6 +56,7 @@ ALSUB_D void other_edges(const int32_t *face_edge, int32_t h, int32_t &x, int32_
 }
 
 __global__ void __launch_bounds__(kThreads) k_loop_count(LevelDev p, int32_t *__restrict__ cnt) {
+    ALSUB_GRID_WAIT();
     const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= p.E) return;
     const int2 hh = __ldg(p.edge_hh + e);
@@ -77,8 +78,7 @@ __global__ void __launch_bounds__(kThreads) k_loop_count(LevelDev p, int32_t *__
 
 void loop_edge_base(const LevelDev &p, int32_t *cnt, int32_t *base, void *scratch, cudaStream_t s, Launches &L) {
     if (p.E <= 0) return;
-    k_loop_count<<<grid_for(p.E), kThreads, 0, s>>>(p, cnt);
-    L.done("loop_count", s);
+    launch(L, "loop_count", k_loop_count, dim3(grid_for(p.E)), dim3(kThreads), 0, s, p, cnt);
     scan_exclusive(cnt, base, p.E, nullptr, scratch, s, L);
 }
 
@@ -100,6 +100,7 @@ ALSUB_D int32_t loop_inner(const LevelDev &p, int32_t m, int32_t x, int32_t z, i
 
 template <bool ADJ>
 __global__ void __launch_bounds__(kThreads) k_loop_face(LevelDev p, ChildDev c) {
+    ALSUB_GRID_WAIT();
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= p.F) return;
     const int32_t V = p.V;
@@ -159,6 +160,7 @@ ALSUB_D int32_t loop_c2next(int32_t x) { return 3 * (4 * (x / 3) + (x % 3 + 1) %
 
 template <bool ADJ>
 __global__ void __launch_bounds__(kThreads) k_loop_edge(LevelDev p, ChildDev c, Frames fr) {
+    ALSUB_GRID_WAIT();
     const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= p.E) return;
     const int2 hh = __ldg(p.edge_hh + e);
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(kThreads) k_loop_edge(LevelDev p, ChildDev c, 
 
 template <bool ADJ>
 __global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c, Frames fr) {
+    ALSUB_GRID_WAIT();
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= p.V) return;
     const int32_t h0 = __ldg(p.vtx_slot0 + v);
@@ -219,19 +222,16 @@ void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool top
     (void)scratch;
     const bool A = adj && topo;
     if (topo && p.F > 0) {
-        if (A) k_loop_face<true><<<grid_for(p.F), kThreads, 0, s>>>(p, c);
-        else k_loop_face<false><<<grid_for(p.F), kThreads, 0, s>>>(p, c);
-        L.done("loop_face", s);
+        if (A) launch(L, "loop_face", k_loop_face<true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c);
+        else launch(L, "loop_face", k_loop_face<false>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c);
     }
     if (p.E > 0) {
-        if (A) k_loop_edge<true><<<grid_for(p.E), kThreads, 0, s>>>(p, c, fr);
-        else k_loop_edge<false><<<grid_for(p.E), kThreads, 0, s>>>(p, c, fr);
-        L.done("loop_edge", s);
+        if (A) launch(L, "loop_edge", k_loop_edge<true>, dim3(grid_for(p.E)), dim3(kThreads), 0, s, p, c, fr);
+        else launch(L, "loop_edge", k_loop_edge<false>, dim3(grid_for(p.E)), dim3(kThreads), 0, s, p, c, fr);
     }
     if (p.V > 0) {
-        if (A) k_loop_vertex<true><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
-        else k_loop_vertex<false><<<grid_for(p.V), kThreads, 0, s>>>(p, c, fr);
-        L.done("loop_vertex", s);
+        if (A) launch(L, "loop_vertex", k_loop_vertex<true>, dim3(grid_for(p.V)), dim3(kThreads), 0, s, p, c, fr);
+        else launch(L, "loop_vertex", k_loop_vertex<false>, dim3(grid_for(p.V)), dim3(kThreads), 0, s, p, c, fr);
     }
 }
 
@@ -255,6 +255,7 @@ ALSUB_D void warp_store_9(int32_t *stage, const int32_t (&v)[9], int32_t *dst, i
 
 template <bool ADJ, int NBC>
 __global__ void __launch_bounds__(kThreads) k_s3_face(LevelDev p, ChildDev c, Frames fr, bool topo) {
+    ALSUB_GRID_WAIT();
     __shared__ int32_t s_stage[kThreads / 32][9 * 32];
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = i < p.F;
@@ -303,6 +304,7 @@ __global__ void __launch_bounds__(kThreads) k_s3_face(LevelDev p, ChildDev c, Fr
 // from the parent rows (the triangle's corners and the three neighbouring face points).
 template <int NBC>
 __global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, VSegs g) {
+    ALSUB_GRID_WAIT();
     __shared__ int32_t s_lo[kMaxSeg], s_pre[kMaxSeg + 1];
     const int64_t nblk = gridDim.x, b = blockIdx.x;
     if (threadIdx.x < g.nseg) {
@@ -394,20 +396,18 @@ void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool to
     const bool one = fr.nb == 1;
     if (p.F > 0) {
         if (A) {
-            if (one) k_s3_face<true, 1><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
-            else k_s3_face<true, 0><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+            if (one) launch(L, "s3_face", k_s3_face<true, 1>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo);
+            else launch(L, "s3_face", k_s3_face<true, 0>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo);
         } else {
-            if (one) k_s3_face<false, 1><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
-            else k_s3_face<false, 0><<<grid_for(p.F), kThreads, 0, s>>>(p, c, fr, topo);
+            if (one) launch(L, "s3_face", k_s3_face<false, 1>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo);
+            else launch(L, "s3_face", k_s3_face<false, 0>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo);
         }
-        L.done("s3_face", s);
     }
     if (p.V > 0) {
         const unsigned nblk = (unsigned)std::max<int64_t>(grid_for(p.V, 4 * kThreads),
                                                           std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
-        if (one) k_s3_vertex<1><<<nblk, kThreads, 0, s>>>(p, fr, g);
-        else k_s3_vertex<0><<<nblk, kThreads, 0, s>>>(p, fr, g);
-        L.done("s3_vertex", s);
+        if (one) launch(L, "s3_vertex", k_s3_vertex<1>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
+        else launch(L, "s3_vertex", k_s3_vertex<0>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
     }
 }
 

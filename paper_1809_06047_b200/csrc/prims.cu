@@ -39,6 +39,7 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 
 __global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t *__restrict__ in, int32_t *__restrict__ out,
                                                      int64_t n, unsigned long long *status, int32_t *total) {
+    ALSUB_GRID_WAIT();
     __shared__ int s_tile;
     __shared__ int s_data[kScanTile + kScanTile / 32];
     __shared__ int s_warp[kScanThreads / 32];
@@ -124,8 +125,7 @@ void scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *total, 
     }
     cudaMemsetAsync(scratch, 0, scan_scratch_bytes(n), s);
     int64_t tiles = ceil_div(n, kScanTile);
-    k_scan<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, n, (unsigned long long *)scratch, total);
-    L.done("scan", s);
+    launch(L, "scan", k_scan, dim3((unsigned)tiles), dim3(kScanThreads), 0, s, in, out, n, (unsigned long long *)scratch, total);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -144,6 +144,7 @@ size_t sort_scratch_bytes(int64_t n) {
 
 __global__ void __launch_bounds__(kSortThreads) k_rs_hist(const int32_t *__restrict__ keys, int64_t n, int shift,
                                                         int32_t *__restrict__ counts, int nblocks) {
+    ALSUB_GRID_WAIT();
     __shared__ int h[256];
     h[threadIdx.x] = 0;
     __syncthreads();
@@ -160,6 +161,7 @@ __global__ void __launch_bounds__(kSortThreads) k_rs_scatter(const int32_t *__re
                                                            const int32_t *__restrict__ vals, int64_t n, int shift,
                                                            const int32_t *__restrict__ offs, int nblocks,
                                                            int32_t *__restrict__ okeys, int32_t *__restrict__ ovals) {
+    ALSUB_GRID_WAIT();
     __shared__ int run[256];
     __shared__ int wc[kSortThreads / 32][256];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -205,11 +207,9 @@ void radix_sort_pairs(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *
     int32_t *ka = keys, *va = vals, *kb = keys_alt, *vb = vals_alt;
     for (int p = 0; p < passes; ++p) {
         int shift = 8 * p;
-        k_rs_hist<<<nblocks, kSortThreads, 0, s>>>(ka, n, shift, counts, nblocks);
-        L.done("rs_hist", s);
+        launch(L, "rs_hist", k_rs_hist, dim3(nblocks), dim3(kSortThreads), 0, s, ka, n, shift, counts, nblocks);
         scan_exclusive(counts, offs, cnt, nullptr, scan_scratch, s, L);
-        k_rs_scatter<<<nblocks, kSortThreads, 0, s>>>(ka, va, n, shift, offs, nblocks, kb, vb);
-        L.done("rs_scatter", s);
+        launch(L, "rs_scatter", k_rs_scatter, dim3(nblocks), dim3(kSortThreads), 0, s, ka, va, n, shift, offs, nblocks, kb, vb);
         int32_t *t;
         t = ka; ka = kb; kb = t;
         t = va; va = vb; vb = t;
@@ -227,7 +227,7 @@ void radix_sort_pairs(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *
 // back in parallel, one per thread).
 // ------------------------------------------------------------------------------------------
 constexpr int kOsThreads = 256;
-constexpr int kOsItems = 8;
+constexpr int kOsItems = 4;
 constexpr int kOsTile = kOsThreads * kOsItems;
 
 static int64_t os_tiles(int64_t n) { return ceil_div(n > 0 ? n : 1, kOsTile); }
@@ -239,6 +239,7 @@ size_t onesweep_scratch_bytes(int64_t n, int passes) {
 
 __global__ void __launch_bounds__(kOsThreads) k_os_hist(const int32_t *__restrict__ keys, int64_t n, int passes,
                                                       int32_t *__restrict__ counts) {
+    ALSUB_GRID_WAIT();
     __shared__ int h[4][256];
     for (int p = 0; p < passes; ++p) h[p][threadIdx.x] = 0;
     __syncthreads();
@@ -257,6 +258,7 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(const int32_t *__restric
                                                       int64_t n, int shift, const int32_t *__restrict__ counts,
                                                       uint32_t *status, unsigned *counter, int32_t *__restrict__ okeys,
                                                       int32_t *__restrict__ ovals) {
+    ALSUB_GRID_WAIT();
     __shared__ int s_tile;
     __shared__ int s_base[256];       // global exclusive prefix of the digit + this tile's look-back
     __shared__ int s_cnt[256];        // this tile's digit counts
@@ -350,17 +352,15 @@ void radix_sort_onesweep(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_
     if (n <= 1) return;
     if (!counts_ready) {
         cudaMemsetAsync(counts, 0, sizeof(int32_t) * 256 * passes, s);
-        k_os_hist<<<(unsigned)std::min<int64_t>(ceil_div(n, kOsThreads), 4 * 148), kOsThreads, 0, s>>>(keys, n, passes, counts);
-        L.done("os_hist", s);
+        launch(L, "os_hist", k_os_hist, dim3((unsigned)std::min<int64_t>(ceil_div(n, kOsThreads), 4 * 148)), dim3(kOsThreads), 0, s, keys, n, passes, counts);
     }
     cudaMemsetAsync(scratch, 0, onesweep_scratch_bytes(n, passes), s);
     const int64_t tiles = os_tiles(n);
     int32_t *ka = keys, *va = vals, *kb = keys_alt, *vb = vals_alt;
     for (int p = 0; p < passes; ++p) {
         char *base = (char *)scratch + (size_t)p * (64 + (size_t)tiles * 256 * 4);
-        k_os_pass<<<(unsigned)tiles, kOsThreads, 0, s>>>(ka, va, n, 8 * p, counts + 256 * p, (uint32_t *)(base + 64),
+        launch(L, "os_pass", k_os_pass, dim3((unsigned)tiles), dim3(kOsThreads), 0, s, ka, va, n, 8 * p, counts + 256 * p, (uint32_t *)(base + 64),
                                                          (unsigned *)base, kb, vb);
-        L.done("os_pass", s);
         int32_t *t;
         t = ka; ka = kb; kb = t;
         t = va; va = vb; vb = t;
@@ -375,6 +375,7 @@ void radix_sort_onesweep(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_
 // CSR offsets of sorted keys (run-length of the sorted key array)
 // ------------------------------------------------------------------------------------------
 __global__ void k_offsets(const int32_t *__restrict__ keys, int64_t n, int32_t *__restrict__ off, int32_t nkeys) {
+    ALSUB_GRID_WAIT();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int32_t k = keys[i];
@@ -385,6 +386,7 @@ __global__ void k_offsets(const int32_t *__restrict__ keys, int64_t n, int32_t *
 }
 
 __global__ void k_fill_i32(int32_t *p, int64_t n, int32_t val) {
+    ALSUB_GRID_WAIT();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = val;
 }
@@ -394,8 +396,7 @@ void offsets_from_sorted(const int32_t *keys, int64_t n, int32_t *off, int32_t n
         cudaMemsetAsync(off, 0, sizeof(int32_t) * ((size_t)nkeys + 1), s);
         return;
     }
-    k_offsets<<<grid_for(n), kThreads, 0, s>>>(keys, n, off, nkeys);
-    L.done("offsets", s);
+    launch(L, "offsets", k_offsets, dim3(grid_for(n)), dim3(kThreads), 0, s, keys, n, off, nkeys);
 }
 
 }  // namespace alsub
