@@ -55,22 +55,32 @@ def level_counts(m, levels):
     return out
 
 
-def kernel_bytes_cc(name, c, adj, prev=None):
+def kernel_bytes_cc(name, c, prev, lvl, levels):
     """Algorithmic bytes of one launch of a CC level kernel: every array the
-    kernel reads or writes, counted once.  c = counts of the parent level l, prev = level l-1."""
+    kernel reads or writes, counted once.  c = counts of the parent level lvl, prev = level lvl-1.
+    Mirrors the plan in api.cu: the last refined level (lvl = levels-1 >= 2) recomputes its edge
+    rows from the grandparent and iterates the grandparent's edges, so level levels-1 never stores
+    face_edge / face_twin / edge pairs; twins are only stored where the next level emits adjacency."""
     V, F, S, E = c["V"], c["F"], c["S"], c["E"]
-    Fp = prev["F"] if prev else 0           # face points born at level l (smoothed by cc_face, l >= 2)
+    Fp = prev["F"] if prev else 0
     Ep = prev["E"] if prev else 0
-    fpv = prev is not None and c.get("level", 0) >= 2
+    adj = lvl < levels - 1                        # this level emits child adjacency
+    gp_last = levels >= 3 and lvl == levels - 1   # grandparent path at the last level
+    child_rows = adj and not (levels >= 3 and lvl + 1 == levels - 1)  # child face_edge / edge pairs stored
+    child_twin = lvl + 2 < levels
+    fpv = lvl >= 2
     if name == "cc_face":
-        rd = 4 * S + 4 * S + 12 * V + (4 * S if adj else 0)               # face_vtx, face_edge, P (+face_twin)
-        wr = 12 * F + 16 * S + ((16 * S + 16 * S) if adj else 0)          # f, child faces (+face_edge', face_twin')
-        wr += 12 * Fp if fpv else 0                                          # vertex points of the new face points
+        rd = 4 * S + 12 * V + (48 * Fp if gp_last else 4 * S) + (4 * S if adj else 0)
+        wr = 12 * F + 16 * S + (16 * S if child_rows else 0) + (16 * S if child_twin else 0)
+        wr += (12 * Fp + 12 * F) if fpv else 0    # new face-point vertices + half ring sums
     elif name == "cc_edge":
-        rd = 8 * E + 4 * S + 12 * V + 12 * F                                # edge pairs, face_vtx rows, P, f
-        wr = 12 * E + (8 * (2 * E + S) if adj else 0)                        # e (+ child edge pairs)
+        if gp_last:
+            rd = 8 * Ep + 16 * Fp + 12 * V + 12 * F
+        else:
+            rd = 8 * E + 4 * S + 12 * V + 12 * F
+        wr = 12 * E + (8 * (2 * E + S) if child_rows else 0)
     elif name == "cc_vertex":
-        rd = 4 * S + 12 * V + 12 * F + 8 * Ep                               # face_vtx, P, f, birth edge pairs
+        rd = 4 * S + 12 * V + 12 * F + 8 * Ep + (12 * F if fpv else 0)
         wr = 12 * (V - (Fp if fpv else 0))
     else:
         return None
@@ -290,14 +300,14 @@ def run_alsub(args):
             row["survey_frac"] = row["survey_GBps"] / peak if row["survey_GBps"] else None
             kk = {}
             for n, t in ks.items():
-                b = kernel_bytes_cc(n, c, not final, cnt[lvl - 1] if lvl > 0 else None)
+                b = kernel_bytes_cc(n, c, cnt[lvl - 1] if lvl > 0 else None, lvl, levels)
                 kk[n] = {"ms": t, "alg_bytes": b, "GBps": (b / (t * 1e6)) if b else None,
                          "frac": (b / (t * 1e6) / peak) if b else None}
             row["kernels"] = kk
         per_level.append(row)
     # dominant kernel = the largest share of the step
     (dname, dlvl), dms = max(kt.items(), key=lambda kv: kv[1])
-    dbytes = kernel_bytes_cc(dname, cnt[dlvl], dlvl < levels - 1, cnt[dlvl - 1] if dlvl > 0 else None) \
+    dbytes = kernel_bytes_cc(dname, cnt[dlvl], cnt[dlvl - 1] if dlvl > 0 else None, dlvl, levels) \
         if dlvl >= 0 else None
     achieved = dbytes / (dms * 1e6) if dbytes else None
     traffic = None

@@ -382,9 +382,13 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
             c.face_vtx = A<int32_t>(m, c.S, s, ML, ok);
             c.pos = A<float>(m, 3 * c.V, s, ML, ok);
             if (has_child) {
-                c.face_twin = A<int32_t>(m, c.S, s, ML, ok);
+                // CC consumes a level's twins only to emit the adjacency of ITS child (adj)
+                if (scheme != ALSUB_CATMULL_CLARK || adj) c.face_twin = A<int32_t>(m, c.S, s, ML, ok);
                 if (scheme == ALSUB_LOOP) c.vtx_slot0 = A<int32_t>(m, c.V, s, ML, ok);
-                if (scheme != ALSUB_SQRT3) {
+                // CC, levels >= 3: the last refined level recomputes its edge rows and iterates its
+                // parent's edges (cc.cu), so its face_edge / edge pairs are never stored
+                const bool last_cc = scheme == ALSUB_CATMULL_CLARK && levels >= 3 && l == levels - 1;
+                if (scheme != ALSUB_SQRT3 && !last_cc) {
                     c.face_edge = A<int32_t>(m, c.S, s, ML, ok);
                     c.edge_hh = A<int2>(m, c.E, s, ML, ok);
                 }
@@ -404,7 +408,6 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
             c.loop_base = A<int32_t>(m, c.E, s, ML, ok);
             max_scan = std::max<int64_t>(max_scan, c.E);
         }
-        (void)adj;
     }
     size_t need = std::max(build0_scratch_bytes(m->V0, m->S0), scan_scratch_bytes(max_scan));
     if (need > m->scratch_bytes) {
@@ -492,7 +495,10 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
         Frames fr{P.pos, C.pos, 3 * P.V, 3 * C.V, 1, m->hs, 0};
         if (scheme == ALSUB_CATMULL_CLARK) {
             VSegs g = make_segs(m, l);
-            cc_level(p, c, fr, true, adj, g, s, L);
+            LevelDev gp{};
+            const bool use_gp = l >= 2 && P.edge_hh == nullptr;
+            if (use_gp) gp = dev_of(m->lv[l - 1]);
+            cc_level(p, c, fr, true, adj, g, use_gp ? &gp : nullptr, s, L);
             if (special) crease_level(p, c, fr, (int32_t)(P.V + P.F), 0, true, s, L);
         } else if (scheme == ALSUB_LOOP) {
             if (adj || special) loop_edge_base(p, P.loop_cnt, P.loop_base, m->scratch, s, L);
@@ -659,8 +665,25 @@ extern "C" alsub_status alsub_level_topology(const alsub_mesh *mc, int32_t level
         }
     }
     if (edge_vtx || edge_face) {
-        const bool have = L->edges_valid && (level == 0 || level < m->levels) && L->edge_hh;
+        const bool rebuild = L->edge_hh == nullptr && m->scheme == ALSUB_CATMULL_CLARK && level >= 2 &&
+                             level < m->levels;
+        const bool have = L->edges_valid && (level == 0 || level < m->levels) && (L->edge_hh || rebuild);
         if (!have) { free_list(m, tmp, s); return fail(ALSUB_E_ARG, "edge tables are not kept for this level"); }
+        LevelHost Lx = *L;
+        if (rebuild) {
+            // re-emit the edge pairs of this (last refined) level with the parent's topology kernels
+            Lx.edge_hh = A<int2>(m, L->E, s, tmp, ok);
+            if (!ok) return fail(ALSUB_E_NOMEM, "export buffer");
+            const LevelHost &Pp = m->lv[level - 1];
+            LevelDev pd = dev_of(Pp);
+            ChildDev cd = child_of(Lx);
+            cd.face_edge = nullptr;
+            cd.face_twin = nullptr;
+            Frames fr0{nullptr, nullptr, 0, 0, 0, nullptr, 0};
+            VSegs g = make_segs(m, level - 1);
+            cc_level(pd, cd, fr0, true, true, g, nullptr, s, Ln);
+        }
+        L = &Lx;
         int32_t *dv = edge_vtx && !is_device_ptr(edge_vtx) ? A<int32_t>(m, 2 * L->E, s, tmp, ok) : edge_vtx;
         int32_t *df = edge_face && !is_device_ptr(edge_face) ? A<int32_t>(m, 2 * L->E, s, tmp, ok) : edge_face;
         if (!ok) return fail(ALSUB_E_NOMEM, "export buffer");
@@ -763,7 +786,10 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
             Frames fr{P, Pn, 3 * Pl.V, 3 * m->lv[l + 1].V, n, m->frame_hs, m->hs_elems};
             if (scheme == ALSUB_CATMULL_CLARK) {
                 VSegs g = make_segs(m, l);
-                cc_level(p, c, fr, false, false, g, s, L);
+                LevelDev gp{};
+                const bool use_gp = l >= 2 && Pl.edge_hh == nullptr;
+                if (use_gp) gp = dev_of(m->lv[l - 1]);
+                cc_level(p, c, fr, false, false, g, use_gp ? &gp : nullptr, s, L);
                 if (special) crease_level(p, c, fr, (int32_t)(Pl.V + Pl.F), 0, false, s, L);
             } else if (scheme == ALSUB_LOOP) {
                 loop_level(p, c, fr, false, false, m->scratch, s, L);

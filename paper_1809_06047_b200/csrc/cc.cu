@@ -41,8 +41,24 @@ ALSUB_D void warp_store_rows(int4 *stage, const int4 (&rows)[4], int4 *dst, int6
     __syncwarp();
 }
 
-template <bool ADJ, bool BND, int NBC>
-__global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev c, Frames fr, bool topo, bool fpv) {
+// the edge-id row of level-l face r = child (R, t) of level-(l-1) quad R, in closed form from R's
+// rows (what the level-(l-1) face kernel would have stored as face_edge; used at the last level)
+ALSUB_D int4 child_edge_row(const LevelDev &gp, int32_t r) {
+    const int32_t R = r >> 2, t = r & 3, tn = (t + 1) & 3, tp = (t + 3) & 3;
+    const int4 a = __ldg(reinterpret_cast<const int4 *>(gp.face_vtx) + R);
+    const int4 b = __ldg(reinterpret_cast<const int4 *>(gp.face_edge) + R);
+    const int4 c = __ldg(reinterpret_cast<const int4 *>(gp.face_twin) + R);
+    const int32_t v[4] = {a.x, a.y, a.z, a.w}, e[4] = {b.x, b.y, b.z, b.w}, tw[4] = {c.x, c.y, c.z, c.w};
+    const int32_t bt = 4 * e[t] - (gp.B > 0 ? bprefix(gp.bnd_word, gp.bnd_wpre, e[t]) : 0);
+    const int32_t bq = 4 * e[tp] - (gp.B > 0 ? bprefix(gp.bnd_word, gp.bnd_wpre, e[tp]) : 0);
+    const int32_t h = 4 * R + t, hp = 4 * R + tp;
+    return make_int4(bt + (v[t] > v[tn]), bt + 2 + (tw[t] >= 0 && tw[t] < h), bq + 2 + (tw[tp] >= 0 && tw[tp] < hp),
+                     bq + (v[t] > v[tp]));
+}
+
+template <bool ADJ, bool BND, int NBC, bool GPE>
+__global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev c, Frames fr, bool topo, bool fpv,
+                                                         LevelDev gp) {
     ALSUB_GRID_WAIT();
     __shared__ int4 s_stage[kThreads / 32][128];
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -53,6 +69,13 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
     const int32_t v[4] = {fv.x, fv.y, fv.z, fv.w};
     const int32_t V = p.V, F = p.F;
     const int nb = NBC ? NBC : fr.nb;
+    // edge-id row: loaded (or recomputed from the grandparent rows) up front so that its loads are
+    // in flight together with the position gathers
+    int4 fe = make_int4(0, 0, 0, 0);
+    if (topo && valid) {
+        if constexpr (GPE) fe = child_edge_row(gp, r);
+        else fe = __ldg(reinterpret_cast<const int4 *>(p.face_edge) + r);
+    }
     for (int f = 0; f < nb; ++f) {
         const float *P = fr.P + f * fr.Pstride;
         float *Pn = fr.Pn + f * fr.Pnstride;
@@ -84,7 +107,6 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
         }
     }
     if (!topo) return;
-    const int4 fe = valid ? __ldg(reinterpret_cast<const int4 *>(p.face_edge) + r) : make_int4(0, 0, 0, 0);
     const int32_t e[4] = {fe.x, fe.y, fe.z, fe.w};
     const int64_t row0 = 4 * (int64_t)(r - lane), nrows = 4 * (int64_t)F;
     {
@@ -94,6 +116,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
         warp_store_rows(stage, rows, reinterpret_cast<int4 *>(c.face_vtx), row0, nrows, lane);
     }
     if constexpr (ADJ) {
+        if (c.face_edge == nullptr) return;  // the child is the last level: its rows are recomputed there
         const int4 ft = valid ? __ldg(reinterpret_cast<const int4 *>(p.face_twin) + r) : make_int4(-1, -1, -1, -1);
         const int32_t tw[4] = {ft.x, ft.y, ft.z, ft.w};
         int32_t base[4];
@@ -109,6 +132,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
                                 base[tp] + 2 + (tw[tp] >= 0 && tw[tp] < hp), base[tp] + (v[t] > v[tp]));
         }
         warp_store_rows(stage, rows, reinterpret_cast<int4 *>(c.face_edge), row0, nrows, lane);
+        if (c.face_twin == nullptr) return;  // the child is the last refined level: no twins needed
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const int tn = (t + 1) & 3, tp = (t + 3) & 3;
@@ -152,8 +176,9 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_gen(LevelDev p, ChildDev c
             reinterpret_cast<int4 *>(c.face_edge)[h] =
                 make_int4(bt + (vt > vn), bt + 2 + (twt >= 0 && twt < h), bp + 2 + (twp >= 0 && twp < hp),
                           bp + (vt > vp));
-            reinterpret_cast<int4 *>(c.face_twin)[h] =
-                make_int4(twt >= 0 ? 4 * tp.next(twt) + 3 : -1, 4 * hn + 2, 4 * hp + 1, twp >= 0 ? 4 * twp : -1);
+            if (c.face_twin)
+                reinterpret_cast<int4 *>(c.face_twin)[h] =
+                    make_int4(twt >= 0 ? 4 * tp.next(twt) + 3 : -1, 4 * hn + 2, 4 * hp + 1, twp >= 0 ? 4 * twp : -1);
         }
     }
 }
@@ -231,10 +256,12 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
                 if (y < 0) return make_int2(x, -1);
                 return make_int2(min(x, y), max(x, y));
             };
-            c.edge_hh[base + 0] = pair(a0, a1);
-            c.edge_hh[base + 1] = pair(b0, b1);
-            c.edge_hh[base + 2] = pair(4 * h + 1, 4 * hn[k] + 2);  // (fp of face(h), ep); h < tw
-            if (tw >= 0) c.edge_hh[base + 3] = pair(4 * tw + 1, 4 * tp.next(tw) + 2);
+            if (c.edge_hh) {
+                c.edge_hh[base + 0] = pair(a0, a1);
+                c.edge_hh[base + 1] = pair(b0, b1);
+                c.edge_hh[base + 2] = pair(4 * h + 1, 4 * hn[k] + 2);  // (fp of face(h), ep); h < tw
+                if (tw >= 0) c.edge_hh[base + 3] = pair(4 * tw + 1, 4 * tp.next(tw) + 2);
+            }
             if constexpr (BND) {
                 // child boundary bits and, in closed form, the child per-word prefix:
                 // bprefix'(base + k) = 2 bprefix(e) + bnd_e min(k, 2)
@@ -250,6 +277,77 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
                 }
             }
         }
+    }
+}
+
+// ---------------- last-level edge kernel over the grandparent edges ----------------
+// At the last refined level l (>= 2) the level-l edges are iterated as the 3-4 children of each
+// level-(l-1) edge e' = (h', tw'): (lo,ep), (hi,ep), (fp_R,ep), (fp_S,ep) with ids base(e')+k and
+// faces {h_ab, next(h_ba)}, {h_ba, next(h_ab)}, {h', next(h')}, {tw', next(tw')} (level-l face
+// index = level-(l-1) slot).  Five position gathers and four face points serve all four edge
+// points, and the level-l edge pairs never need to be stored.
+template <int NBC>
+__global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp, Frames fr) {
+    ALSUB_GRID_WAIT();
+    // the block's children are the contiguous id range [base(e_first), base(e_last) + nch): staged
+    // in shared memory and written back as one coalesced float run
+    __shared__ float s_out[4 * kThreads * 3];
+    __shared__ int32_t s_base0, s_end;
+    const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = e < gp.E;
+    int2 hh = make_int2(0, -1);
+    if (valid) hh = __ldg(gp.edge_hh + e);
+    const int32_t h = hh.x, tw = hh.y;
+    const int32_t R = h >> 2, t = h & 3;
+    const int4 row = valid ? __ldg(reinterpret_cast<const int4 *>(gp.face_vtx) + R) : make_int4(0, 0, 0, 0);
+    const int32_t rv[4] = {row.x, row.y, row.z, row.w};
+    const int32_t va = rv[t], vb = rv[(t + 1) & 3];
+    const int32_t Vg = gp.V, Fg = gp.F;
+    const int32_t ep = Vg + Fg + e, fpR = Vg + R, fpS = tw >= 0 ? Vg + (tw >> 2) : 0;
+    const int32_t nh = (h & ~3) | ((h + 1) & 3), nt = tw >= 0 ? ((tw & ~3) | ((tw + 1) & 3)) : 0;
+    const int32_t base = valid ? 4 * e - (gp.B > 0 ? bprefix(gp.bnd_word, gp.bnd_wpre, e) : 0) : 0;
+    const int32_t nch = tw < 0 ? 3 : 4;
+    const int32_t last = min((int32_t)(blockIdx.x * blockDim.x + blockDim.x), gp.E) - 1;
+    if (threadIdx.x == 0) s_base0 = base;
+    if (valid && e == last) s_end = base + nch;
+    const bool fwd = va < vb;  // h runs lo -> hi
+    const int32_t lo = fwd ? va : vb, hi = fwd ? vb : va;
+    const int32_t f0a = fwd ? h : tw, f0b = fwd ? nt : nh;  // faces of (lo, ep)
+    const int32_t f1a = fwd ? tw : h, f1b = fwd ? nh : nt;  // faces of (hi, ep)
+    const int32_t V = p.V, F = p.F;
+    const int nb = NBC ? NBC : fr.nb;
+    __syncthreads();
+    const int32_t base0 = s_base0, n = s_end - base0;
+    const int32_t o = base - base0;
+    for (int f = 0; f < nb; ++f) {
+        const float *P = fr.P + f * fr.Pstride;
+        float *Pn = fr.Pn + f * fr.Pnstride;
+        if (valid) {
+            const P3 plo = ld3(P, lo), phi = ld3(P, hi), pep = ld3(P, ep), pR = ld3(P, fpR);
+            const P3 fh = ld3c(Pn, V + h), fnh = ld3c(Pn, V + nh);
+            P3 q[4];
+            q[2] = 0.25f * (pR + pep + fh + fnh);
+            if (tw < 0) {
+                q[0] = 0.5f * (plo + pep);
+                q[1] = 0.5f * (phi + pep);
+            } else {
+                const P3 pS = ld3(P, fpS), ft = ld3c(Pn, V + tw), fnt = ld3c(Pn, V + nt);
+                const P3 fa = (f0a == h ? fh : ft) + (f0b == nh ? fnh : fnt);
+                const P3 fb = (f1a == h ? fh : ft) + (f1b == nh ? fnh : fnt);
+                q[0] = 0.25f * (plo + pep + fa);
+                q[1] = 0.25f * (phi + pep + fb);
+                q[3] = 0.25f * (pS + pep + ft + fnt);
+            }
+            for (int k = 0; k < nch; ++k) {
+                s_out[3 * (o + k) + 0] = q[k].x;
+                s_out[3 * (o + k) + 1] = q[k].y;
+                s_out[3 * (o + k) + 2] = q[k].z;
+            }
+        }
+        __syncthreads();
+        float *dst = Pn + 3 * ((int64_t)V + F + base0);
+        for (int32_t i = threadIdx.x; i < 3 * n; i += blockDim.x) dst[i] = s_out[i];
+        __syncthreads();
     }
 }
 
@@ -388,23 +486,32 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
 // ------------------------------------------------------------------------------------------
 template <int ORDER, bool ADJ, bool BND>
 static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, const VSegs &g,
-                      cudaStream_t s, Launches &L) {
+                      const LevelDev *gp, cudaStream_t s, Launches &L) {
     const bool fpv = g.level >= 2;  // face points born at this level are smoothed by the face kernel
+    const bool one = fr.nb == 1;
+    const LevelDev gpd = gp ? *gp : LevelDev{};
     if (p.F > 0) {
-        const bool one = fr.nb == 1;
         if constexpr (ORDER == 4) {
-            if (one) launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 1>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv);
-            else launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 0>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv);
+            if (gp) {
+                if (one) launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 1, true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd);
+                else launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 0, true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd);
+            } else {
+                if (one) launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 1, false>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd);
+                else launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 0, false>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd);
+            }
         } else {
             if (one) launch(L, "cc_face", k_cc_face_gen<ORDER, ADJ, BND, 1>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo);
             else launch(L, "cc_face", k_cc_face_gen<ORDER, ADJ, BND, 0>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo);
         }
     }
-    if (p.E > 0) {
+    if (gp && gp->E > 0) {
+        if (one) launch(L, "cc_edge", k_cc_edge_gp<1>, dim3(grid_for(gp->E)), dim3(kThreads), 0, s, p, gpd, fr);
+        else launch(L, "cc_edge", k_cc_edge_gp<0>, dim3(grid_for(gp->E)), dim3(kThreads), 0, s, p, gpd, fr);
+    } else if (p.E > 0) {
         constexpr int IT = 2;
-        const unsigned g = grid_for(p.E, kThreads * IT);
-        if (fr.nb == 1) launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 1, IT>, dim3(g), dim3(kThreads), 0, s, p, c, fr, topo);
-        else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT>, dim3(g), dim3(kThreads), 0, s, p, c, fr, topo);
+        const unsigned gdim = grid_for(p.E, kThreads * IT);
+        if (one) launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 1, IT>, dim3(gdim), dim3(kThreads), 0, s, p, c, fr, topo);
+        else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT>, dim3(gdim), dim3(kThreads), 0, s, p, c, fr, topo);
     }
     if (p.V > 0) {
         // >= 2 waves of 148 SMs for small levels, 4 vertices per thread for large ones
@@ -417,26 +524,26 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bo
 
 template <int ORDER>
 static void cc_dispatch(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &g,
-                        cudaStream_t s, Launches &L) {
+                        const LevelDev *gp, cudaStream_t s, Launches &L) {
     const bool bnd = p.B > 0;
     if (adj && topo) {
-        if (bnd) cc_launch<ORDER, true, true>(p, c, fr, topo, g, s, L);
-        else cc_launch<ORDER, true, false>(p, c, fr, topo, g, s, L);
+        if (bnd) cc_launch<ORDER, true, true>(p, c, fr, topo, g, gp, s, L);
+        else cc_launch<ORDER, true, false>(p, c, fr, topo, g, gp, s, L);
     } else {
-        cc_launch<ORDER, false, false>(p, c, fr, topo, g, s, L);
+        cc_launch<ORDER, false, false>(p, c, fr, topo, g, gp, s, L);
     }
 }
 
 void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &g,
-              cudaStream_t s, Launches &L) {
+              const LevelDev *gp, cudaStream_t s, Launches &L) {
     if (adj && topo && p.B > 0) {
         const int32_t nw = (int32_t)ceil_div(c.E > 0 ? c.E : 1, 32);
         cudaMemsetAsync(c.bnd_word, 0, sizeof(uint32_t) * nw, s);
     }
     // level-0 meshes of uniform order use the generic kernels too (their M^T comes from the sort);
     // levels >= 1 are reduced quad matrices
-    if (p.order == 4 && p.face_off == nullptr) cc_dispatch<4>(p, c, fr, topo, adj, g, s, L);
-    else cc_dispatch<0>(p, c, fr, topo, adj, g, s, L);
+    if (p.order == 4 && p.face_off == nullptr) cc_dispatch<4>(p, c, fr, topo, adj, g, gp, s, L);
+    else cc_dispatch<0>(p, c, fr, topo, adj, g, gp, s, L);
 }
 
 }  // namespace alsub

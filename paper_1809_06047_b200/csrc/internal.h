@@ -176,8 +176,10 @@ struct VSegs {
 
 // mode: adj = emit child adjacency (not the last level); topo = emit child faces;
 //       acc = accumulate crease valency/sharpness (refine) vs reuse stored (eval_frames)
+// gp (nullable) = the grandparent level: at the last refined level (>= 2) the face kernel
+// recomputes its edge ids from gp's rows and the edge kernel iterates gp's edges
 void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &segs,
-              cudaStream_t s, Launches &L);
+              const LevelDev *gp, cudaStream_t s, Launches &L);
 void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
                 cudaStream_t s, Launches &L);
 void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &g,
