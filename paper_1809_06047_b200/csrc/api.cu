@@ -90,6 +90,8 @@ struct alsub_mesh {
     int64_t graph_launches = 0;
     int64_t plan_runs = 0;  // refines run with the current plan (graph recorded from the 2nd on)
     cudaStream_t cap_stream = nullptr;
+    cudaStream_t side_stream = nullptr;  // second branch for independent level kernels
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t last_launches = 0;
     // frames
     int frames_nb = 0;
@@ -298,6 +300,9 @@ extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t
     m->NSV0 = sc[3];
     m->user_creases = (m->K0 - m->B0) > 0;
     CU(cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&m->side_stream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
     m->last_launches = L.n;
     *out = m;
     g_err.clear();
@@ -475,6 +480,9 @@ static VSegs make_segs(alsub_mesh *m, int l) {
 
 static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     const int scheme = m->scheme, levels = m->levels;
+    L.side = m->side_stream;
+    L.ev_fork = m->ev_fork;
+    L.ev_join = m->ev_join;
     // a1-a3: level-0 mesh matrix, M^T by radix sort, edge index, creases
     L.level = -1;
     build0_validate(m->b0, s, L);
@@ -767,6 +775,9 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
     }
     const bool special = scheme != ALSUB_SQRT3 && m->K0 > 0;
     Launches L;
+    L.side = m->side_stream;
+    L.ev_fork = m->ev_fork;
+    L.ev_join = m->ev_join;
     for (int32_t f0 = 0; f0 < num_frames; f0 += nb) {
         const int n = std::min(nb, num_frames - f0);
         const float *Pin = frames_in + 3 * V0 * (int64_t)f0;
@@ -823,6 +834,9 @@ extern "C" void alsub_mesh_destroy(alsub_mesh *m) {
     free_list(m, m->mem_create, s);
     cudaStreamSynchronize(s);
     if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
+    if (m->side_stream) cudaStreamDestroy(m->side_stream);
+    if (m->ev_fork) cudaEventDestroy(m->ev_fork);
+    if (m->ev_join) cudaEventDestroy(m->ev_join);
     delete m;
 }
 

@@ -504,14 +504,22 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bo
             else launch(L, "cc_face", k_cc_face_gen<ORDER, ADJ, BND, 0>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo);
         }
     }
+    // the edge and vertex kernels only share read-only inputs: run them as parallel branches
+    const bool fork = L.can_fork();
+    cudaStream_t se = s;
+    if (fork) {
+        cudaEventRecord(L.ev_fork, s);
+        cudaStreamWaitEvent(L.side, L.ev_fork, 0);
+        se = L.side;
+    }
     if (gp && gp->E > 0) {
-        if (one) launch(L, "cc_edge", k_cc_edge_gp<1>, dim3(grid_for(gp->E)), dim3(kThreads), 0, s, p, gpd, fr);
-        else launch(L, "cc_edge", k_cc_edge_gp<0>, dim3(grid_for(gp->E)), dim3(kThreads), 0, s, p, gpd, fr);
+        if (one) launch(L, "cc_edge", k_cc_edge_gp<1>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, fr);
+        else launch(L, "cc_edge", k_cc_edge_gp<0>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, fr);
     } else if (p.E > 0) {
         constexpr int IT = 2;
         const unsigned gdim = grid_for(p.E, kThreads * IT);
-        if (one) launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 1, IT>, dim3(gdim), dim3(kThreads), 0, s, p, c, fr, topo);
-        else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT>, dim3(gdim), dim3(kThreads), 0, s, p, c, fr, topo);
+        if (one) launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 1, IT>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
+        else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
     }
     if (p.V > 0) {
         // >= 2 waves of 148 SMs for small levels, 4 vertices per thread for large ones
@@ -519,6 +527,10 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bo
                                                           std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
         if constexpr (ORDER == 4) launch(L, "cc_vertex", k_cc_vertex<4>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
         else launch(L, "cc_vertex", k_cc_vertex<0>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
+    }
+    if (fork) {
+        cudaEventRecord(L.ev_join, L.side);
+        cudaStreamWaitEvent(s, L.ev_join, 0);
     }
 }
 

@@ -13,6 +13,11 @@ namespace alsub {
 // Counts kernel launches issued into a stream (reported by alsub_last_launch_count).
 struct Launches {
     int64_t n = 0;
+    // optional second stream for independent kernels of a level (forked / joined with events;
+    // inside stream capture this becomes parallel graph branches)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool can_fork() const { return side != nullptr && !timing; }
     // optional per-kernel timing (alsub_refine_profile): an event after every launch
     bool timing = false;
     int level = -1;
