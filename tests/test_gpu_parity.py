@@ -245,3 +245,100 @@ def test_deterministic():
             m.refine("cc", 4)
             res.append(m.positions(4).cpu())
     assert torch.equal(res[0], res[1])
+
+
+# ------------------------------------------------------------------------------------------
+# more edge cases
+# ------------------------------------------------------------------------------------------
+
+def test_parity_shuffled_armor_L4():
+    """Locality stress: seeded random vertex/face relabelling + face rotations."""
+    compare(mg.shuffled(mg.armor9k()), "cc", 4, edges=True)
+
+
+def test_loop_boundary_and_creases():
+    """Loop on an open creased triangle grid: boundary = inf creases (reading R14) + semi-sharp."""
+    m = mg.grid(5, 4, tri_cells=[(i, j) for i in range(5) for j in range(4)])
+    vid = lambda i, j: j * 6 + i
+    m["crease"] = np.array([(vid(1, 2), vid(2, 2)), (vid(2, 2), vid(3, 2)), (vid(2, 1), vid(2, 2))], np.int32)
+    m["sigma"] = np.array([2.5, 0.5, np.inf], np.float32)
+    compare(m, "loop", 4)
+
+
+def test_plan_switch_and_dynamic_positions():
+    """The same handle refined with different schemes/levels, and new positions after the graph
+    was recorded (the graph reads the handle's level-0 buffer)."""
+    Mesh = _gpu()
+    mesh = mg.torus_tris(10, 8)
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"]) as m:
+        for scheme, L in (("loop", 3), ("sqrt3", 2), ("cc", 3), ("cc", 3), ("cc", 3)):
+            m.refine(scheme, L)
+            w = oracle.refine(mesh, scheme, L)[-1]
+            assert np.array_equal(m.topology(L)["face_vtx"].cpu().numpy(), w["face_vtx"])
+            assert np.abs(m.positions(L).cpu().numpy() - w["pos"]).max() / diag_of(mesh) < TOL
+        m2 = mg.random_positions(mesh, seed=9)
+        m.set_positions(torch.from_numpy(m2["pos"]).cuda())
+        m.refine("cc", 3)  # graph replay
+        w = oracle.refine(m2, "cc", 3)[-1]
+        assert np.abs(m.positions(3).cpu().numpy() - w["pos"]).max() / diag_of(m2) < TOL
+
+
+def test_eval_frames_many_batches_host_buffers():
+    """19 frames (2 full batches of 8 + a partial one), host input and output buffers."""
+    Mesh = _gpu()
+    mesh = mg.armor(6, 5, 6, 1, 1, 2, name="armor_small")
+    frames = np.stack([mg.frame_positions(mesh["pos"], t, 19) for t in range(19)])
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine("cc", 4)
+        VL = m.counts(4)["verts"]
+        out = np.zeros((19, VL, 3), np.float32)
+        from paper_1809_06047_b200 import alsub as A
+        A._check(A.lib().alsub_eval_frames(m._h, 4, frames.ctypes.data, 19, out.ctypes.data, None))
+        for t in (0, 8, 18):
+            mm = dict(mesh)
+            mm["pos"] = frames[t]
+            w = oracle.refine(mm, "cc", 4)[-1]["pos"]
+            assert np.abs(out[t] - w).max() / diag_of(mesh) < TOL
+        # levels below the refined depth
+        out2 = m.eval_frames(torch.from_numpy(frames[:3]).cuda(), 2)
+        w = oracle.refine(dict(mesh, pos=frames[2]), "cc", 2)[-1]["pos"]
+        assert np.abs(out2[2].cpu().numpy() - w).max() / diag_of(mesh) < TOL
+
+
+def test_overflow_is_reported():
+    """A level whose counts exceed int32 ids is refused with E_OVERFLOW, not computed wrongly."""
+    from paper_1809_06047_b200 import AlsubError
+    Mesh = _gpu()
+    mesh = mg.cube()
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"]) as m:
+        with pytest.raises(AlsubError) as ei:
+            m.refine("cc", 15)  # 6 * 4^15 faces * 4 slots > 2^31
+        assert ei.value.status == "E_OVERFLOW"
+        m.refine("cc", 2)  # the handle stays usable
+
+
+def test_level_counts_and_errors():
+    from paper_1809_06047_b200 import AlsubError
+    Mesh = _gpu()
+    mesh = mg.cube()
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"]) as m:
+        c0 = m.counts(0)
+        assert (c0["verts"], c0["faces"], c0["edges"], c0["face_order"]) == (8, 6, 12, 4)
+        with pytest.raises(AlsubError):
+            m.counts(1)  # not refined yet
+        m.refine("cc", 2)
+        assert m.counts(2)["faces"] == 96
+        with pytest.raises(AlsubError):
+            m.refine("cc", -1)
+        with pytest.raises(AlsubError):
+            m.positions(3)
+
+
+def test_device_tensor_inputs():
+    Mesh = _gpu()
+    mesh = mg.icosahedron()
+    t = lambda a: torch.from_numpy(a).cuda()
+    with Mesh(t(mesh["face_off"]), t(mesh["face_vtx"]), t(mesh["pos"])) as m:
+        m.refine("loop", 3)
+        w = oracle.refine(mesh, "loop", 3)[-1]
+        assert np.array_equal(m.topology(3)["face_vtx"].cpu().numpy(), w["face_vtx"])
