@@ -485,6 +485,13 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     L.ev_join = m->ev_join;
     // a1-a3: level-0 mesh matrix, M^T by radix sort, edge index, creases
     L.level = -1;
+    {
+        ZeroSegs z;
+        build0_zero_segments(m->b0, z);
+        for (int l = 1; l < levels; ++l)  // child boundary words (atomicOr targets of the edge kernels)
+            if (m->lv[l].bnd_word) z.add(m->lv[l].bnd_word, ceil_div(m->lv[l].E > 0 ? m->lv[l].E : 1, 32));
+        zero_segments(z, s, L);
+    }
     build0_validate(m->b0, s, L);
     build0_count_edges(m->b0, s, L);
     build0_fill(m->b0, false, s, L);
@@ -688,6 +695,7 @@ extern "C" alsub_status alsub_level_topology(const alsub_mesh *mc, int32_t level
             cd.face_edge = nullptr;
             cd.face_twin = nullptr;
             Frames fr0{nullptr, nullptr, 0, 0, 0, nullptr, 0};
+            if (Lx.bnd_word) CU(cudaMemsetAsync(Lx.bnd_word, 0, sizeof(uint32_t) * ceil_div(Lx.E, 32), s));
             VSegs g = make_segs(m, level - 1);
             cc_level(pd, cd, fr0, true, true, g, nullptr, s, Ln);
         }

@@ -341,14 +341,41 @@ static int bits_for(int32_t V) {
 
 static int passes_for(int32_t V) { return (bits_for(V) + 7) / 8; }
 
+// scratch arena: [one-sweep statuses | 5 scan status regions], each region 256-byte aligned, so a
+// single k_zero launch can initialise all of them for a refine
+static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+static size_t region_bytes(int32_t V, int32_t S) { return al(scan_scratch_bytes(std::max(V, S) + 1)); }
+static void *region(const Build0 &b, int k) {
+    if (!b.zeroed) return b.scratch;  // create: one region reused (memset before every use)
+    const size_t os = al(onesweep_scratch_bytes(b.S, passes_for(b.V)));
+    return (char *)b.scratch + (k == 0 ? 0 : os + (size_t)(k - 1) * region_bytes(b.V, b.S));
+}
 size_t build0_scratch_bytes(int32_t V, int32_t S) {
-    return std::max(onesweep_scratch_bytes(S, passes_for(V)), scan_scratch_bytes(std::max(V, S) + 1));
+    return al(onesweep_scratch_bytes(S, passes_for(V))) + 5 * region_bytes(V, S);
+}
+
+void build0_zero_segments(Build0 &b, ZeroSegs &z) {
+    const int32_t E = b.E, nw = (int32_t)ceil_div(E > 0 ? E : 1, 32);
+    z.add(b.vtx_cnt, (int64_t)b.V + 1);
+    z.add(b.digits, 256 * 4);
+    z.add(b.scalars + 1, 3);
+    z.add(b.bnd_word, nw);
+    z.add(b.vbnd, b.V);
+    z.add(b.edge_sigma, E);
+    z.add(b.edge_cidx, E, -1);
+    z.add(b.sp_flag, E);
+    z.add(b.sv_cnt, b.V);
+    z.add(b.sv_cur, b.V);
+    z.add(b.scratch, (int64_t)(build0_scratch_bytes(b.V, b.S) / 4));
+    b.zeroed = true;
 }
 
 // a1: validation + sort input + M^T row lengths + radix digit histograms
 void build0_validate(Build0 &b, cudaStream_t s, Launches &L) {
-    cudaMemsetAsync(b.vtx_cnt, 0, sizeof(int32_t) * ((size_t)b.V + 1), s);
-    cudaMemsetAsync(b.digits, 0, sizeof(int32_t) * 256 * 4, s);
+    if (!b.zeroed) {
+        cudaMemsetAsync(b.vtx_cnt, 0, sizeof(int32_t) * ((size_t)b.V + 1), s);
+        cudaMemsetAsync(b.digits, 0, sizeof(int32_t) * 256 * 4, s);
+    }
     if (b.F > 0) {
         launch(L, "b0_prep", k_b0_prep, dim3(grid_for(b.F)), dim3(kThreads), 0, s, b.face_off, b.face_vtx, b.F, b.V, passes_for(b.V), b.slot_face,
                                                      b.sort_k, b.sort_v, b.vtx_cnt, b.digits, b.flags);
@@ -359,13 +386,14 @@ void build0_validate(Build0 &b, cudaStream_t s, Launches &L) {
 // one-sweep radix sort -> vtx_slot aliases sort_v), then the per-vertex upper-triangle counts of E
 void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L) {
     T0 tp{b.face_off, b.slot_face};
-    scan_exclusive(b.vtx_cnt, b.vtx_off, (int64_t)b.V + 1, nullptr, b.scratch, s, L);
-    radix_sort_onesweep(b.sort_k, b.sort_v, b.sort_k2, b.sort_v2, b.S, bits_for(b.V), b.digits, true, b.scratch, s, L);
+    scan_exclusive(b.vtx_cnt, b.vtx_off, (int64_t)b.V + 1, nullptr, region(b, 1), s, L, b.zeroed);
+    radix_sort_onesweep(b.sort_k, b.sort_v, b.sort_k2, b.sort_v2, b.S, bits_for(b.V), b.digits, true, region(b, 0), s,
+                        L, b.zeroed);
     if (b.V > 0) {
         launch(L, "b0_edge_count", k_edge_count, dim3(grid_for(32 * (int64_t)b.V)), dim3(kThreads), 0, s, b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
                                                                         b.edge_cnt);
     }
-    scan_exclusive(b.edge_cnt, b.edge_off, b.V, b.scalars + 0, b.scratch, s, L);
+    scan_exclusive(b.edge_cnt, b.edge_off, b.V, b.scalars + 0, region(b, 2), s, L, b.zeroed);
 }
 
 // numeric a3 + crease matrix + special lists
@@ -373,9 +401,11 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     T0 tp{b.face_off, b.slot_face};
     const int32_t E = b.E;
     const int32_t nw = (int32_t)ceil_div(E > 0 ? E : 1, 32);
-    cudaMemsetAsync(b.scalars + 1, 0, 3 * sizeof(int32_t), s);
-    cudaMemsetAsync(b.bnd_word, 0, sizeof(uint32_t) * nw, s);
-    if (b.V > 0) cudaMemsetAsync(b.vbnd, 0, sizeof(int32_t) * b.V, s);
+    if (!b.zeroed) {
+        cudaMemsetAsync(b.scalars + 1, 0, 3 * sizeof(int32_t), s);
+        cudaMemsetAsync(b.bnd_word, 0, sizeof(uint32_t) * nw, s);
+        if (b.V > 0) cudaMemsetAsync(b.vbnd, 0, sizeof(int32_t) * b.V, s);
+    }
     if (b.V > 0) {
         launch(L, "b0_edge_fill", k_edge_fill, dim3(grid_for(32 * (int64_t)b.V)), dim3(kThreads), 0, s, b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
                                                                        b.edge_off, b.face_edge, b.face_twin, b.edge_hh,
@@ -385,12 +415,12 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
             launch(L, "b0_check_fans", k_check_fans, dim3(grid_for(b.V)), dim3(kThreads), 0, s, b.face_twin, b.vtx_off, b.vtx_slot0, tp, b.V, b.flags);
         }
     }
-    if (E > 0) {
+    if (E > 0 && !b.zeroed) {
         cudaMemsetAsync(b.edge_sigma, 0, sizeof(float) * E, s);
         cudaMemsetAsync(b.edge_cidx, 0xff, sizeof(int32_t) * E, s);
         cudaMemsetAsync(b.sp_flag, 0, sizeof(int32_t) * E, s);
     }
-    if (b.V > 0) {
+    if (b.V > 0 && !b.zeroed) {
         cudaMemsetAsync(b.sv_cnt, 0, sizeof(int32_t) * b.V, s);
         cudaMemsetAsync(b.sv_cur, 0, sizeof(int32_t) * b.V, s);
     }
@@ -398,13 +428,13 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     launch(L, "b0_flags", k_b0_flags, dim3(grid_for(nf)), dim3(kThreads), 0, s, b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
                                                  b.face_edge, b.edge_hh, tp, b.V, E, b.bnd_word, nw, b.edge_sigma,
                                                  b.edge_cidx, b.sp_flag, b.bnd_wcnt, b.flags);
-    scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, b.scratch, s, L);
-    scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, b.scratch, s, L);
+    scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, region(b, 3), s, L, b.zeroed);
+    scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, region(b, 4), s, L, b.zeroed);
     if (E > 0) {
         launch(L, "b0_special", k_b0_special, dim3(grid_for(E)), dim3(kThreads), 0, s, b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp, E,
                                                       b.sp, b.sv_cnt);
     }
-    scan_exclusive(b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V, b.scratch, s, L);
+    scan_exclusive(b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V, region(b, 5), s, L, b.zeroed);
     if (E > 0) {
         launch(L, "b0_sv_list", k_b0_svlist, dim3(grid_for(E)), dim3(kThreads), 0, s, b.sp, b.scalars + 2, E, b.sv_off, b.sv_cur, b.sv_list);
     }

@@ -548,10 +548,6 @@ static void cc_dispatch(const LevelDev &p, const ChildDev &c, const Frames &fr, 
 
 void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &g,
               const LevelDev *gp, cudaStream_t s, Launches &L) {
-    if (adj && topo && p.B > 0) {
-        const int32_t nw = (int32_t)ceil_div(c.E > 0 ? c.E : 1, 32);
-        cudaMemsetAsync(c.bnd_word, 0, sizeof(uint32_t) * nw, s);
-    }
     // level-0 meshes of uniform order use the generic kernels too (their M^T comes from the sort);
     // levels >= 1 are reduced quad matrices
     if (p.order == 4 && p.face_off == nullptr) cc_dispatch<4>(p, c, fr, topo, adj, g, gp, s, L);

@@ -69,7 +69,18 @@ inline unsigned grid_for(int64_t n, int threads = kThreads) {
 // receives the sum.  `scratch` must hold scan_scratch_bytes(n) bytes.
 size_t scan_scratch_bytes(int64_t n);
 void scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *total, void *scratch,
-                    cudaStream_t s, Launches &L);
+                    cudaStream_t s, Launches &L, bool prezeroed = false);
+// initialise up to 16 int32 arrays in one launch
+struct ZeroSegs {
+    int n = 0;
+    int32_t *ptr[32];
+    int64_t words[32];
+    int32_t value[32];
+    void add(void *p, int64_t w, int32_t v = 0) {
+        if (p && w > 0) { ptr[n] = (int32_t *)p; words[n] = w; value[n] = v; ++n; }
+    }
+};
+void zero_segments(const ZeroSegs &z, cudaStream_t s, Launches &L);
 // LSD radix sort of (key, value) int32 pairs, keys in [0, 2^bits).  Stable.  Result in
 // keys/vals; keys_alt/vals_alt are ping-pong buffers of n entries.
 size_t sort_scratch_bytes(int64_t n);
@@ -80,7 +91,8 @@ void radix_sort_pairs(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *
 // keys/vals when the number of passes is even, else copied back.
 size_t onesweep_scratch_bytes(int64_t n, int passes);
 void radix_sort_onesweep(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *vals_alt, int64_t n, int bits,
-                         int32_t *counts, bool counts_ready, void *scratch, cudaStream_t s, Launches &L);
+                         int32_t *counts, bool counts_ready, void *scratch, cudaStream_t s, Launches &L,
+                         bool prezeroed = false);
 // CSR offsets of sorted keys: off[v] = first i with key[i] >= v, v in [0, nkeys] (run-length).
 void offsets_from_sorted(const int32_t *keys, int64_t n, int32_t *off, int32_t nkeys, cudaStream_t s,
                          Launches &L);
@@ -115,8 +127,11 @@ struct Build0 {
     int32_t *scalars;             // device scalars: [0] E, [1] B, [2] K special, [3] NSV
     int32_t E;                    // host-known after the count pass (create) or plan (refine)
     void *scratch;
+    bool zeroed = false;          // refine: every work array and scan region pre-initialised by k_zero
 };
 size_t build0_scratch_bytes(int32_t V, int32_t S);
+// refine: add the level-0 work arrays / scan regions to z (one k_zero launch instead of memsets)
+void build0_zero_segments(Build0 &b, ZeroSegs &z);
 void build0_validate(Build0 &b, cudaStream_t s, Launches &L);
 void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L);  // through edge_off + scalars[0]
 void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L);  // needs b.E
@@ -181,6 +196,7 @@ struct VSegs {
 
 // mode: adj = emit child adjacency (not the last level); topo = emit child faces;
 //       acc = accumulate crease valency/sharpness (refine) vs reuse stored (eval_frames)
+// The child boundary words (c.bnd_word) must be zero on entry when adj && p.B > 0.
 // gp (nullable) = the grandparent level: at the last refined level (>= 2) the face kernel
 // recomputes its edge ids from gp's rows and the edge kernel iterates gp's edges
 void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &segs,

@@ -118,12 +118,12 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t *__restrict
 }
 
 void scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *total, void *scratch, cudaStream_t s,
-                    Launches &L) {
+                    Launches &L, bool prezeroed) {
     if (n <= 0) {
         if (total) cudaMemsetAsync(total, 0, sizeof(int32_t), s);
         return;
     }
-    cudaMemsetAsync(scratch, 0, scan_scratch_bytes(n), s);
+    if (!prezeroed) cudaMemsetAsync(scratch, 0, scan_scratch_bytes(n), s);
     int64_t tiles = ceil_div(n, kScanTile);
     launch(L, "scan", k_scan, dim3((unsigned)tiles), dim3(kScanThreads), 0, s, in, out, n, (unsigned long long *)scratch, total);
 }
@@ -346,7 +346,8 @@ __global__ void __launch_bounds__(kOsThreads) k_os_pass(const int32_t *__restric
 }
 
 void radix_sort_onesweep(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *vals_alt, int64_t n, int bits,
-                         int32_t *counts, bool counts_ready, void *scratch, cudaStream_t s, Launches &L) {
+                         int32_t *counts, bool counts_ready, void *scratch, cudaStream_t s, Launches &L,
+                         bool prezeroed) {
     int passes = (bits + 7) / 8;
     if (passes < 1) passes = 1;
     if (n <= 1) return;
@@ -354,7 +355,7 @@ void radix_sort_onesweep(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_
         cudaMemsetAsync(counts, 0, sizeof(int32_t) * 256 * passes, s);
         launch(L, "os_hist", k_os_hist, dim3((unsigned)std::min<int64_t>(ceil_div(n, kOsThreads), 4 * 148)), dim3(kOsThreads), 0, s, keys, n, passes, counts);
     }
-    cudaMemsetAsync(scratch, 0, onesweep_scratch_bytes(n, passes), s);
+    if (!prezeroed) cudaMemsetAsync(scratch, 0, onesweep_scratch_bytes(n, passes), s);
     const int64_t tiles = os_tiles(n);
     int32_t *ka = keys, *va = vals, *kb = keys_alt, *vb = vals_alt;
     for (int p = 0; p < passes; ++p) {
@@ -369,6 +370,23 @@ void radix_sort_onesweep(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_
         cudaMemcpyAsync(keys, ka, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
         cudaMemcpyAsync(vals, va, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
     }
+}
+
+// ------------------------------------------------------------------------------------------
+// one launch that initialises many small arrays (replaces a chain of memset graph nodes)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_zero(ZeroSegs z) {
+    ALSUB_GRID_WAIT();
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    for (int k = 0; k < z.n; ++k)
+        for (int64_t i = tid; i < z.words[k]; i += nth) z.ptr[k][i] = z.value[k];
+}
+
+void zero_segments(const ZeroSegs &z, cudaStream_t s, Launches &L) {
+    int64_t mx = 0;
+    for (int k = 0; k < z.n; ++k) mx = std::max(mx, z.words[k]);
+    if (mx == 0) return;
+    launch(L, "zero", k_zero, dim3((unsigned)std::min<int64_t>(ceil_div(mx, kThreads), 4 * 148)), dim3(kThreads), 0, s, z);
 }
 
 // ------------------------------------------------------------------------------------------
