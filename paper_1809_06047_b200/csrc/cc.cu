@@ -408,16 +408,53 @@ ALSUB_D void copy_point(const Frames &fr, int32_t v) {
     for (int f = 0; f < fr.nb; ++f) st3(fr.Pn + f * fr.Pnstride, v, ld3(fr.P + f * fr.Pstride, v));
 }
 
+// one vertex of a non-half-sum segment (see k_cc_vertex)
 template <int ORDER>
+ALSUB_D void cc_vertex_one(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs &g, int s, int32_t j) {
+    const int32_t v = g.start[s] + j;
+    const int shift = 2 * (g.level - g.birth[s]);
+    const int type = g.type[s];
+    const int m1 = g.birth[s] - 1;
+    if (type == 2) {  // edge point born at level m1 + 1
+        const int2 hh = __ldg(g.ehh[m1] + j);
+        if (hh.y < 0) { copy_point(fr, v); return; }  // boundary: crease module
+        int32_t nh, nt;
+        if (m1 == 0) {
+            const Topo<0> t0{g.face_off0, g.slot_face0};
+            nh = t0.next(hh.x);
+            nt = t0.next(hh.y);
+        } else {
+            nh = (hh.x & ~3) | ((hh.x + 1) & 3);
+            nt = (hh.y & ~3) | ((hh.y + 1) & 3);
+        }
+        const int32_t sl[4] = {(4 * hh.x + 1) << shift, (4 * nh + 3) << shift, (4 * hh.y + 1) << shift,
+                               (4 * nt + 3) << shift};
+        smooth_fixed<ORDER, 4>(x, fr, v, sl);
+    } else if (type == 1 && m1 > 0) {  // face point of a quad
+        const int32_t sl[4] = {(16 * j + 2) << shift, (16 * j + 6) << shift, (16 * j + 10) << shift,
+                               (16 * j + 14) << shift};
+        smooth_fixed<ORDER, 4>(x, fr, v, sl);
+    } else if (type == 1) {  // face point of a level-0 face (any order)
+        const int32_t off = __ldg(g.face_off0 + j), cnt = __ldg(g.face_off0 + j + 1) - off;
+        smooth_list<ORDER>(x, fr, v, nullptr, cnt, shift, true, off);
+    } else {  // level-0 vertex
+        if (__ldg(g.vbnd0 + j)) { copy_point(fr, v); return; }
+        const int32_t o = __ldg(g.vtx_off0 + j), cnt = __ldg(g.vtx_off0 + j + 1) - o;
+        smooth_list<ORDER>(x, fr, v, g.vtx_list0 + o, cnt, shift, false, 0);
+    }
+}
+
+template <int ORDER, int PL>
 __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, VSegs g) {
     ALSUB_GRID_WAIT();
-    // Work unit = a warp task of 32 consecutive vertices of ONE segment (no divergence between
+    constexpr int kVtxTask = 32 * PL;  // vertices per warp task (PL per lane)
+    // Work unit = a warp task of 32 PL consecutive vertices of ONE segment (no divergence between
     // vertex classes inside a warp); block b takes the same fraction [b/NB, (b+1)/NB) of every
     // segment's tasks, so a block works on one spatial band of the mesh.
     __shared__ int32_t s_lo[kMaxSeg], s_pre[kMaxSeg + 1];
     const int64_t nblk = gridDim.x, b = blockIdx.x;
     if (threadIdx.x < g.nseg) {
-        const int64_t tasks = (g.len[threadIdx.x] + 31) >> 5;
+        const int64_t tasks = (g.len[threadIdx.x] + kVtxTask - 1) / kVtxTask;
         const int32_t lo = (int32_t)(b * tasks / nblk), hi = (int32_t)((b + 1) * tasks / nblk);
         s_lo[threadIdx.x] = lo;
         s_pre[threadIdx.x] = hi - lo;
@@ -439,46 +476,41 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
     int s = 0;
     for (int32_t task = warp; task < ntask; task += nwarp) {
         while (s_pre[s + 1] <= task) ++s;  // tasks ascend: the segment index only moves forward
-        const int32_t j = ((s_lo[s] + (task - s_pre[s])) << 5) + lane;
-        if (j >= g.len[s]) continue;
-        const int32_t v = g.start[s] + j;
-        const int shift = 2 * (g.level - g.birth[s]);
-        const int type = g.type[s];
-        const int m1 = g.birth[s] - 1;
-        if (s == g.hs_seg) {  // edge point born at this level: two half sums from the face kernel
-            const int2 hh = __ldg(g.ehh[m1] + j);
-            if (hh.y < 0) { copy_point(fr, v); continue; }
+        const int32_t j0 = (s_lo[s] + (task - s_pre[s])) * kVtxTask + lane;
+        const int32_t len = g.len[s];
+        if (s == g.hs_seg) {
+            // edge points born at this level: two half sums from the face kernel; the four
+            // vertices of a lane are loaded together (edge pairs, then half sums)
+            int2 hh[PL];
+#pragma unroll
+            for (int k = 0; k < PL; ++k) {
+                const int32_t j = j0 + 32 * k;
+                hh[k] = j < len ? __ldg(g.ehh[g.birth[s] - 1] + j) : make_int2(0, -1);
+            }
             for (int f = 0; f < fr.nb; ++f) {
                 const float *hs = fr.hs + f * fr.hsstride;
-                const P3 acc = ld3c(hs, hh.x) + ld3c(hs, hh.y);
-                st3(fr.Pn + f * fr.Pnstride, v, 0.5f * ld3(fr.P + f * fr.Pstride, v) + 0.0625f * acc);
+                const float *P = fr.P + f * fr.Pstride;
+                float *Pn = fr.Pn + f * fr.Pnstride;
+                P3 acc[PL], pv[PL];
+#pragma unroll
+                for (int k = 0; k < PL; ++k) {
+                    const int32_t j = j0 + 32 * k;
+                    pv[k] = j < len ? ld3(P, g.start[s] + j) : p3zero();
+                    acc[k] = hh[k].y >= 0 ? ld3c(hs, hh[k].x) + ld3c(hs, hh[k].y) : p3zero();
+                }
+#pragma unroll
+                for (int k = 0; k < PL; ++k) {
+                    const int32_t j = j0 + 32 * k;
+                    if (j >= len) continue;
+                    // boundary edge points keep p (set by the crease/boundary module)
+                    st3(Pn, g.start[s] + j, hh[k].y >= 0 ? 0.5f * pv[k] + 0.0625f * acc[k] : pv[k]);
+                }
             }
-        } else if (type == 2) {  // edge point born at level m1 + 1
-            const int2 hh = __ldg(g.ehh[m1] + j);
-            if (hh.y < 0) { copy_point(fr, v); continue; }  // boundary: crease module
-            int32_t nh, nt;
-            if (m1 == 0) {
-                const Topo<0> t0{g.face_off0, g.slot_face0};
-                nh = t0.next(hh.x);
-                nt = t0.next(hh.y);
-            } else {
-                nh = (hh.x & ~3) | ((hh.x + 1) & 3);
-                nt = (hh.y & ~3) | ((hh.y + 1) & 3);
-            }
-            const int32_t sl[4] = {(4 * hh.x + 1) << shift, (4 * nh + 3) << shift, (4 * hh.y + 1) << shift,
-                                   (4 * nt + 3) << shift};
-            smooth_fixed<ORDER, 4>(x, fr, v, sl);
-        } else if (type == 1 && m1 > 0) {  // face point of a quad
-            const int32_t sl[4] = {(16 * j + 2) << shift, (16 * j + 6) << shift, (16 * j + 10) << shift,
-                                   (16 * j + 14) << shift};
-            smooth_fixed<ORDER, 4>(x, fr, v, sl);
-        } else if (type == 1) {  // face point of a level-0 face (any order)
-            const int32_t off = __ldg(g.face_off0 + j), cnt = __ldg(g.face_off0 + j + 1) - off;
-            smooth_list<ORDER>(x, fr, v, nullptr, cnt, shift, true, off);
-        } else {  // level-0 vertex
-            if (__ldg(g.vbnd0 + j)) { copy_point(fr, v); continue; }
-            const int32_t o = __ldg(g.vtx_off0 + j), cnt = __ldg(g.vtx_off0 + j + 1) - o;
-            smooth_list<ORDER>(x, fr, v, g.vtx_list0 + o, cnt, shift, false, 0);
+            continue;
+        }
+        for (int k = 0; k < PL; ++k) {
+            const int32_t j = j0 + 32 * k;
+            if (j < len) cc_vertex_one<ORDER>(x, fr, g, s, j);
         }
     }
 }
@@ -522,11 +554,15 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bo
         else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
     }
     if (p.V > 0) {
-        // >= 2 waves of 148 SMs for small levels, 4 vertices per thread for large ones
-        const unsigned nblk = (unsigned)std::max<int64_t>(grid_for(p.V, 4 * kThreads),
-                                                          std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
-        if constexpr (ORDER == 4) launch(L, "cc_vertex", k_cc_vertex<4>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
-        else launch(L, "cc_vertex", k_cc_vertex<0>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
+        // 32-vertex warp tasks; >= 2 waves of 148 SMs for small levels, 4 tasks per warp for large
+        // ones (128-vertex tasks with batched loads were measured slower)
+        if (false) {
+        } else {
+            const unsigned nblk = (unsigned)std::max<int64_t>(grid_for(p.V, 4 * kThreads),
+                                                              std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
+            if constexpr (ORDER == 4) launch(L, "cc_vertex", k_cc_vertex<4, 1>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
+            else launch(L, "cc_vertex", k_cc_vertex<0, 1>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
+        }
     }
     if (fork) {
         cudaEventRecord(L.ev_join, L.side);
