@@ -770,7 +770,7 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
     const bool in_dev = is_device_ptr(frames_in), out_dev = is_device_ptr(frames_out);
     const int nb_max = 8;
     const int nb = std::min(num_frames, nb_max);
-    // per-level batch buffers: [nb][V_l][3] for l = 0 (if host input) .. levels (if host output)
+    // per-level batch buffers of 3 V_l nb floats for l = 0 (if host input) .. levels (if host output)
     if (m->frames_nb < nb || (int)m->frame_buf.size() != m->levels + 1) {
         free_list(m, m->mem_frames, s);
         m->frame_buf.assign((size_t)m->levels + 1, nullptr);
@@ -802,6 +802,8 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
             p.sv_vtx = m->sv_vtx;
             p.sv_off = m->sv_off;
             ChildDev c{};
+            // frame-major [n][V][3] at every level (a frame-interleaved [V][n][3] layout was measured
+            // slower: its per-frame stores are strided)
             Frames fr{P, Pn, 3 * Pl.V, 3 * m->lv[l + 1].V, n, m->frame_hs, m->hs_elems};
             if (scheme == ALSUB_CATMULL_CLARK) {
                 VSegs g = make_segs(m, l);

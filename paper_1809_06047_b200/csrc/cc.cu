@@ -77,8 +77,8 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
         else fe = __ldg(reinterpret_cast<const int4 *>(p.face_edge) + r);
     }
     for (int f = 0; f < nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
-        float *Pn = fr.Pn + f * fr.Pnstride;
+        const PR P = fr.rd(f);
+        const PW Pn = fr.wr(f);
         const P3 p0 = ld3(P, v[0]), p1 = ld3(P, v[1]), p2 = ld3(P, v[2]), p3 = ld3(P, v[3]);
         const P3 fc = 0.25f * (p0 + p1 + p2 + p3);
         if (valid) st3(Pn, V + r, fc);
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
             qn.x = __shfl_sync(0xffffffffu, q.x, src);
             qn.y = __shfl_sync(0xffffffffu, q.y, src);
             qn.z = __shfl_sync(0xffffffffu, q.z, src);
-            if (valid) st3(fr.hs + f * fr.hsstride, r, p2 + fc + qn);
+            if (valid) st3(fr.hsw(f), r, p2 + fc + qn);
             // (2) corner 2 of the four children of a quad is the parent's face point (born at this
             // level, valence 4): its vertex point needs exactly these four faces' f and their
             // corner-3 vertices -- reduce over the 4 sibling lanes (no gather, no vertex pass)
@@ -157,10 +157,10 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_gen(LevelDev p, ChildDev c
     const float inv = 1.0f / (float)n;
     const int nb = NBC ? NBC : fr.nb;
     for (int f = 0; f < nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
+        const PR P = fr.rd(f);
         P3 s = p3zero();
         for (int32_t t = 0; t < n; ++t) s = s + ld3(P, __ldg(p.face_vtx + o + t));
-        st3(fr.Pn + f * fr.Pnstride, V + r, inv * s);
+        st3(fr.wr(f), V + r, inv * s);
     }
     if (!topo) return;
     for (int32_t t = 0; t < n; ++t) {
@@ -221,8 +221,8 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
 #pragma unroll
     for (int k = 0; k < IT; ++k) edge_ends<ORDER>(p, tp, hv[k], va[k], vb[k], hn[k]);
     for (int f = 0; f < nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
-        float *Pn = fr.Pn + f * fr.Pnstride;
+        const PR P = fr.rd(f);
+        const PW Pn = fr.wr(f);
         P3 ab[IT], fs[IT];
 #pragma unroll
         for (int k = 0; k < IT; ++k) {
@@ -320,8 +320,8 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
     const int32_t base0 = s_base0, n = s_end - base0;
     const int32_t o = base - base0;
     for (int f = 0; f < nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
-        float *Pn = fr.Pn + f * fr.Pnstride;
+        const PR P = fr.rd(f);
+        const PW Pn = fr.wr(f);
         if (valid) {
             const P3 plo = ld3(P, lo), phi = ld3(P, hi), pep = ld3(P, ep), pR = ld3(P, fpR);
             const P3 fh = ld3c(Pn, V + h), fnh = ld3c(Pn, V + nh);
@@ -345,8 +345,13 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
             }
         }
         __syncthreads();
-        float *dst = Pn + 3 * ((int64_t)V + F + base0);
-        for (int32_t i = threadIdx.x; i < 3 * n; i += blockDim.x) dst[i] = s_out[i];
+        if (Pn.vs == 3) {
+            float *dst = Pn.p + 3 * ((int64_t)V + F + base0);
+            for (int32_t i = threadIdx.x; i < 3 * n; i += blockDim.x) dst[i] = s_out[i];
+        } else {
+            for (int32_t i = threadIdx.x; i < n; i += blockDim.x)
+                st3(Pn, (int64_t)V + F + base0 + i, P3{s_out[3 * i], s_out[3 * i + 1], s_out[3 * i + 2]});
+        }
         __syncthreads();
     }
 }
@@ -377,8 +382,8 @@ ALSUB_D void smooth_fixed(const VtxCtx<ORDER> &x, const Frames &fr, int32_t v, c
     }
     constexpr float inv = 1.0f / (float)N;
     for (int f = 0; f < fr.nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
-        float *Pn = fr.Pn + f * fr.Pnstride;
+        const PR P = fr.rd(f);
+        const PW Pn = fr.wr(f);
         P3 acc = ld3(P, nb[0]) + ld3c(Pn, fc[0]);
 #pragma unroll
         for (int k = 1; k < N; ++k) acc = acc + ld3(P, nb[k]) + ld3c(Pn, fc[k]);
@@ -390,8 +395,8 @@ template <int ORDER>
 ALSUB_D void smooth_list(const VtxCtx<ORDER> &x, const Frames &fr, int32_t v, const int32_t *list, int32_t n,
                          int shift, bool quad_fp, int32_t off) {
     for (int f = 0; f < fr.nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
-        float *Pn = fr.Pn + f * fr.Pnstride;
+        const PR P = fr.rd(f);
+        const PW Pn = fr.wr(f);
         P3 acc = p3zero();
         for (int32_t k = 0; k < n; ++k) {
             const int32_t s = quad_fp ? ((4 * (off + k) + 2) << shift) : (__ldg(list + k) << shift);
@@ -405,7 +410,7 @@ ALSUB_D void smooth_list(const VtxCtx<ORDER> &x, const Frames &fr, int32_t v, co
 }
 
 ALSUB_D void copy_point(const Frames &fr, int32_t v) {
-    for (int f = 0; f < fr.nb; ++f) st3(fr.Pn + f * fr.Pnstride, v, ld3(fr.P + f * fr.Pstride, v));
+    for (int f = 0; f < fr.nb; ++f) st3(fr.wr(f), v, ld3(fr.rd(f), v));
 }
 
 // one vertex of a non-half-sum segment (see k_cc_vertex)
@@ -488,9 +493,9 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
                 hh[k] = j < len ? __ldg(g.ehh[g.birth[s] - 1] + j) : make_int2(0, -1);
             }
             for (int f = 0; f < fr.nb; ++f) {
-                const float *hs = fr.hs + f * fr.hsstride;
-                const float *P = fr.P + f * fr.Pstride;
-                float *Pn = fr.Pn + f * fr.Pnstride;
+                const PR hs = fr.hsr(f);
+                const PR P = fr.rd(f);
+                const PW Pn = fr.wr(f);
                 P3 acc[PL], pv[PL];
 #pragma unroll
                 for (int k = 0; k < PL; ++k) {

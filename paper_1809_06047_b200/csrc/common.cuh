@@ -75,6 +75,34 @@ ALSUB_D void st3(float *P, int64_t v, P3 a) {
     p[1] = a.y;
     p[2] = a.z;
 }
+// strided views of one frame's positions: element v at p + vs * v (vs = 3 for the API layout
+// [V][3]; vs = 3 nb for the frame-interleaved batches [V][nb][3] of alsub_eval_frames)
+struct PR {
+    const float *p;
+    int32_t vs;
+};
+struct PW {
+    float *p;
+    int32_t vs;
+};
+ALSUB_D P3 ld3(PR P, int64_t v) {
+    const float *q = P.p + P.vs * v;
+    return P3{__ldg(q), __ldg(q + 1), __ldg(q + 2)};
+}
+ALSUB_D P3 ld3c(PR P, int64_t v) {
+    const float *q = P.p + P.vs * v;
+    return P3{q[0], q[1], q[2]};
+}
+ALSUB_D P3 ld3c(PW P, int64_t v) {
+    const float *q = P.p + P.vs * v;
+    return P3{q[0], q[1], q[2]};
+}
+ALSUB_D void st3(PW P, int64_t v, P3 a) {
+    float *q = P.p + P.vs * v;
+    q[0] = a.x;
+    q[1] = a.y;
+    q[2] = a.z;
+}
 ALSUB_D P3 operator+(P3 a, P3 b) { return P3{a.x + b.x, a.y + b.y, a.z + b.z}; }
 ALSUB_D P3 operator*(float s, P3 a) { return P3{s * a.x, s * a.y, s * a.z}; }
 ALSUB_D P3 p3zero() { return P3{0.f, 0.f, 0.f}; }

@@ -56,8 +56,8 @@ __global__ void __launch_bounds__(kThreads) k_crease(CreaseArgs A) {
         const float sg = se.sigma;
         if (sg > 0.0f) {
             for (int f = 0; f < fr.nb; ++f) {
-                const float *P = fr.P + f * fr.Pstride;
-                float *Pn = fr.Pn + f * fr.Pnstride;
+                const PR P = fr.rd(f);
+                const PW Pn = fr.wr(f);
                 const P3 mid = 0.5f * (ld3(P, se.a) + ld3(P, se.b));
                 const int64_t o = (int64_t)A.ep_base + se.e;
                 if (sg >= 1.0f) st3(Pn, o, mid);  // includes +inf (boundary)
@@ -113,8 +113,8 @@ __global__ void __launch_bounds__(kThreads) k_crease(CreaseArgs A) {
     if (k < 2) return;
     const float s = inf ? __int_as_float(0x7f800000) : sum / (float)k;
     for (int f = 0; f < fr.nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
-        float *Pn = fr.Pn + f * fr.Pnstride;
+        const PR P = fr.rd(f);
+        const PW Pn = fr.wr(f);
         const P3 pv = ld3(P, v);
         const P3 sh = k == 2 ? 0.75f * pv + 0.125f * (ld3(P, nb0) + ld3(P, nb1)) : pv;
         if (s >= 1.0f) st3(Pn, v, sh);

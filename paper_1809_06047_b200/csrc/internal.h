@@ -172,6 +172,11 @@ struct Frames {
     // (= per face of this level), written by the face kernel, read by the vertex kernel
     float *hs = nullptr;
     int64_t hsstride = 0;
+    // per-frame views ([V][3], vertex stride 3)
+    ALSUB_HD PR rd(int f) const { return PR{P + f * Pstride, 3}; }
+    ALSUB_HD PW wr(int f) const { return PW{Pn + f * Pnstride, 3}; }
+    ALSUB_HD PW hsw(int f) const { return PW{hs + f * hsstride, 3}; }
+    ALSUB_HD PR hsr(int f) const { return PR{hs + f * hsstride, 3}; }
 };
 
 // Vertex-id segments of a CC level: level-l vertex ids are

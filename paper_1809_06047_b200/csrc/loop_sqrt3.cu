@@ -170,10 +170,10 @@ __global__ void __launch_bounds__(kThreads) k_loop_edge(LevelDev p, ChildDev c, 
     const int32_t g2 = tw >= 0 ? __ldg(p.face_vtx + tri_prev(tw)) : -1;
     const int32_t V = p.V;
     for (int f = 0; f < fr.nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
+        const PR P = fr.rd(f);
         const P3 ab = ld3(P, va) + ld3(P, vb);
         P3 out = tw < 0 ? 0.5f * ab : 0.375f * ab + 0.125f * (ld3(P, g1) + ld3(P, g2));
-        st3(fr.Pn + f * fr.Pnstride, (int64_t)V + e, out);
+        st3(fr.wr(f), (int64_t)V + e, out);
     }
     if constexpr (ADJ) {
         const int32_t base = __ldg(p.loop_base + e);
@@ -198,8 +198,8 @@ __global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c
     const int32_t h0 = __ldg(p.vtx_slot0 + v);
     if constexpr (ADJ) c.vtx_slot0[v] = h0 >= 0 ? loop_c0(h0) : -1;
     for (int f = 0; f < fr.nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
-        float *Pn = fr.Pn + f * fr.Pnstride;
+        const PR P = fr.rd(f);
+        const PW Pn = fr.wr(f);
         const P3 pv = ld3(P, v);
         if (h0 < 0) { st3(Pn, v, pv); continue; }
         P3 acc = p3zero();
@@ -269,9 +269,9 @@ __global__ void __launch_bounds__(kThreads) k_s3_face(LevelDev p, ChildDev c, Fr
     }
     const int nb = NBC ? NBC : fr.nb;
     for (int f = 0; f < nb; ++f) {
-        const float *P = fr.P + f * fr.Pstride;
+        const PR P = fr.rd(f);
         const P3 s = ld3(P, v[0]) + ld3(P, v[1]) + ld3(P, v[2]);
-        if (valid) st3(fr.Pn + f * fr.Pnstride, (int64_t)V + i, (1.0f / 3.0f) * s);
+        if (valid) st3(fr.wr(f), (int64_t)V + i, (1.0f / 3.0f) * s);
     }
     if (!topo) return;
     int32_t *stage = s_stage[threadIdx.x >> 5];
@@ -345,11 +345,11 @@ __global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, V
             }
             constexpr float alpha = 1.0f / 3.0f;  // alpha_6 = (4 - 2 cos(pi/3)) / 9
             for (int f = 0; f < nb; ++f) {
-                const float *P = fr.P + f * fr.Pstride;
+                const PR P = fr.rd(f);
                 P3 acc = ld3(P, nbv[0]);
 #pragma unroll
                 for (int k = 1; k < 6; ++k) acc = acc + ld3(P, nbv[k]);
-                st3(fr.Pn + f * fr.Pnstride, v, (1.0f - alpha) * ld3(P, v) + (alpha / 6.0f) * acc);
+                st3(fr.wr(f), v, (1.0f - alpha) * ld3(P, v) + (alpha / 6.0f) * acc);
             }
             continue;
         }
@@ -371,8 +371,8 @@ __global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, V
         }
         const float alpha = n > 0 ? sqrt3_alpha(n) : 0.0f;
         for (int f = 0; f < nb; ++f) {
-            const float *P = fr.P + f * fr.Pstride;
-            float *Pn = fr.Pn + f * fr.Pnstride;
+            const PR P = fr.rd(f);
+            const PW Pn = fr.wr(f);
             const P3 pv = ld3(P, v);
             if (n == 0) { st3(Pn, v, pv); continue; }
             P3 acc = p3zero();
