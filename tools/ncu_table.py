@@ -39,10 +39,12 @@ if out_md:
     # per (kernel family, level) DRAM bytes for bench.py's roofline.traffic; the CC level kernels of
     # one refine are captured in launch order, so launch index == level for cc_face/cc_edge/cc_vertex
     summ = {}
+    level = -1
     for d in rows:
         base = d['kernel'].split('<')[0].replace('k_', '', 1)
-        fam = {'cc_face_quad': 'cc_face', 'cc_face_gen': 'cc_face'}.get(base, base)
-        key = f"{fam}@L{d['launch'] if fam != 'cc_face' else sum(1 for x in rows[:rows.index(d)] if x['kernel'].startswith(('k_cc_face',)))}"
-        summ[key] = {'dram_bytes': d['dram__bytes_read.sum'] + d['dram__bytes_write.sum'],
-                     'time_us': d['gpu__time_duration.sum'] * 1e6, 'kernel': d['kernel']}
+        fam = {'cc_face_quad': 'cc_face', 'cc_face_gen': 'cc_face', 'cc_edge_gp': 'cc_edge'}.get(base, base)
+        if fam == 'cc_face':
+            level += 1  # the CC level kernels of one refine are captured in order face, edge, vertex
+        summ[f"{fam}@L{level}"] = {'dram_bytes': d['dram__bytes_read.sum'] + d['dram__bytes_write.sum'],
+                                   'time_us': d['gpu__time_duration.sum'] * 1e6, 'kernel': d['kernel']}
     json.dump({'source': rep, 'kernels': summ}, open(os.path.join(os.path.dirname(out_md), 'ncu_summary.json'), 'w'), indent=1)
