@@ -73,6 +73,7 @@ def kernel_bytes_cc(name, c, prev, lvl, levels):
         rd = 4 * S + 12 * V + (48 * Fp if gp_last else 4 * S) + (4 * S if adj else 0)
         wr = 12 * F + 16 * S + (16 * S if child_rows else 0) + (16 * S if child_twin else 0)
         wr += (12 * Fp + 12 * F) if fpv else 0    # new face-point vertices + half ring sums
+        wr += 12 * F if lvl >= 1 else 0             # corner-0 contributions c0
     elif name == "cc_edge":
         if gp_last:
             rd = 8 * Ep + 16 * Fp + 12 * V + 12 * F
@@ -80,7 +81,10 @@ def kernel_bytes_cc(name, c, prev, lvl, levels):
             rd = 8 * E + 4 * S + 12 * V + 12 * F
         wr = 12 * E + (8 * (2 * E + S) if child_rows else 0)
     elif name == "cc_vertex":
-        rd = 4 * S + 12 * V + 12 * F + 8 * Ep + (12 * F if fpv else 0)
+        if lvl >= 1:  # c0 sums for vertices born earlier, half sums for new edge points
+            rd = 12 * V + 12 * F + 8 * Ep + (12 * F if fpv else 0) + (0 if fpv else 4 * S + 12 * F)
+        else:
+            rd = 4 * S + 12 * V + 12 * F
         wr = 12 * (V - (Fp if fpv else 0))
     else:
         return None

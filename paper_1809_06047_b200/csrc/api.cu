@@ -79,6 +79,9 @@ struct alsub_mesh {
     int32_t *sv_vtx_create = nullptr, *sv_off_create = nullptr;
     float *hs = nullptr;          // half ring sums (CC, levels >= 2), [3 * max F_l] floats
     int64_t hs_elems = 0;
+    float *c0 = nullptr;          // corner-0 contributions (CC, levels >= 1), [3 * max F_l] floats
+    int64_t c0_elems = 0;
+    float *frame_c0 = nullptr;
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
     void *scratch_create = nullptr;
@@ -376,6 +379,10 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
     if (scheme == ALSUB_CATMULL_CLARK)
         for (int l = 2; l < levels; ++l) m->hs_elems = std::max<int64_t>(m->hs_elems, 3 * lv[l].F);
     m->hs = m->hs_elems ? A<float>(m, m->hs_elems, s, ML, ok) : nullptr;
+    m->c0_elems = 0;
+    if (scheme == ALSUB_CATMULL_CLARK)
+        for (int l = 1; l < levels; ++l) m->c0_elems = std::max<int64_t>(m->c0_elems, 3 * lv[l].F);
+    m->c0 = m->c0_elems ? A<float>(m, m->c0_elems, s, ML, ok) : nullptr;
     m->b0.sv_vtx = m->sv_vtx;
     m->b0.sv_off = m->sv_off;
     int64_t max_scan = std::max<int64_t>(m->V0, m->S0) + 1;
@@ -507,7 +514,7 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
         ChildDev c = child_of(C);
         c.sv_vtx = m->sv_vtx;
         c.sv_off = m->sv_off;
-        Frames fr{P.pos, C.pos, 3 * P.V, 3 * C.V, 1, m->hs, 0};
+        Frames fr{P.pos, C.pos, 3 * P.V, 3 * C.V, 1, m->hs, 0, l >= 1 ? m->c0 : nullptr, 0};
         if (scheme == ALSUB_CATMULL_CLARK) {
             VSegs g = make_segs(m, l);
             LevelDev gp{};
@@ -778,6 +785,7 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
         for (int l = 0; l <= m->levels; ++l)
             m->frame_buf[l] = A<float>(m, 3 * m->lv[l].V * nb, s, m->mem_frames, ok);
         m->frame_hs = m->hs_elems ? A<float>(m, m->hs_elems * nb, s, m->mem_frames, ok) : nullptr;
+        m->frame_c0 = m->c0_elems ? A<float>(m, m->c0_elems * nb, s, m->mem_frames, ok) : nullptr;
         if (!ok) return fail(ALSUB_E_NOMEM, "frame batch buffers");
         m->frames_nb = nb;
     }
@@ -804,7 +812,8 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
             ChildDev c{};
             // frame-major [n][V][3] at every level (a frame-interleaved [V][n][3] layout was measured
             // slower: its per-frame stores are strided)
-            Frames fr{P, Pn, 3 * Pl.V, 3 * m->lv[l + 1].V, n, m->frame_hs, m->hs_elems};
+            Frames fr{P, Pn, 3 * Pl.V, 3 * m->lv[l + 1].V, n, m->frame_hs, m->hs_elems,
+                      (l >= 1 && scheme == ALSUB_CATMULL_CLARK) ? m->frame_c0 : nullptr, m->c0_elems};
             if (scheme == ALSUB_CATMULL_CLARK) {
                 VSegs g = make_segs(m, l);
                 LevelDev gp{};

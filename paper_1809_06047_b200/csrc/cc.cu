@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
         const P3 p0 = ld3(P, v[0]), p1 = ld3(P, v[1]), p2 = ld3(P, v[2]), p3 = ld3(P, v[3]);
         const P3 fc = 0.25f * (p0 + p1 + p2 + p3);
         if (valid) st3(Pn, V + r, fc);
+        if (valid && fr.c0) st3(fr.c0w(f), r, p1 + fc);
         if (fpv) {
             // (1) the edge point of parent slot r (born at this level) sits at corner 1 of child
             // r and corner 3 of child r+1 (mod 4): its half ring sum from this parent face is
@@ -414,12 +415,73 @@ ALSUB_D void copy_point(const Frames &fr, int32_t v) {
 }
 
 // one vertex of a non-half-sum segment (see k_cc_vertex)
+// vertex born before this level: every incident level-l face q has it at corner 0, and the face
+// kernel left c0[q] = p(corner 1) + f_q, so S = (1 - 2/n) p + 1/n^2 sum_q c0[q]
+template <int N>
+ALSUB_D void smooth_c0(const Frames &fr, int32_t v, const int32_t (&q)[N]) {
+    constexpr float inv = 1.0f / (float)N;
+    for (int f = 0; f < fr.nb; ++f) {
+        const PR c0 = fr.c0r(f);
+        P3 acc = ld3c(c0, q[0]);
+#pragma unroll
+        for (int k = 1; k < N; ++k) acc = acc + ld3c(c0, q[k]);
+        st3(fr.wr(f), v, (1.0f - 2.0f * inv) * ld3(fr.rd(f), v) + (inv * inv) * acc);
+    }
+}
+
 template <int ORDER>
 ALSUB_D void cc_vertex_one(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs &g, int s, int32_t j) {
     const int32_t v = g.start[s] + j;
     const int shift = 2 * (g.level - g.birth[s]);
     const int type = g.type[s];
     const int m1 = g.birth[s] - 1;
+    if (fr.c0 && shift >= 2) {
+        // faces = slots >> 2 = birth slots << (shift - 2)
+        const int fs = shift - 2;
+        if (type == 2) {
+            const int2 hh = __ldg(g.ehh[m1] + j);
+            if (hh.y < 0) { copy_point(fr, v); return; }
+            int32_t nh, nt;
+            if (m1 == 0) {
+                const Topo<0> t0{g.face_off0, g.slot_face0};
+                nh = t0.next(hh.x);
+                nt = t0.next(hh.y);
+            } else {
+                nh = (hh.x & ~3) | ((hh.x + 1) & 3);
+                nt = (hh.y & ~3) | ((hh.y + 1) & 3);
+            }
+            const int32_t q[4] = {(4 * hh.x + 1) << fs, (4 * nh + 3) << fs, (4 * hh.y + 1) << fs, (4 * nt + 3) << fs};
+            smooth_c0<4>(fr, v, q);
+        } else if (type == 1 && m1 > 0) {
+            const int32_t q[4] = {(16 * j + 2) << fs, (16 * j + 6) << fs, (16 * j + 10) << fs, (16 * j + 14) << fs};
+            smooth_c0<4>(fr, v, q);
+        } else {
+            // level-0 vertex (its level-0 row) or face point of a level-0 face of any order
+            int32_t o, cnt;
+            const bool lv0 = type == 0;
+            if (lv0) {
+                if (__ldg(g.vbnd0 + j)) { copy_point(fr, v); return; }
+                o = __ldg(g.vtx_off0 + j);
+                cnt = __ldg(g.vtx_off0 + j + 1) - o;
+            } else {
+                o = __ldg(g.face_off0 + j);
+                cnt = __ldg(g.face_off0 + j + 1) - o;
+            }
+            for (int f = 0; f < fr.nb; ++f) {
+                const PR c0 = fr.c0r(f);
+                P3 acc = p3zero();
+                for (int32_t k = 0; k < cnt; ++k) {
+                    const int32_t b = lv0 ? __ldg(g.vtx_list0 + o + k) : 4 * (o + k) + 2;
+                    acc = acc + ld3c(c0, b << fs);
+                }
+                const P3 pv = ld3(fr.rd(f), v);
+                if (cnt == 0) { st3(fr.wr(f), v, pv); continue; }
+                const float inv = 1.0f / (float)cnt;
+                st3(fr.wr(f), v, (1.0f - 2.0f * inv) * pv + (inv * inv) * acc);
+            }
+        }
+        return;
+    }
     if (type == 2) {  // edge point born at level m1 + 1
         const int2 hh = __ldg(g.ehh[m1] + j);
         if (hh.y < 0) { copy_point(fr, v); return; }  // boundary: crease module

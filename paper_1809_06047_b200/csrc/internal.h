@@ -172,11 +172,17 @@ struct Frames {
     // (= per face of this level), written by the face kernel, read by the vertex kernel
     float *hs = nullptr;
     int64_t hsstride = 0;
+    // CC levels >= 1: per-face contribution to its corner-0 vertex, c0[q] = p(corner 1) + f_q,
+    // written by the face kernel; every vertex born before this level sums its faces' c0
+    float *c0 = nullptr;
+    int64_t c0stride = 0;
     // per-frame views ([V][3], vertex stride 3)
     ALSUB_HD PR rd(int f) const { return PR{P + f * Pstride, 3}; }
     ALSUB_HD PW wr(int f) const { return PW{Pn + f * Pnstride, 3}; }
     ALSUB_HD PW hsw(int f) const { return PW{hs + f * hsstride, 3}; }
     ALSUB_HD PR hsr(int f) const { return PR{hs + f * hsstride, 3}; }
+    ALSUB_HD PW c0w(int f) const { return PW{c0 + f * c0stride, 3}; }
+    ALSUB_HD PR c0r(int f) const { return PR{c0 + f * c0stride, 3}; }
 };
 
 // Vertex-id segments of a CC level: level-l vertex ids are
