@@ -302,6 +302,7 @@ extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t
     m->K0 = sc[2];
     m->NSV0 = sc[3];
     m->user_creases = (m->K0 - m->B0) > 0;
+    b.no_special = m->K0 == 0 && m->B0 == 0;
     CU(cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&m->side_stream, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));

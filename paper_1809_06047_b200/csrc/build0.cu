@@ -424,6 +424,7 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
         cudaMemsetAsync(b.sv_cnt, 0, sizeof(int32_t) * b.V, s);
         cudaMemsetAsync(b.sv_cur, 0, sizeof(int32_t) * b.V, s);
     }
+    if (b.zeroed && b.no_special) return;  // closed and crease-free: no special lists, no boundary words
     const int64_t nf = std::max<int64_t>(std::max<int64_t>(E, 32 * (int64_t)b.K_in), nw);
     launch(L, "b0_flags", k_b0_flags, dim3(grid_for(nf)), dim3(kThreads), 0, s, b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
                                                  b.face_edge, b.edge_hh, tp, b.V, E, b.bnd_word, nw, b.edge_sigma,

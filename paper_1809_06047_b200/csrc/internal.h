@@ -128,6 +128,7 @@ struct Build0 {
     int32_t E;                    // host-known after the count pass (create) or plan (refine)
     void *scratch;
     bool zeroed = false;          // refine: every work array and scan region pre-initialised by k_zero
+    bool no_special = false;      // refine of a closed, crease-free mesh: skip boundary/crease tables
 };
 size_t build0_scratch_bytes(int32_t V, int32_t S);
 // refine: add the level-0 work arrays / scan regions to z (one k_zero launch instead of memsets)
