@@ -59,6 +59,8 @@ struct LevelHost {
     SpEdge *sp = nullptr;       // special edges of this level [nsp]
     int64_t nsp = 0;            // = 2^l K_0
     int32_t *sv_list = nullptr; // [2 nsp] incident special edges of the special vertices
+    uint32_t *spw = nullptr;    // CC fused crease: special-edge bitmask of this level
+    int32_t *spwpre = nullptr;
     int64_t nsv = 0;            // special vertices of this level (prefix of the shared table)
     float *pos = nullptr;
 };
@@ -143,6 +145,7 @@ static LevelDev dev_of(const LevelHost &L) {
     p.face_vtx = L.face_vtx; p.face_edge = L.face_edge; p.face_twin = L.face_twin; p.edge_hh = L.edge_hh;
     p.vtx_slot0 = L.vtx_slot0; p.bnd_word = L.bnd_word; p.bnd_wpre = L.bnd_wpre; p.loop_base = L.loop_base;
     p.sp = L.sp; p.nsp = (int32_t)L.nsp; p.sv_list = L.sv_list; p.nsv = (int32_t)L.nsv;
+    p.spw = L.spw; p.spwpre = L.spwpre;
     return p;
 }
 
@@ -151,7 +154,7 @@ static ChildDev child_of(const LevelHost &L) {
     c.V = (int32_t)L.V; c.F = (int32_t)L.F; c.S = (int32_t)L.S; c.E = (int32_t)L.E;
     c.face_vtx = L.face_vtx; c.face_edge = L.face_edge; c.face_twin = L.face_twin; c.edge_hh = L.edge_hh;
     c.vtx_slot0 = L.vtx_slot0; c.bnd_word = L.bnd_word; c.bnd_wpre = L.bnd_wpre;
-    c.sp = L.sp; c.sv_list = L.sv_list;
+    c.sp = L.sp; c.sv_list = L.sv_list; c.spw = L.spw; c.spwpre = L.spwpre;
     return c;
 }
 
@@ -164,6 +167,7 @@ static void set_level0_view(alsub_mesh *m, LevelHost &L) {
     L.edge_hh = b.edge_hh; L.vtx_slot0 = b.vtx_slot0;
     L.bnd_word = b.bnd_word; L.bnd_wpre = b.bnd_wpre;
     L.sp = b.sp; L.nsp = m->K0; L.sv_list = b.sv_list; L.nsv = m->NSV0;
+    L.spw = b.spw; L.spwpre = b.spwpre;
     L.pos = m->pos0;
 }
 
@@ -288,6 +292,8 @@ extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t
     b.sv_cnt = A<int32_t>(m, num_verts, s, ML, ok);
     b.sv_cur = A<int32_t>(m, num_verts, s, ML, ok);
     b.sv_list = A<int32_t>(m, 2 * (int64_t)E0, s, ML, ok);
+    b.spw = A<uint32_t>(m, nw, s, ML, ok);
+    b.spwpre = A<int32_t>(m, nw, s, ML, ok);
     m->sv_vtx = m->sv_vtx_create = b.sv_vtx;
     m->sv_off = m->sv_off_create = b.sv_off;
     if (!ok) return bail(fail(ALSUB_E_NOMEM, "device allocation failed"));
@@ -414,6 +420,10 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
             if (special) {
                 c.sp = A<SpEdge>(m, c.nsp, s, ML, ok);
                 c.sv_list = A<int32_t>(m, 2 * c.nsp, s, ML, ok);
+                if (scheme == ALSUB_CATMULL_CLARK && has_child) {
+                    c.spw = A<uint32_t>(m, ceil_div(c.E, 32), s, ML, ok);
+                    c.spwpre = A<int32_t>(m, ceil_div(c.E, 32), s, ML, ok);
+                }
             }
         }
         if (scheme == ALSUB_LOOP && has_child && (adj || special)) {
@@ -442,6 +452,7 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
 }
 
 // ---------------- the level loop ----------------
+constexpr int64_t kFuseCreaseMaxV = 1 << 20;  // levels below this fuse the crease module
 // vertex-id segments of sqrt3 level l: [V0 | F0 | F1 | ... | F_{l-1}]
 static VSegs make_segs_s3(alsub_mesh *m, int l) {
     VSegs g{};
@@ -478,6 +489,9 @@ static VSegs make_segs(alsub_mesh *m, int l) {
         g.birth[n] = (int8_t)k; ++n;
         g.start[n] = (int32_t)(q.V + q.F); g.len[n] = (int32_t)q.E; g.type[n] = 2; g.birth[n] = (int8_t)k; ++n;
         g.ehh[k - 1] = q.edge_hh;
+        g.spw[k - 1] = q.spw;
+        g.spwpre[k - 1] = q.spwpre;
+        g.nsvb[k - 1] = (int32_t)q.nsv;
     }
     g.nseg = n;
     g.hs_seg = l >= 2 ? n - 1 : -1;  // the last segment = edge points born at level l
@@ -496,8 +510,10 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     {
         ZeroSegs z;
         build0_zero_segments(m->b0, z);
-        for (int l = 1; l < levels; ++l)  // child boundary words (atomicOr targets of the edge kernels)
+        for (int l = 1; l < levels; ++l) {  // child boundary / special words (atomicOr targets of the edge kernels)
             if (m->lv[l].bnd_word) z.add(m->lv[l].bnd_word, ceil_div(m->lv[l].E > 0 ? m->lv[l].E : 1, 32));
+            if (m->lv[l].spw) z.add(m->lv[l].spw, ceil_div(m->lv[l].E > 0 ? m->lv[l].E : 1, 32));
+        }
         zero_segments(z, s, L);
     }
     build0_validate(m->b0, s, L);
@@ -512,6 +528,7 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
         LevelDev p = dev_of(P);
         p.sv_vtx = m->sv_vtx;
         p.sv_off = m->sv_off;
+        p.inherit = 1;
         ChildDev c = child_of(C);
         c.sv_vtx = m->sv_vtx;
         c.sv_off = m->sv_off;
@@ -521,8 +538,11 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
             LevelDev gp{};
             const bool use_gp = l >= 2 && P.edge_hh == nullptr;
             if (use_gp) gp = dev_of(m->lv[l - 1]);
+            // crease module fused into the level kernels on small levels (the latency of a separate
+            // pass dominates there), a separate kernel on large ones (fusion costs occupancy)
+            p.crease = (special && !use_gp && P.V < kFuseCreaseMaxV) ? 1 : 0;
             cc_level(p, c, fr, true, adj, g, use_gp ? &gp : nullptr, s, L);
-            if (special) crease_level(p, c, fr, (int32_t)(P.V + P.F), 0, true, s, L);
+            if (special && !p.crease) crease_level(p, c, fr, (int32_t)(P.V + P.F), 0, true, s, L);
         } else if (scheme == ALSUB_LOOP) {
             if (adj || special) loop_edge_base(p, P.loop_cnt, P.loop_base, m->scratch, s, L);
             loop_level(p, c, fr, true, adj, m->scratch, s, L);
@@ -810,6 +830,7 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
             LevelDev p = dev_of(Pl);
             p.sv_vtx = m->sv_vtx;
             p.sv_off = m->sv_off;
+            p.inherit = 0;
             ChildDev c{};
             // frame-major [n][V][3] at every level (a frame-interleaved [V][n][3] layout was measured
             // slower: its per-frame stores are strided)
@@ -820,8 +841,9 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
                 LevelDev gp{};
                 const bool use_gp = l >= 2 && Pl.edge_hh == nullptr;
                 if (use_gp) gp = dev_of(m->lv[l - 1]);
+                p.crease = (special && !use_gp && Pl.V < kFuseCreaseMaxV) ? 1 : 0;
                 cc_level(p, c, fr, false, false, g, use_gp ? &gp : nullptr, s, L);
-                if (special) crease_level(p, c, fr, (int32_t)(Pl.V + Pl.F), 0, false, s, L);
+                if (special && !p.crease) crease_level(p, c, fr, (int32_t)(Pl.V + Pl.F), 0, false, s, L);
             } else if (scheme == ALSUB_LOOP) {
                 loop_level(p, c, fr, false, false, m->scratch, s, L);
                 if (special) crease_level(p, c, fr, (int32_t)Pl.V, 1, false, s, L);

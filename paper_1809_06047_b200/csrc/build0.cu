@@ -282,10 +282,18 @@ __global__ void __launch_bounds__(kThreads) k_b0_special(const int2 *__restrict_
                                                        const float *__restrict__ edge_sigma,
                                                        const int32_t *__restrict__ flag, const int32_t *__restrict__ off,
                                                        T0 tp, int32_t E, SpEdge *__restrict__ sp,
-                                                       int32_t *__restrict__ sv_cnt) {
+                                                       int32_t *__restrict__ sv_cnt, uint32_t *__restrict__ spw,
+                                                       int32_t *__restrict__ spwpre) {
     ALSUB_GRID_WAIT();
     const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= E || !flag[e]) return;
+    // the special-edge bitmask word of these 32 edges (one warp = one word) and its prefix
+    const int fl = e < E ? flag[e] : 0;
+    const unsigned word = __ballot_sync(0xffffffffu, fl != 0);
+    if ((threadIdx.x & 31) == 0 && e < E) {
+        spw[e >> 5] = word;
+        spwpre[e >> 5] = off[e];
+    }
+    if (e >= E || !fl) return;
     const int2 hh = edge_hh[e];
     const int32_t va = face_vtx[hh.x], vb = face_vtx[tp.next(hh.x)];
     const bool bnd = hh.y < 0;
@@ -433,7 +441,7 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, region(b, 4), s, L, b.zeroed);
     if (E > 0) {
         launch(L, "b0_special", k_b0_special, dim3(grid_for(E)), dim3(kThreads), 0, s, b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp, E,
-                                                      b.sp, b.sv_cnt);
+                                                      b.sp, b.sv_cnt, b.spw, b.spwpre);
     }
     scan_exclusive(b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V, region(b, 5), s, L, b.zeroed);
     if (E > 0) {

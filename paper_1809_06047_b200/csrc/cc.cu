@@ -14,6 +14,7 @@
 // Boundary vertices and creases are overwritten afterwards by crease.cu (boundary = inf crease).
 #include <algorithm>
 
+#include "crease_fused.cuh"
 #include "internal.h"
 
 namespace alsub {
@@ -204,23 +205,29 @@ ALSUB_D void edge_ends(const LevelDev &p, const Topo<ORDER> &tp, int32_t h, int3
     }
 }
 
-template <int ORDER, bool ADJ, bool BND, int NBC, int IT>
+template <int ORDER, bool ADJ, bool BND, int NBC, int IT, bool CR>
 __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Frames fr, bool topo) {
     ALSUB_GRID_WAIT();
     const Topo<ORDER> tp{p.face_off, p.slot_face};
     const int32_t e0 = blockIdx.x * (kThreads * IT) + threadIdx.x;
     const int32_t V = p.V, F = p.F;
     const int nb = NBC ? NBC : fr.nb;
-    int32_t hv[IT], tv[IT], va[IT], vb[IT], hn[IT];
+    int32_t hv[IT], tv[IT], va[IT], vb[IT], hn[IT], jl[IT];
+    float sg[IT];
 #pragma unroll
     for (int k = 0; k < IT; ++k) {
         const int32_t e = e0 + k * kThreads;
         const int2 hh = e < p.E ? __ldg(p.edge_hh + e) : make_int2(0, -1);
         hv[k] = hh.x;
         tv[k] = hh.y;
+        // fused crease module: list index of the edge (boundary / creased edges are ~1% of a level)
+        jl[k] = (CR && e < p.E) ? sp_index(p.spw, p.spwpre, e) : -1;
     }
 #pragma unroll
-    for (int k = 0; k < IT; ++k) edge_ends<ORDER>(p, tp, hv[k], va[k], vb[k], hn[k]);
+    for (int k = 0; k < IT; ++k) {
+        edge_ends<ORDER>(p, tp, hv[k], va[k], vb[k], hn[k]);
+        sg[k] = jl[k] >= 0 ? p.sp[jl[k]].sigma : 0.0f;
+    }
     for (int f = 0; f < nb; ++f) {
         const PR P = fr.rd(f);
         const PW Pn = fr.wr(f);
@@ -234,19 +241,22 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
         for (int k = 0; k < IT; ++k) {
             const int32_t e = e0 + k * kThreads;
             if (e >= p.E) continue;
-            st3(Pn, (int64_t)V + F + e, tv[k] < 0 ? 0.5f * ab[k] : 0.25f * (ab[k] + fs[k]));
+            P3 out = tv[k] < 0 ? 0.5f * ab[k] : 0.25f * (ab[k] + fs[k]);
+            if (jl[k] >= 0) out = crease_edge_point(sg[k], out, 0.5f * ab[k]);
+            st3(Pn, (int64_t)V + F + e, out);
         }
     }
-    if constexpr (ADJ) {
-        if (!topo) return;
+    if (!topo) return;
 #pragma unroll
-        for (int k = 0; k < IT; ++k) {
-            const int32_t e = e0 + k * kThreads;
-            if (e >= p.E) continue;
-            const int32_t h = hv[k], tw = tv[k];
-            // structured child edge ids: block [base, base + 4 - bnd) = (lo,ep), (hi,ep), (fp_min,ep), (fp_max,ep)
-            const int32_t bp = BND ? bprefix(p.bnd_word, p.bnd_wpre, e) : 0;
-            const int32_t base = 4 * e - bp;
+    for (int k = 0; k < IT; ++k) {
+        const int32_t e = e0 + k * kThreads;
+        if (e >= p.E) continue;
+        const int32_t h = hv[k], tw = tv[k];
+        // structured child edge ids: block [base, base + 4 - bnd) = (lo,ep), (hi,ep), (fp_min,ep), (fp_max,ep)
+        const int32_t bp = (ADJ ? BND : p.B > 0) ? bprefix(p.bnd_word, p.bnd_wpre, e) : 0;
+        const int32_t base = 4 * e - bp;
+        if (CR && p.inherit && jl[k] >= 0) fused_inherit(p, c, jl[k], p.sp[jl[k]], base, V + F + e);
+        if constexpr (ADJ) {
             const bool fwd = va[k] < vb[k];
             const int32_t h_ab = fwd ? h : tw, h_ba = fwd ? tw : h;
             // child half-edges: (lo,ep): lo->ep = 4 h_ab, ep->lo = 4 next(h_ba) + 3; (hi,ep) symmetric
@@ -263,10 +273,10 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
                 c.edge_hh[base + 2] = pair(4 * h + 1, 4 * hn[k] + 2);  // (fp of face(h), ep); h < tw
                 if (tw >= 0) c.edge_hh[base + 3] = pair(4 * tw + 1, 4 * tp.next(tw) + 2);
             }
+            const int32_t nch = tw < 0 ? 3 : 4;
             if constexpr (BND) {
                 // child boundary bits and, in closed form, the child per-word prefix:
                 // bprefix'(base + k) = 2 bprefix(e) + bnd_e min(k, 2)
-                const int32_t nch = tw < 0 ? 3 : 4;
                 if (tw < 0) {
                     atomicOr(c.bnd_word + (base >> 5), 1u << (base & 31));
                     atomicOr(c.bnd_word + ((base + 1) >> 5), 1u << ((base + 1) & 31));
@@ -277,6 +287,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
                     c.bnd_wpre[w] = 2 * bp + (tw < 0 ? min(kk, 2) : 0);
                 }
             }
+            if (CR && c.spw) fused_child_words(c, base, nch, sp_prefix(p.spw, p.spwpre, e), jl[k] >= 0);
         }
     }
 }
@@ -288,7 +299,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
 // index = level-(l-1) slot).  Five position gathers and four face points serve all four edge
 // points, and the level-l edge pairs never need to be stored.
 template <int NBC>
-__global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp, Frames fr) {
+__global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp, ChildDev c, Frames fr) {
     ALSUB_GRID_WAIT();
     // the block's children are the contiguous id range [base(e_first), base(e_last) + nch): staged
     // in shared memory and written back as one coalesced float run
@@ -339,6 +350,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
                 q[1] = 0.25f * (phi + pep + fb);
                 q[3] = 0.25f * (pS + pep + ft + fnt);
             }
+
             for (int k = 0; k < nch; ++k) {
                 s_out[3 * (o + k) + 0] = q[k].x;
                 s_out[3 * (o + k) + 1] = q[k].y;
@@ -372,9 +384,15 @@ struct VtxCtx {
     int32_t V;
 };
 
-// accumulate the smooth point of v over nx slots for every frame
+// store the vertex point of v: the smooth value, overridden by the boundary/crease rule when v is
+// a special vertex (fused crease module)
+ALSUB_D void emit_vertex(const Frames &fr, int f, int32_t v, const VCr &cr, P3 smooth) {
+    st3(fr.wr(f), v, cr.k >= 2 ? crease_vertex_point(cr, fr.rd(f), v, smooth) : smooth);
+}
+
+// accumulate the smooth point of v over N slots for every frame
 template <int ORDER, int N>
-ALSUB_D void smooth_fixed(const VtxCtx<ORDER> &x, const Frames &fr, int32_t v, const int32_t (&sl)[N]) {
+ALSUB_D void smooth_fixed(const VtxCtx<ORDER> &x, const Frames &fr, int32_t v, const int32_t (&sl)[N], const VCr &cr) {
     int32_t nb[N], fc[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -388,13 +406,13 @@ ALSUB_D void smooth_fixed(const VtxCtx<ORDER> &x, const Frames &fr, int32_t v, c
         P3 acc = ld3(P, nb[0]) + ld3c(Pn, fc[0]);
 #pragma unroll
         for (int k = 1; k < N; ++k) acc = acc + ld3(P, nb[k]) + ld3c(Pn, fc[k]);
-        st3(Pn, v, (1.0f - 2.0f * inv) * ld3(P, v) + (inv * inv) * acc);
+        emit_vertex(fr, f, v, cr, (1.0f - 2.0f * inv) * ld3(P, v) + (inv * inv) * acc);
     }
 }
 
 template <int ORDER>
 ALSUB_D void smooth_list(const VtxCtx<ORDER> &x, const Frames &fr, int32_t v, const int32_t *list, int32_t n,
-                         int shift, bool quad_fp, int32_t off) {
+                         int shift, bool quad_fp, int32_t off, const VCr &cr) {
     for (int f = 0; f < fr.nb; ++f) {
         const PR P = fr.rd(f);
         const PW Pn = fr.wr(f);
@@ -406,31 +424,80 @@ ALSUB_D void smooth_list(const VtxCtx<ORDER> &x, const Frames &fr, int32_t v, co
         const P3 pv = ld3(P, v);
         if (n == 0) { st3(Pn, v, pv); continue; }
         const float inv = 1.0f / (float)n;
-        st3(Pn, v, (1.0f - 2.0f * inv) * pv + (inv * inv) * acc);
+        emit_vertex(fr, f, v, cr, (1.0f - 2.0f * inv) * pv + (inv * inv) * acc);
     }
 }
 
-ALSUB_D void copy_point(const Frames &fr, int32_t v) {
-    for (int f = 0; f < fr.nb; ++f) st3(fr.wr(f), v, ld3(fr.rd(f), v));
+ALSUB_D void copy_point(const Frames &fr, int32_t v, const VCr &cr) {
+    for (int f = 0; f < fr.nb; ++f) emit_vertex(fr, f, v, cr, ld3(fr.rd(f), v));
 }
 
-// one vertex of a non-half-sum segment (see k_cc_vertex)
 // vertex born before this level: every incident level-l face q has it at corner 0, and the face
 // kernel left c0[q] = p(corner 1) + f_q, so S = (1 - 2/n) p + 1/n^2 sum_q c0[q]
 template <int N>
-ALSUB_D void smooth_c0(const Frames &fr, int32_t v, const int32_t (&q)[N]) {
+ALSUB_D void smooth_c0(const Frames &fr, int32_t v, const int32_t (&q)[N], const VCr &cr) {
     constexpr float inv = 1.0f / (float)N;
     for (int f = 0; f < fr.nb; ++f) {
         const PR c0 = fr.c0r(f);
         P3 acc = ld3c(c0, q[0]);
 #pragma unroll
         for (int k = 1; k < N; ++k) acc = acc + ld3c(c0, q[k]);
-        st3(fr.wr(f), v, (1.0f - 2.0f * inv) * ld3(fr.rd(f), v) + (inv * inv) * acc);
+        emit_vertex(fr, f, v, cr, (1.0f - 2.0f * inv) * ld3(fr.rd(f), v) + (inv * inv) * acc);
     }
 }
 
+// special-vertex index of vertex j of segment s (-1 if it cannot be special): level-0 vertices are
+// the identity table; an edge point born at m is special iff its level-(m-1) edge is listed
+ALSUB_D int32_t sv_index(const VSegs &g, int s, int32_t j) {
+    const int type = g.type[s];
+    if (type == 0) return j;
+    if (type == 1) return -1;
+    const int m1 = g.birth[s] - 1;
+    const int32_t idx = sp_index(g.spw[m1], g.spwpre[m1], j);
+    return idx >= 0 ? g.nsvb[m1] + idx : -1;
+}
+
 template <int ORDER>
-ALSUB_D void cc_vertex_one(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs &g, int s, int32_t j) {
+ALSUB_D void cc_vertex_smooth(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs &g, int s, int32_t j, const VCr &cr);
+
+// special (boundary / crease) vertex: the rule of crease_vertex_point, the smooth point only when
+// it is blended in
+template <int ORDER>
+ALSUB_D void cc_vertex_special(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs &g,
+                                               const LevelDev &p, int32_t *csv_list, int s, int32_t j, int32_t i) {
+    const int32_t v = g.start[s] + j;
+    const VCr cr = vertex_crease(p, p.inherit ? csv_list : nullptr, i, v);
+    if (cr.k >= 2 && cr.s >= 1.0f) {  // sharp: no smooth point needed
+        for (int f = 0; f < fr.nb; ++f) st3(fr.wr(f), v, crease_vertex_point(cr, fr.rd(f), v, p3zero()));
+        return;
+    }
+    if (s == g.hs_seg) {
+        const int2 hh = __ldg(g.ehh[g.birth[s] - 1] + j);
+        for (int f = 0; f < fr.nb; ++f) {
+            const PR hs = fr.hsr(f);
+            const P3 acc = ld3c(hs, hh.x) + ld3c(hs, hh.y);
+            emit_vertex(fr, f, v, cr, 0.5f * ld3(fr.rd(f), v) + 0.0625f * acc);
+        }
+        return;
+    }
+    cc_vertex_smooth<ORDER>(x, fr, g, s, j, cr);
+}
+
+template <int ORDER, bool CR>
+ALSUB_D void cc_vertex_one(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs &g, const LevelDev &p,
+                           int32_t *csv_list, int s, int32_t j) {
+    if constexpr (CR) {
+        const int32_t i = sv_index(g, s, j);
+        if (i >= 0 && p.sv_off[i + 1] > p.sv_off[i]) {
+            cc_vertex_special<ORDER>(x, fr, g, p, csv_list, s, j, i);
+            return;
+        }
+    }
+    cc_vertex_smooth<ORDER>(x, fr, g, s, j, VCr{0, 0.0f, -1, -1});
+}
+
+template <int ORDER>
+ALSUB_D void cc_vertex_smooth(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs &g, int s, int32_t j, const VCr &cr) {
     const int32_t v = g.start[s] + j;
     const int shift = 2 * (g.level - g.birth[s]);
     const int type = g.type[s];
@@ -440,7 +507,7 @@ ALSUB_D void cc_vertex_one(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs
         const int fs = shift - 2;
         if (type == 2) {
             const int2 hh = __ldg(g.ehh[m1] + j);
-            if (hh.y < 0) { copy_point(fr, v); return; }
+            if (hh.y < 0) { copy_point(fr, v, cr); return; }
             int32_t nh, nt;
             if (m1 == 0) {
                 const Topo<0> t0{g.face_off0, g.slot_face0};
@@ -451,16 +518,16 @@ ALSUB_D void cc_vertex_one(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs
                 nt = (hh.y & ~3) | ((hh.y + 1) & 3);
             }
             const int32_t q[4] = {(4 * hh.x + 1) << fs, (4 * nh + 3) << fs, (4 * hh.y + 1) << fs, (4 * nt + 3) << fs};
-            smooth_c0<4>(fr, v, q);
+            smooth_c0<4>(fr, v, q, cr);
         } else if (type == 1 && m1 > 0) {
             const int32_t q[4] = {(16 * j + 2) << fs, (16 * j + 6) << fs, (16 * j + 10) << fs, (16 * j + 14) << fs};
-            smooth_c0<4>(fr, v, q);
+            smooth_c0<4>(fr, v, q, cr);
         } else {
             // level-0 vertex (its level-0 row) or face point of a level-0 face of any order
             int32_t o, cnt;
             const bool lv0 = type == 0;
             if (lv0) {
-                if (__ldg(g.vbnd0 + j)) { copy_point(fr, v); return; }
+                if (__ldg(g.vbnd0 + j)) { copy_point(fr, v, cr); return; }
                 o = __ldg(g.vtx_off0 + j);
                 cnt = __ldg(g.vtx_off0 + j + 1) - o;
             } else {
@@ -477,14 +544,14 @@ ALSUB_D void cc_vertex_one(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs
                 const P3 pv = ld3(fr.rd(f), v);
                 if (cnt == 0) { st3(fr.wr(f), v, pv); continue; }
                 const float inv = 1.0f / (float)cnt;
-                st3(fr.wr(f), v, (1.0f - 2.0f * inv) * pv + (inv * inv) * acc);
+                emit_vertex(fr, f, v, cr, (1.0f - 2.0f * inv) * pv + (inv * inv) * acc);
             }
         }
         return;
     }
     if (type == 2) {  // edge point born at level m1 + 1
         const int2 hh = __ldg(g.ehh[m1] + j);
-        if (hh.y < 0) { copy_point(fr, v); return; }  // boundary: crease module
+        if (hh.y < 0) { copy_point(fr, v, cr); return; }  // boundary (special, handled above)
         int32_t nh, nt;
         if (m1 == 0) {
             const Topo<0> t0{g.face_off0, g.slot_face0};
@@ -496,23 +563,23 @@ ALSUB_D void cc_vertex_one(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs
         }
         const int32_t sl[4] = {(4 * hh.x + 1) << shift, (4 * nh + 3) << shift, (4 * hh.y + 1) << shift,
                                (4 * nt + 3) << shift};
-        smooth_fixed<ORDER, 4>(x, fr, v, sl);
+        smooth_fixed<ORDER, 4>(x, fr, v, sl, cr);
     } else if (type == 1 && m1 > 0) {  // face point of a quad
         const int32_t sl[4] = {(16 * j + 2) << shift, (16 * j + 6) << shift, (16 * j + 10) << shift,
                                (16 * j + 14) << shift};
-        smooth_fixed<ORDER, 4>(x, fr, v, sl);
+        smooth_fixed<ORDER, 4>(x, fr, v, sl, cr);
     } else if (type == 1) {  // face point of a level-0 face (any order)
         const int32_t off = __ldg(g.face_off0 + j), cnt = __ldg(g.face_off0 + j + 1) - off;
-        smooth_list<ORDER>(x, fr, v, nullptr, cnt, shift, true, off);
+        smooth_list<ORDER>(x, fr, v, nullptr, cnt, shift, true, off, cr);
     } else {  // level-0 vertex
-        if (__ldg(g.vbnd0 + j)) { copy_point(fr, v); return; }
+        if (__ldg(g.vbnd0 + j)) { copy_point(fr, v, cr); return; }
         const int32_t o = __ldg(g.vtx_off0 + j), cnt = __ldg(g.vtx_off0 + j + 1) - o;
-        smooth_list<ORDER>(x, fr, v, g.vtx_list0 + o, cnt, shift, false, 0);
+        smooth_list<ORDER>(x, fr, v, g.vtx_list0 + o, cnt, shift, false, 0, cr);
     }
 }
 
-template <int ORDER, int PL>
-__global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, VSegs g) {
+template <int ORDER, int PL, bool CR>
+__global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, VSegs g, int32_t *csv_list) {
     ALSUB_GRID_WAIT();
     constexpr int kVtxTask = 32 * PL;  // vertices per warp task (PL per lane)
     // Work unit = a warp task of 32 PL consecutive vertices of ONE segment (no divergence between
@@ -546,38 +613,33 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
         const int32_t j0 = (s_lo[s] + (task - s_pre[s])) * kVtxTask + lane;
         const int32_t len = g.len[s];
         if (s == g.hs_seg) {
-            // edge points born at this level: two half sums from the face kernel; the four
-            // vertices of a lane are loaded together (edge pairs, then half sums)
-            int2 hh[PL];
-#pragma unroll
+            // edge points born at this level: two half sums from the face kernel
+            const int m1 = g.birth[s] - 1;
             for (int k = 0; k < PL; ++k) {
                 const int32_t j = j0 + 32 * k;
-                hh[k] = j < len ? __ldg(g.ehh[g.birth[s] - 1] + j) : make_int2(0, -1);
-            }
-            for (int f = 0; f < fr.nb; ++f) {
-                const PR hs = fr.hsr(f);
-                const PR P = fr.rd(f);
-                const PW Pn = fr.wr(f);
-                P3 acc[PL], pv[PL];
-#pragma unroll
-                for (int k = 0; k < PL; ++k) {
-                    const int32_t j = j0 + 32 * k;
-                    pv[k] = j < len ? ld3(P, g.start[s] + j) : p3zero();
-                    acc[k] = hh[k].y >= 0 ? ld3c(hs, hh[k].x) + ld3c(hs, hh[k].y) : p3zero();
+                if (j >= len) continue;
+                const int32_t v = g.start[s] + j;
+                if constexpr (CR) {
+                    const int32_t i = sv_index(g, s, j);
+                    if (i >= 0) {  // boundary / creased parent edge
+                        cc_vertex_special<ORDER>(x, fr, g, p, csv_list, s, j, i);
+                        continue;
+                    }
                 }
-#pragma unroll
-                for (int k = 0; k < PL; ++k) {
-                    const int32_t j = j0 + 32 * k;
-                    if (j >= len) continue;
-                    // boundary edge points keep p (set by the crease/boundary module)
-                    st3(Pn, g.start[s] + j, hh[k].y >= 0 ? 0.5f * pv[k] + 0.0625f * acc[k] : pv[k]);
+                const int2 hh = __ldg(g.ehh[m1] + j);
+                for (int f = 0; f < fr.nb; ++f) {
+                    // boundary edge points keep p (set by the separate crease/boundary pass)
+                    if (hh.y < 0) { st3(fr.wr(f), v, ld3(fr.rd(f), v)); continue; }
+                    const PR hs = fr.hsr(f);
+                    const P3 acc = ld3c(hs, hh.x) + ld3c(hs, hh.y);
+                    st3(fr.wr(f), v, 0.5f * ld3(fr.rd(f), v) + 0.0625f * acc);
                 }
             }
             continue;
         }
         for (int k = 0; k < PL; ++k) {
             const int32_t j = j0 + 32 * k;
-            if (j < len) cc_vertex_one<ORDER>(x, fr, g, s, j);
+            if (j < len) cc_vertex_one<ORDER, CR>(x, fr, g, p, csv_list, s, j);
         }
     }
 }
@@ -612,13 +674,20 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bo
         se = L.side;
     }
     if (gp && gp->E > 0) {
-        if (one) launch(L, "cc_edge", k_cc_edge_gp<1>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, fr);
-        else launch(L, "cc_edge", k_cc_edge_gp<0>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, fr);
+        if (one) launch(L, "cc_edge", k_cc_edge_gp<1>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, c, fr);
+        else launch(L, "cc_edge", k_cc_edge_gp<0>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, c, fr);
     } else if (p.E > 0) {
         constexpr int IT = 2;
         const unsigned gdim = grid_for(p.E, kThreads * IT);
-        if (one) launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 1, IT>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
-        else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
+        // p.crease: boundary/crease rules fused into the kernels (small levels, where a separate
+        // pass costs a full dependent-kernel latency); otherwise crease.cu runs after this level
+        if (p.crease) {
+            if (one) launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 1, IT, true>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
+            else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT, true>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
+        } else {
+            if (one) launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 1, IT, false>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
+            else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT, false>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
+        }
     }
     if (p.V > 0) {
         // 32-vertex warp tasks; >= 2 waves of 148 SMs for small levels, 4 tasks per warp for large
@@ -627,8 +696,8 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bo
         } else {
             const unsigned nblk = (unsigned)std::max<int64_t>(grid_for(p.V, 4 * kThreads),
                                                               std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
-            if constexpr (ORDER == 4) launch(L, "cc_vertex", k_cc_vertex<4, 1>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
-            else launch(L, "cc_vertex", k_cc_vertex<0, 1>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
+            if (p.crease) launch(L, "cc_vertex", k_cc_vertex<ORDER == 4 ? 4 : 0, 1, true>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g, c.sv_list);
+            else launch(L, "cc_vertex", k_cc_vertex<ORDER == 4 ? 4 : 0, 1, false>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g, c.sv_list);
         }
     }
     if (fork) {

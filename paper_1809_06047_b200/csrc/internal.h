@@ -123,6 +123,8 @@ struct Build0 {
     SpEdge *sp;                   // [cap] special edges
     int32_t *sv_vtx;              // [cap] special vertices
     int32_t *sv_cnt, *sv_off, *sv_cur, *sv_list;  // special-vertex CSR (level 0)
+    uint32_t *spw;                // [ceil(E/32)] special-edge bitmask (level 0)
+    int32_t *spwpre;              // [ceil(E/32)] its per-word prefix (= sp_off at the word start)
     int32_t *flags;               // device status flags
     int32_t *scalars;             // device scalars: [0] E, [1] B, [2] K special, [3] NSV
     int32_t E;                    // host-known after the count pass (create) or plan (refine)
@@ -152,6 +154,11 @@ struct LevelDev {
     int32_t nsp;
     const int32_t *sv_vtx, *sv_off, *sv_list;
     int32_t nsv;
+    // CC: edge e is special iff bit e of spw; its list index = spwpre[e/32] + popcount (fused crease)
+    const uint32_t *spw;
+    const int32_t *spwpre;
+    int32_t crease;   // 1 = apply boundary/crease rules inside the level kernels (CC)
+    int32_t inherit;  // 1 = also build the child special lists
 };
 struct ChildDev {
     int32_t V, F, S, E;  // child counts
@@ -161,6 +168,8 @@ struct ChildDev {
     int32_t *bnd_wpre;
     SpEdge *sp;
     int32_t *sv_vtx, *sv_off, *sv_list;
+    uint32_t *spw;
+    int32_t *spwpre;
 };
 
 // positions: P [nb][V][3] (frame stride Pstride floats), Pn [nb][V'][3]
@@ -204,6 +213,10 @@ struct VSegs {
     // sqrt3: slot multiplier 3^(l-m) per segment and the level m-1 face rows
     int32_t mult[kMaxSeg];
     const int32_t *fvx[kMaxLevels], *ftw[kMaxLevels];
+    // CC fused crease: special bitmask / prefix and special-vertex count of level m-1 per birth
+    const uint32_t *spw[kMaxLevels];
+    const int32_t *spwpre[kMaxLevels];
+    int32_t nsvb[kMaxLevels];
 };
 
 // mode: adj = emit child adjacency (not the last level); topo = emit child faces;
