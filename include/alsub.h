@@ -134,6 +134,28 @@ alsub_status alsub_level_positions(const alsub_mesh *mesh, int32_t level, float 
 alsub_status alsub_eval_frames(alsub_mesh *mesh, int32_t levels, const float *frames_in, int32_t num_frames,
                                float *frames_out, void *stream);
 
+/* Extra vertex channels (uv, colours, any per-vertex linear data):
+ * refine `channels` values per control vertex with the same stencils as the positions (same
+ * smooth / boundary / crease rules, reading R22) through the topology of the last alsub_refine.
+ *   attr_in [V0][channels] fp32, attr_out [V_levels][channels] fp32 (host or device pointers;
+ *   host output synchronises `stream`).  Channels are packed three at a time into frames of
+ *   alsub_eval_frames by a device kernel and unpacked the same way.
+ * Errors: E_ARG (channels < 0, null pointers, levels beyond the last refine), E_NOMEM, E_CUDA. */
+alsub_status alsub_eval_attributes(alsub_mesh *mesh, int32_t levels, const float *attr_in, int32_t channels,
+                                   float *attr_out, void *stream);
+
+/* Hierarchical edits / displacement ("we have access to the vertex data after each
+ * iteration and can arbitrarily modify it").  alsub_level_positions_ptr returns the handle-owned
+ * device array [V_level][3] fp32 of level `level` of the last refine (level 0 = the control
+ * positions); it stays valid until the next alsub_refine with a different level count or
+ * alsub_mesh_destroy.  The caller may write it (stream-ordered), then alsub_reevaluate
+ * recomputes the positions of levels from_level+1 .. levels from it over the stored topology
+ * (static mode; topology and crease sharpness unchanged).  A later alsub_refine recomputes
+ * everything from the level-0 positions.
+ * Errors: E_ARG (null pointers, level / from_level outside 0 .. levels of the last refine). */
+alsub_status alsub_level_positions_ptr(alsub_mesh *mesh, int32_t level, float **pos_dev);
+alsub_status alsub_reevaluate(alsub_mesh *mesh, int32_t from_level, void *stream);
+
 /* Number of kernel launches issued by the last alsub_refine / alsub_eval_frames call
  * (a graph replay counts the kernels inside it). */
 int64_t alsub_last_launch_count(const alsub_mesh *mesh);

@@ -358,3 +358,23 @@ CONFIGS = {
     4: dict(name="torus100k_sqrt3_L5", mesh=torus100k, scheme="sqrt3", levels=5),
     5: dict(name="armor50k_cc_L4_frames4096", mesh=armor50k, scheme="cc", levels=4, frames=4096),
 }
+
+
+def vertex_channels(mesh, channels, seed=SEED_FRAMES):
+    """Seeded per-vertex attribute data [V][channels] fp32 (uv-like: two affine functions of the
+    position plus noise, then noise channels) for the extra-channel path."""
+    rng = np.random.default_rng(seed)
+    p = np.asarray(mesh["pos"], np.float64)
+    V = p.shape[0]
+    out = rng.standard_normal((V, channels)) * 0.1
+    if channels >= 1:
+        out[:, 0] += 0.5 + 0.3 * p[:, 0] + 0.1 * p[:, 2]
+    if channels >= 2:
+        out[:, 1] += 0.5 + 0.3 * p[:, 1] - 0.1 * p[:, 2]
+    return out.astype(np.float32)
+
+
+def displacement(n, seed=SEED_FRAMES, scale=0.01):
+    """Seeded per-vertex displacement vectors [n][3] fp32 (hierarchical-edit tests)."""
+    rng = np.random.default_rng(seed + 1)
+    return (rng.standard_normal((n, 3)) * scale).astype(np.float32)

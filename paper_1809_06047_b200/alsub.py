@@ -66,6 +66,9 @@ def lib():
     L.alsub_level_topology.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp]
     L.alsub_level_positions.argtypes = [vp, i32, vp, vp]
     L.alsub_eval_frames.argtypes = [vp, i32, vp, i32, vp, vp]
+    L.alsub_eval_attributes.argtypes = [vp, i32, vp, i32, vp, vp]
+    L.alsub_level_positions_ptr.argtypes = [vp, i32, C.POINTER(vp)]
+    L.alsub_reevaluate.argtypes = [vp, i32, vp]
     L.alsub_last_launch_count.argtypes = [vp]
     L.alsub_last_launch_count.restype = i64
     L.alsub_mesh_destroy.argtypes = [vp]
@@ -73,7 +76,8 @@ def lib():
     L.alsub_last_error.restype = C.c_char_p
     L.alsub_version.restype = C.c_char_p
     for f in ("alsub_mesh_create", "alsub_set_positions", "alsub_refine", "alsub_refine_profile", "alsub_level_counts",
-              "alsub_level_topology", "alsub_level_positions", "alsub_eval_frames"):
+              "alsub_level_topology", "alsub_level_positions", "alsub_eval_frames", "alsub_eval_attributes",
+              "alsub_level_positions_ptr", "alsub_reevaluate"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -100,6 +104,16 @@ def _as(t, dtype):
         return t.to(dtype).contiguous()
     npdt = {torch.int32: np.int32, torch.float32: np.float32}[dtype]
     return np.ascontiguousarray(np.asarray(t), dtype=npdt)
+
+
+def _device_view(addr, shape):
+    """A float32 CUDA tensor aliasing handle-owned device memory (no copy, no ownership)."""
+    n = int(np.prod(shape))
+
+    class _Iface:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (int(addr), False), "version": 3}
+
+    return torch.as_tensor(_Iface(), device="cuda").view(*shape)
 
 
 def _stream(stream):
@@ -246,6 +260,30 @@ class Mesh:
             out = torch.empty((B, VL, 3), dtype=torch.float32, device="cuda")
         _check(self._lib.alsub_eval_frames(self._h, int(levels), _ptr(fr), B, _ptr(out), _stream(stream)))
         return out
+
+    def eval_attributes(self, attr, levels, out=None, stream=None):
+        """Extra vertex channels: attr [V0, C] -> [V_levels, C] with the position stencils."""
+        a = _as(attr, torch.float32)
+        Cn = int(a.shape[1]) if a.ndim == 2 else 1
+        VL = self.counts(levels)["verts"]
+        if out is None:
+            out = torch.empty((VL, Cn), dtype=torch.float32, device="cuda")
+        _check(self._lib.alsub_eval_attributes(self._h, int(levels), _ptr(a), Cn, _ptr(out), _stream(stream)))
+        return out
+
+    def level_positions_view(self, level):
+        """The handle-owned device positions of `level` as a writable [V, 3] tensor view
+        (hierarchical edits / displacement); follow writes with reevaluate()."""
+        p = C.c_void_p()
+        _check(self._lib.alsub_level_positions_ptr(self._h, int(level), C.byref(p)))
+        V = self.counts(level)["verts"]
+        if V == 0:
+            return torch.empty((0, 3), dtype=torch.float32, device="cuda")
+        return _device_view(p.value, (V, 3))
+
+    def reevaluate(self, from_level, stream=None):
+        """Recompute the positions of levels > from_level from the (edited) level from_level."""
+        _check(self._lib.alsub_reevaluate(self._h, int(from_level), _stream(stream)))
 
     @property
     def last_launch_count(self):

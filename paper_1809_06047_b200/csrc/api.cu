@@ -782,6 +782,95 @@ extern "C" alsub_status alsub_level_positions(const alsub_mesh *m, int32_t level
     return ALSUB_OK;
 }
 
+// ---------------- static mode ----------------
+// One level of static evaluation over the stored topology of level l (only the eval
+// half of every module runs): positions fr.P (level l) -> fr.Pn (level l + 1) for fr.nb frames.
+static void static_level(alsub_mesh *m, int l, const Frames &fr, cudaStream_t s, Launches &L) {
+    const int scheme = m->scheme;
+    const bool special = scheme != ALSUB_SQRT3 && m->K0 > 0;
+    const LevelHost &Pl = m->lv[l];
+    LevelDev p = dev_of(Pl);
+    p.sv_vtx = m->sv_vtx;
+    p.sv_off = m->sv_off;
+    p.inherit = 0;
+    ChildDev c{};
+    if (scheme == ALSUB_CATMULL_CLARK) {
+        VSegs g = make_segs(m, l);
+        LevelDev gp{};
+        const bool use_gp = l >= 2 && Pl.edge_hh == nullptr;
+        if (use_gp) gp = dev_of(m->lv[l - 1]);
+        p.crease = (special && !use_gp && Pl.V < kFuseCreaseMaxV) ? 1 : 0;
+        cc_level(p, c, fr, false, false, g, use_gp ? &gp : nullptr, s, L);
+        if (special && !p.crease) crease_level(p, c, fr, (int32_t)(Pl.V + Pl.F), 0, false, s, L);
+    } else if (scheme == ALSUB_LOOP) {
+        loop_level(p, c, fr, false, false, m->scratch, s, L);
+        if (special) crease_level(p, c, fr, (int32_t)Pl.V, 1, false, s, L);
+    } else {
+        VSegs g = make_segs_s3(m, l);
+        sqrt3_level(p, c, fr, false, false, g, s, L);
+    }
+}
+
+extern "C" alsub_status alsub_level_positions_ptr(alsub_mesh *m, int32_t level, float **pos_dev) {
+    if (!m || !pos_dev) return fail(ALSUB_E_ARG, "null argument");
+    if (level == 0) { *pos_dev = m->pos0; return ALSUB_OK; }
+    LevelHost *L = const_cast<LevelHost *>(level_of(m, level));
+    if (!L) return fail(ALSUB_E_ARG, "level out of range");
+    *pos_dev = L->pos;
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_reevaluate(alsub_mesh *m, int32_t from_level, void *stream) {
+    if (!m) return fail(ALSUB_E_ARG, "null argument");
+    if (m->levels < 0 || from_level < 0 || from_level > m->levels)
+        return fail(ALSUB_E_ARG, "from_level outside 0 .. levels of the last alsub_refine");
+    cudaStream_t s = (cudaStream_t)stream;
+    Launches L;
+    L.side = m->side_stream;
+    L.ev_fork = m->ev_fork;
+    L.ev_join = m->ev_join;
+    for (int l = from_level; l < m->levels; ++l) {
+        const float *P = l == 0 ? m->pos0 : m->lv[l].pos;
+        Frames fr{P, m->lv[l + 1].pos, 3 * m->lv[l].V, 3 * m->lv[l + 1].V, 1, m->hs, 0,
+                  (l >= 1 && m->scheme == ALSUB_CATMULL_CLARK) ? m->c0 : nullptr, 0};
+        static_level(m, l, fr, s, L);
+    }
+    m->last_launches = L.n;
+    CU(cudaGetLastError());
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_eval_attributes(alsub_mesh *m, int32_t levels, const float *attr_in, int32_t channels,
+                                              float *attr_out, void *stream) {
+    if (!m || channels < 0 || (channels > 0 && (!attr_in || !attr_out))) return fail(ALSUB_E_ARG, "bad argument");
+    if (m->levels < 0 || levels < 0 || levels > m->levels) return fail(ALSUB_E_ARG, "levels exceed the last alsub_refine");
+    if (channels == 0) return ALSUB_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t V0 = m->V0, VL = m->lv[levels].V;
+    const int32_t ng = (channels + 2) / 3;
+    std::vector<std::pair<void *, size_t>> tmp;
+    bool ok = true;
+    float *in_dev = const_cast<float *>(attr_in), *out_dev = attr_out;
+    if (!is_device_ptr(attr_in)) in_dev = A<float>(m, V0 * channels, s, tmp, ok);
+    if (!is_device_ptr(attr_out)) out_dev = A<float>(m, VL * channels, s, tmp, ok);
+    float *fin = A<float>(m, 3 * V0 * ng, s, tmp, ok), *fout = A<float>(m, 3 * VL * ng, s, tmp, ok);
+    if (!ok) { free_list(m, tmp, s); return fail(ALSUB_E_NOMEM, "attribute staging buffers"); }
+    if (in_dev != attr_in) CU(cudaMemcpyAsync(in_dev, attr_in, sizeof(float) * V0 * channels, cudaMemcpyHostToDevice, s));
+    Launches L;
+    pack_channels(in_dev, V0, channels, fin, s, L);
+    const alsub_status st = alsub_eval_frames(m, levels, fin, ng, fout, stream);
+    if (st != ALSUB_OK) { free_list(m, tmp, s); return st; }
+    unpack_channels(fout, VL, channels, out_dev, s, L);
+    if (out_dev != attr_out) {
+        CU(cudaMemcpyAsync(attr_out, out_dev, sizeof(float) * VL * channels, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+    }
+    m->last_launches += L.n;
+    free_list(m, tmp, s);
+    CU(cudaGetLastError());
+    return ALSUB_OK;
+}
+
 // ---------------- static mode: frames ----------------
 extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const float *frames_in, int32_t num_frames,
                                           float *frames_out, void *stream) {
@@ -825,32 +914,12 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
         float *Pout_final = out_dev ? frames_out + 3 * VL * (int64_t)f0 : m->frame_buf[levels];
         const float *P = Pin;
         for (int l = 0; l < levels; ++l) {
-            const LevelHost &Pl = m->lv[l];
             float *Pn = (l + 1 == levels) ? Pout_final : m->frame_buf[l + 1];
-            LevelDev p = dev_of(Pl);
-            p.sv_vtx = m->sv_vtx;
-            p.sv_off = m->sv_off;
-            p.inherit = 0;
-            ChildDev c{};
             // frame-major [n][V][3] at every level (a frame-interleaved [V][n][3] layout was measured
-            // slower: its per-frame stores are strided)
-            Frames fr{P, Pn, 3 * Pl.V, 3 * m->lv[l + 1].V, n, m->frame_hs, m->hs_elems,
+            // slower: its per-frame stores are strided, profiles/r01_frames_experiments.md)
+            Frames fr{P, Pn, 3 * m->lv[l].V, 3 * m->lv[l + 1].V, n, m->frame_hs, m->hs_elems,
                       (l >= 1 && scheme == ALSUB_CATMULL_CLARK) ? m->frame_c0 : nullptr, m->c0_elems};
-            if (scheme == ALSUB_CATMULL_CLARK) {
-                VSegs g = make_segs(m, l);
-                LevelDev gp{};
-                const bool use_gp = l >= 2 && Pl.edge_hh == nullptr;
-                if (use_gp) gp = dev_of(m->lv[l - 1]);
-                p.crease = (special && !use_gp && Pl.V < kFuseCreaseMaxV) ? 1 : 0;
-                cc_level(p, c, fr, false, false, g, use_gp ? &gp : nullptr, s, L);
-                if (special && !p.crease) crease_level(p, c, fr, (int32_t)(Pl.V + Pl.F), 0, false, s, L);
-            } else if (scheme == ALSUB_LOOP) {
-                loop_level(p, c, fr, false, false, m->scratch, s, L);
-                if (special) crease_level(p, c, fr, (int32_t)Pl.V, 1, false, s, L);
-            } else {
-                VSegs g = make_segs_s3(m, l);
-                sqrt3_level(p, c, fr, false, false, g, s, L);
-            }
+            static_level(m, l, fr, s, L);
             P = Pn;
         }
         if (!out_dev)

@@ -81,6 +81,9 @@ struct ZeroSegs {
     }
 };
 void zero_segments(const ZeroSegs &z, cudaStream_t s, Launches &L);
+// [V][C] vertex channels <-> ceil(C/3) frames of [V][3] (alsub_eval_attributes)
+void pack_channels(const float *in, int64_t V, int32_t C, float *out, cudaStream_t s, Launches &L);
+void unpack_channels(const float *in, int64_t V, int32_t C, float *out, cudaStream_t s, Launches &L);
 // LSD radix sort of (key, value) int32 pairs, keys in [0, 2^bits).  Stable.  Result in
 // keys/vals; keys_alt/vals_alt are ping-pong buffers of n entries.
 size_t sort_scratch_bytes(int64_t n);

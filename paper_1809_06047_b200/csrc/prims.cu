@@ -418,3 +418,34 @@ void offsets_from_sorted(const int32_t *keys, int64_t n, int32_t *off, int32_t n
 }
 
 }  // namespace alsub
+
+namespace alsub {
+// ---------------- vertex channels <-> 3-float frames (alsub_eval_attributes) ----------------
+// [V][C] channel rows <-> ceil(C/3) frames [g][V][3]; channel 3g + k of vertex v is component k
+// of frame g (the padding components of the last frame are zero)
+__global__ void k_pack_channels(const float *__restrict__ in, int64_t V, int32_t C, float *__restrict__ out) {
+    const int32_t ng = (C + 2) / 3;
+    const int64_t n = V * 3 * ng;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = i / (3 * V), r = i - g * 3 * V, v = r / 3;
+        const int32_t ch = (int32_t)(3 * g + (r - 3 * v));
+        out[i] = ch < C ? in[v * C + ch] : 0.0f;
+    }
+}
+__global__ void k_unpack_channels(const float *__restrict__ in, int64_t V, int32_t C, float *__restrict__ out) {
+    const int64_t n = V * C;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / C;
+        const int32_t ch = (int32_t)(i - v * C), g = ch / 3;
+        out[i] = in[(int64_t)g * 3 * V + 3 * v + (ch - 3 * g)];
+    }
+}
+void pack_channels(const float *in, int64_t V, int32_t C, float *out, cudaStream_t s, Launches &L) {
+    const int64_t n = V * 3 * ((C + 2) / 3);
+    if (n > 0) launch(L, "pack_channels", k_pack_channels, dim3((unsigned)std::min<int64_t>(grid_for(n), 148 * 16)), dim3(kThreads), 0, s, in, V, C, out);
+}
+void unpack_channels(const float *in, int64_t V, int32_t C, float *out, cudaStream_t s, Launches &L) {
+    const int64_t n = V * C;
+    if (n > 0) launch(L, "unpack_channels", k_unpack_channels, dim3((unsigned)std::min<int64_t>(grid_for(n), 148 * 16)), dim3(kThreads), 0, s, in, V, C, out);
+}
+}  // namespace alsub

@@ -342,3 +342,101 @@ def test_device_tensor_inputs():
         m.refine("loop", 3)
         w = oracle.refine(mesh, "loop", 3)[-1]
         assert np.array_equal(m.topology(3)["face_vtx"].cpu().numpy(), w["face_vtx"])
+
+
+def test_eval_attributes_channels():
+    """Extra vertex channels (NEXT-4, reading R22): every channel refined with the position
+    stencils, including boundaries and creases; checked against the oracle channel by channel."""
+    Mesh = _gpu()
+    mesh = mg.armor(8, 6, 7, 1, 2, 2, name="armor_attr")
+    L = 3
+    for C in (1, 2, 5):
+        attr = mg.vertex_channels(mesh, C)
+        with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+            m.refine("cc", L)
+            got_dev = m.eval_attributes(torch.from_numpy(attr).cuda(), L).cpu().numpy()
+            got_host = np.zeros_like(got_dev)
+            m.eval_attributes(attr, L, out=got_host)
+        assert np.array_equal(got_dev, got_host)
+        assert got_dev.shape[1] == C
+        for g in range(0, C, 3):
+            cols = attr[:, g:g + 3]
+            pad = np.zeros((attr.shape[0], 3), np.float32)
+            pad[:, :cols.shape[1]] = cols
+            m2 = dict(mesh)
+            m2["pos"] = pad
+            want = oracle.refine(m2, "cc", L)[-1]["pos"][:, :cols.shape[1]]
+            scale = float(np.linalg.norm(pad.max(0) - pad.min(0)))
+            err = np.abs(got_dev[:, g:g + 3] - want).max() / scale
+            assert err <= TOL, f"C={C} channels {g}..: {err:.3e}"
+
+
+def test_eval_attributes_match_frames_bitwise():
+    """Three channels are exactly one frame of alsub_eval_frames."""
+    Mesh = _gpu()
+    mesh = mg.armor(8, 6, 7, 1, 2, 2, name="armor_attr")
+    attr = mg.vertex_channels(mesh, 3)
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine("cc", 3)
+        a = m.eval_attributes(torch.from_numpy(attr).cuda(), 3)
+        f = m.eval_frames(torch.from_numpy(attr).cuda()[None], 3)[0]
+        assert torch.equal(a, f)
+
+
+@pytest.mark.parametrize("scheme,mesh_fn,L,k", [
+    ("cc", lambda: mg.armor(8, 6, 7, 1, 2, 2, name="armor_edit"), 3, 1),
+    ("cc", lambda: mg.armor(8, 6, 7, 1, 2, 2, name="armor_edit"), 4, 2),
+    ("loop", lambda: mg.tetrahedron(creased=True), 3, 1),
+    ("sqrt3", lambda: mg.torus_tris(10, 8), 3, 2),
+])
+def test_hierarchical_edit_reevaluate(scheme, mesh_fn, L, k):
+    """Displacement / hierarchical edit at level k: write the level-k positions
+    through the handle's view, re-evaluate levels k+1..L; equals the oracle refining the edited
+    level-k mesh L-k more times (topology and crease lists of level k from the oracle itself)."""
+    Mesh = _gpu()
+    mesh = mesh_fn()
+    recs = oracle.refine(mesh, scheme, k)
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine(scheme, L)
+        before = m.positions(L).clone()
+        view = m.level_positions_view(k)
+        view += torch.from_numpy(mg.displacement(view.shape[0])).cuda()
+        edited = view.cpu().numpy().copy()
+        m.reevaluate(k)
+        got = [m.positions(lv).cpu().numpy() for lv in range(k, L + 1)]
+        # topology untouched, positions changed
+        assert not torch.equal(before, m.positions(L))
+    mk = {"face_off": recs[k]["face_off"], "face_vtx": recs[k]["face_vtx"], "pos": edited,
+          "crease": recs[k]["crease"], "sigma": recs[k]["sigma"]}
+    want = oracle.refine(mk, scheme, L - k)
+    diag = diag_of(mesh)
+    assert np.array_equal(got[0], edited)
+    for i in range(1, L - k + 1):
+        err = np.abs(got[i].astype(np.float64) - want[i]["pos"]).max() / diag
+        assert err <= TOL, f"level {k + i}: {err:.3e}"
+
+
+def test_reevaluate_without_edit_is_bitwise_refine():
+    Mesh = _gpu()
+    mesh = mg.armor(8, 6, 7, 1, 2, 2, name="armor_edit")
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine("cc", 4)
+        ref = [m.positions(lv).clone() for lv in range(5)]
+        for k in (0, 2, 3, 4):
+            m.reevaluate(k)
+            for lv in range(5):
+                assert torch.equal(m.positions(lv), ref[lv]), f"from {k}: level {lv}"
+
+
+def test_edit_and_attribute_errors():
+    Mesh = _gpu()
+    from paper_1809_06047_b200.alsub import AlsubError
+    mesh = mg.cube()
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine("cc", 2)
+        with pytest.raises(AlsubError):
+            m.reevaluate(3)
+        with pytest.raises(AlsubError):
+            m.level_positions_view(5)
+        with pytest.raises(AlsubError):
+            m.eval_attributes(np.zeros((8, 2), np.float32), 3)
