@@ -156,6 +156,18 @@ alsub_status alsub_eval_attributes(alsub_mesh *mesh, int32_t levels, const float
 alsub_status alsub_level_positions_ptr(alsub_mesh *mesh, int32_t level, float **pos_dev);
 alsub_status alsub_reevaluate(alsub_mesh *mesh, int32_t from_level, void *stream);
 
+/* Reverse Cuthill-McKee ordering of a control mesh (RCM on the
+ * graph Laplacian of the mesh, rows of M permuted, columns sorted by their first non-zero).
+ * Host pointers, host computation (an offline preprocess; no handle, no GPU needed).
+ *   face_off [num_faces+1], face_vtx [face_off[num_faces]]: the mesh as for alsub_mesh_create
+ *   perm_vtx [num_verts]  out: perm_vtx[new] = old vertex id
+ *   perm_face [num_faces] out: perm_face[new] = old face id (faces by min new vertex id, stable)
+ * Tie breaking is fixed (degree, then id) -- see paper_1809_06047_b200/csrc/reorder.cpp.
+ * Relabel the mesh with these permutations before alsub_mesh_create.
+ * Errors: E_ARG (null pointers, negative counts), E_MESH (vertex index out of range). */
+alsub_status alsub_rcm_order(const int32_t *face_off, const int32_t *face_vtx, int32_t num_faces, int32_t num_verts,
+                             int32_t *perm_vtx, int32_t *perm_face);
+
 /* Number of kernel launches issued by the last alsub_refine / alsub_eval_frames call
  * (a graph replay counts the kernels inside it). */
 int64_t alsub_last_launch_count(const alsub_mesh *mesh);

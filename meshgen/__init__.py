@@ -378,3 +378,16 @@ def displacement(n, seed=SEED_FRAMES, scale=0.01):
     """Seeded per-vertex displacement vectors [n][3] fp32 (hierarchical-edit tests)."""
     rng = np.random.default_rng(seed + 1)
     return (rng.standard_normal((n, 3)) * scale).astype(np.float32)
+
+
+def permuted(mesh, perm_vtx, perm_face):
+    """The mesh relabelled by perm_vtx[new] = old vertex and perm_face[new] = old face (face
+    rotations kept); used with the RCM ordering (NEXT-2)."""
+    perm_vtx = np.asarray(perm_vtx, np.int64)
+    newid = np.empty_like(perm_vtx)
+    newid[perm_vtx] = np.arange(len(perm_vtx))
+    off, vtx = mesh["face_off"], mesh["face_vtx"]
+    faces = [list(newid[vtx[off[r]:off[r + 1]]]) for r in np.asarray(perm_face, np.int64)]
+    pos = np.asarray(mesh["pos"])[perm_vtx]
+    crease = newid[mesh["crease"]].astype(np.int32) if len(mesh["crease"]) else mesh["crease"]
+    return _pack(faces, pos, crease, mesh["sigma"], name=mesh.get("name", "mesh") + "_perm")

@@ -69,6 +69,7 @@ def lib():
     L.alsub_eval_attributes.argtypes = [vp, i32, vp, i32, vp, vp]
     L.alsub_level_positions_ptr.argtypes = [vp, i32, C.POINTER(vp)]
     L.alsub_reevaluate.argtypes = [vp, i32, vp]
+    L.alsub_rcm_order.argtypes = [vp, vp, i32, i32, vp, vp]
     L.alsub_last_launch_count.argtypes = [vp]
     L.alsub_last_launch_count.restype = i64
     L.alsub_mesh_destroy.argtypes = [vp]
@@ -77,7 +78,7 @@ def lib():
     L.alsub_version.restype = C.c_char_p
     for f in ("alsub_mesh_create", "alsub_set_positions", "alsub_refine", "alsub_refine_profile", "alsub_level_counts",
               "alsub_level_topology", "alsub_level_positions", "alsub_eval_frames", "alsub_eval_attributes",
-              "alsub_level_positions_ptr", "alsub_reevaluate"):
+              "alsub_level_positions_ptr", "alsub_reevaluate", "alsub_rcm_order"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -288,6 +289,18 @@ class Mesh:
     @property
     def last_launch_count(self):
         return int(self._lib.alsub_last_launch_count(self._h))
+
+
+def rcm_order(face_off, face_vtx, num_verts):
+    """Reverse Cuthill-McKee ordering of a control mesh (host, NEXT-2): returns numpy
+    (perm_vtx, perm_face) with perm[new] = old."""
+    fo = np.ascontiguousarray(face_off, dtype=np.int32)
+    fv = np.ascontiguousarray(face_vtx, dtype=np.int32)
+    F = len(fo) - 1
+    pv = np.empty(int(num_verts), dtype=np.int32)
+    pf = np.empty(F, dtype=np.int32)
+    _check(lib().alsub_rcm_order(_ptr(fo), _ptr(fv), F, int(num_verts), _ptr(pv), _ptr(pf)))
+    return pv, pf
 
 
 def version():

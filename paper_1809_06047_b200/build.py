@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "lib", "libalsub.so")
-SOURCES = ["prims.cu", "build0.cu", "cc.cu", "crease.cu", "loop_sqrt3.cu", "api.cu"]
+SOURCES = ["prims.cu", "build0.cu", "cc.cu", "crease.cu", "loop_sqrt3.cu", "api.cu", "reorder.cpp"]
 HEADERS = ["common.cuh", "internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -31,7 +31,7 @@ def _stale(target, deps):
 
 
 def _compile(src):
-    out = os.path.join(OBJ, src.replace(".cu", ".o"))
+    out = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "alsub.h")]
     if not _stale(out, deps):
         return out

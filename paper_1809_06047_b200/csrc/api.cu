@@ -29,6 +29,9 @@ static alsub_status fail(alsub_status st, const std::string &msg) {
     g_err = msg;
     return st;
 }
+namespace alsub {
+alsub_status set_error(alsub_status st, const char *msg) { return fail(st, msg); }
+}  // namespace alsub
 
 #define CU(call)                                                                                          \
     do {                                                                                                  \
