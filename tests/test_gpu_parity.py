@@ -440,3 +440,26 @@ def test_edit_and_attribute_errors():
             m.level_positions_view(5)
         with pytest.raises(AlsubError):
             m.eval_attributes(np.zeros((8, 2), np.float32), 3)
+
+
+def test_parity_large_creased_grid_unfused_levels():
+    """A control mesh above the fused-crease threshold (V0 >= 2^20): every level runs the separate
+    crease pass from level 0 on (boundary, sharp, semi-sharp and infinite crease lines)."""
+    import math
+    n = 1024
+    mesh = mg.grid(n, n, z=lambda i, j: 0.05 * math.sin(0.05 * i) * math.cos(0.07 * j), name="grid1024")
+    assert mesh["pos"].shape[0] >= (1 << 20)
+    vid = lambda i, j: j * (n + 1) + i
+    pairs, sig = [], []
+    for i in range(100, 900):
+        pairs.append((vid(i, 512), vid(i + 1, 512)))
+        sig.append(2.5)
+    for j in range(200, 700):
+        pairs.append((vid(300, j), vid(300, j + 1)))
+        sig.append(np.inf)
+    for i in range(50, 400):
+        pairs.append((vid(i, 800), vid(i + 1, 800)))
+        sig.append(0.5)
+    mesh["crease"] = np.asarray(pairs, np.int32)
+    mesh["sigma"] = np.asarray(sig, np.float32)
+    compare(mesh, "cc", 2)
