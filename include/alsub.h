@@ -156,6 +156,25 @@ alsub_status alsub_eval_attributes(alsub_mesh *mesh, int32_t levels, const float
 alsub_status alsub_level_positions_ptr(alsub_mesh *mesh, int32_t level, float **pos_dev);
 alsub_status alsub_reevaluate(alsub_mesh *mesh, int32_t from_level, void *stream);
 
+/* Selective / feature-adaptive subdivision, the extraction module (
+ * P:L459-499, Fig. module_selective).  From level `level` of `mesh` (0, or 1 .. levels of its
+ * last alsub_refine):
+ *   x_0 = vsel [V_level] uint8 (host or device; nonzero = selected), or NULL = the extraordinary
+ *         vertices, valence n = M 1 != 4 (Eq. vo)
+ *   `rings` >= 1 propagation steps q_i = M^T x_i (faces with a selected vertex), x_{i+1} = M q_i
+ *   M' = X M X̊, P' = X P: the selected faces and their vertices, both in ascending original order,
+ *   plus the level's live creases whose two vertices are selected (pairs that are not an edge of
+ *   an extracted face are dropped, reading R25)
+ * become the control mesh (level 0) of a new handle *out (same allocator); refine it as usual.
+ * Synchronises `stream` once (to size the new mesh).  Errors: E_ARG (null pointers, rings < 1,
+ * level out of range), E_NOMEM, E_CUDA, and the alsub_mesh_create errors of the extracted mesh. */
+alsub_status alsub_mesh_extract(const alsub_mesh *mesh, int32_t level, const uint8_t *vsel, int32_t rings,
+                                void *stream, alsub_mesh **out);
+/* Original ids of an extracted handle's control mesh: vtx_map [V0] and face_map [F0] (counts
+ * from alsub_level_counts(extracted, 0)); either may be NULL; host or device pointers.
+ * Errors: E_ARG (null mesh, or a handle not made by alsub_mesh_extract). */
+alsub_status alsub_extract_maps(const alsub_mesh *mesh, int32_t *vtx_map, int32_t *face_map, void *stream);
+
 /* Reverse Cuthill-McKee ordering of a control mesh (RCM on the
  * graph Laplacian of the mesh, rows of M permuted, columns sorted by their first non-zero).
  * Host pointers, host computation (an offline preprocess; no handle, no GPU needed).

@@ -70,6 +70,8 @@ def lib():
     L.alsub_level_positions_ptr.argtypes = [vp, i32, C.POINTER(vp)]
     L.alsub_reevaluate.argtypes = [vp, i32, vp]
     L.alsub_rcm_order.argtypes = [vp, vp, i32, i32, vp, vp]
+    L.alsub_mesh_extract.argtypes = [vp, i32, vp, i32, vp, C.POINTER(vp)]
+    L.alsub_extract_maps.argtypes = [vp, vp, vp, vp]
     L.alsub_last_launch_count.argtypes = [vp]
     L.alsub_last_launch_count.restype = i64
     L.alsub_mesh_destroy.argtypes = [vp]
@@ -78,7 +80,8 @@ def lib():
     L.alsub_version.restype = C.c_char_p
     for f in ("alsub_mesh_create", "alsub_set_positions", "alsub_refine", "alsub_refine_profile", "alsub_level_counts",
               "alsub_level_topology", "alsub_level_positions", "alsub_eval_frames", "alsub_eval_attributes",
-              "alsub_level_positions_ptr", "alsub_reevaluate", "alsub_rcm_order"):
+              "alsub_level_positions_ptr", "alsub_reevaluate", "alsub_rcm_order", "alsub_mesh_extract",
+              "alsub_extract_maps"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -175,6 +178,27 @@ class Mesh:
         self._h = h
         self.scheme = None
         self.levels = None
+
+    def extract(self, level, vsel=None, rings=1, stream=None):
+        """Selective / feature-adaptive subdivision, extraction module: the faces
+        within `rings` propagation steps of the selected vertices of `level` (vsel: bool/uint8
+        [V_level]; None = extraordinary vertices, valence != 4) as a new control mesh.
+        Returns (Mesh, vtx_map, face_map) with the original ids (int32 CUDA tensors)."""
+        sel = None
+        if vsel is not None:
+            sel = vsel.to(torch.uint8).contiguous() if isinstance(vsel, torch.Tensor) else \
+                np.ascontiguousarray(np.asarray(vsel), dtype=np.uint8)
+        h = C.c_void_p()
+        _check(self._lib.alsub_mesh_extract(self._h, int(level), _ptr(sel), int(rings), _stream(stream), C.byref(h)))
+        sub = Mesh.__new__(Mesh)
+        sub._lib, sub.device, sub._keep = self._lib, self.device, []
+        sub._alloc = self._alloc  # the extracted handle allocates through the same allocator
+        sub._h, sub.scheme, sub.levels = h, None, None
+        c = sub.counts(0)
+        vm = torch.empty(c["verts"], dtype=torch.int32, device="cuda")
+        fm = torch.empty(c["faces"], dtype=torch.int32, device="cuda")
+        _check(self._lib.alsub_extract_maps(sub._h, _ptr(vm), _ptr(fm), _stream(stream)))
+        return sub, vm, fm
 
     # -- lifetime --
     def close(self):

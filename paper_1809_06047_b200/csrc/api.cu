@@ -79,6 +79,9 @@ struct alsub_mesh {
     float *in_sigma = nullptr, *pos0 = nullptr;
     Build0 b0{};
     int32_t E0 = 0, B0 = 0, K0 = 0, NSV0 = 0;
+    // a handle made by alsub_mesh_extract: original vertex / face ids of its control mesh
+    int32_t *ext_vmap = nullptr, *ext_fmap = nullptr;
+    bool extracted = false;
     bool user_creases = false;
     int32_t *sv_vtx = nullptr, *sv_off = nullptr;  // shared special-vertex table (prefix per level)
     int32_t *sv_vtx_create = nullptr, *sv_off_create = nullptr;
@@ -182,10 +185,24 @@ static alsub_status map_flags(int32_t flags) {
     return ALSUB_OK;
 }
 
+static alsub_status create_impl(const int32_t *face_off, const int32_t *face_vtx, int32_t num_faces, const float *pos,
+                                int32_t num_verts, const int32_t *crease_pairs, const float *crease_sigma,
+                                int32_t num_creases, const alsub_allocator *alloc, void *stream, alsub_mesh **out,
+                                bool lenient);
+
 extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t *face_vtx, int32_t num_faces,
                                           const float *pos, int32_t num_verts, const int32_t *crease_pairs,
                                           const float *crease_sigma, int32_t num_creases,
                                           const alsub_allocator *alloc, void *stream, alsub_mesh **out) {
+    return create_impl(face_off, face_vtx, num_faces, pos, num_verts, crease_pairs, crease_sigma, num_creases, alloc,
+                       stream, out, false);
+}
+
+// lenient: crease pairs that are not edges are dropped instead of rejected (extracted meshes, R25)
+static alsub_status create_impl(const int32_t *face_off, const int32_t *face_vtx, int32_t num_faces, const float *pos,
+                                int32_t num_verts, const int32_t *crease_pairs, const float *crease_sigma,
+                                int32_t num_creases, const alsub_allocator *alloc, void *stream, alsub_mesh **out,
+                                bool lenient) {
     if (!out) return fail(ALSUB_E_ARG, "out is null");
     *out = nullptr;
     if (num_faces < 0 || num_verts < 0 || num_creases < 0) return fail(ALSUB_E_ARG, "negative count");
@@ -235,6 +252,7 @@ extern "C" alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t
     }
     Build0 &b = m->b0;
     b.V = num_verts; b.F = num_faces; b.S = S0; b.K_in = num_creases; b.order = order;
+    b.crease_lenient = lenient ? 1 : 0;
     b.face_off = m->in_face_off; b.face_vtx = m->in_face_vtx; b.crease_in = m->in_crease; b.sigma_in = m->in_sigma;
     b.slot_face = A<int32_t>(m, S0, s, ML, ok);
     b.sort_k = A<int32_t>(m, S0, s, ML, ok);
@@ -782,6 +800,79 @@ extern "C" alsub_status alsub_level_positions(const alsub_mesh *m, int32_t level
     }
     CU(cudaMemcpyAsync(pos, src, sizeof(float) * 3 * (size_t)V, cudaMemcpyDefault, s));
     if (!is_device_ptr(pos)) CU(cudaStreamSynchronize(s));
+    return ALSUB_OK;
+}
+
+// ---------------- selective subdivision: extraction ----------------
+extern "C" alsub_status alsub_mesh_extract(const alsub_mesh *m, int32_t level, const uint8_t *vsel, int32_t rings,
+                                           void *stream, alsub_mesh **out) {
+    if (!m || !out) return fail(ALSUB_E_ARG, "null argument");
+    *out = nullptr;
+    if (rings < 1) return fail(ALSUB_E_ARG, "rings must be >= 1");
+    if (level < 0 || (level > 0 && level > m->levels)) return fail(ALSUB_E_ARG, "level outside 0 .. levels of the last alsub_refine");
+    cudaStream_t s = (cudaStream_t)stream;
+    ExSrcHost h{};
+    if (level == 0) {
+        h = ExSrcHost{m->V0, m->F0, m->S0, m->order0 == 0 ? 0 : m->order0, m->in_face_off, m->in_face_vtx, m->pos0,
+                      m->b0.sp, m->K0};
+        if (m->order0 != 0) h.face_off = nullptr;
+    } else {
+        const LevelHost &L = m->lv[level];
+        const bool special = m->scheme != ALSUB_SQRT3 && m->K0 > 0;
+        h = ExSrcHost{(int32_t)L.V, (int32_t)L.F, (int32_t)L.S, L.order, nullptr, L.face_vtx, L.pos,
+                      special ? L.sp : nullptr, special ? (int32_t)L.nsp : 0};
+    }
+    alsub_mesh *mm = const_cast<alsub_mesh *>(m);
+    std::vector<std::pair<void *, size_t>> tmp;
+    bool ok = true;
+    const int64_t V = h.V, F = h.F, S = h.S, K = h.nsp;
+    const uint8_t *vsel_dev = vsel;
+    if (vsel && !is_device_ptr(vsel)) {
+        uint8_t *d = A<uint8_t>(mm, V, s, tmp, ok);
+        if (ok && V > 0) CU(cudaMemcpyAsync(d, vsel, (size_t)V, cudaMemcpyHostToDevice, s));
+        vsel_dev = d;
+    }
+    ExWork w{};
+    w.n = A<int32_t>(mm, V, s, tmp, ok); w.x = A<int32_t>(mm, V, s, tmp, ok); w.vid = A<int32_t>(mm, V, s, tmp, ok);
+    w.q = A<int32_t>(mm, F, s, tmp, ok); w.fid = A<int32_t>(mm, F, s, tmp, ok); w.fo = A<int32_t>(mm, F, s, tmp, ok);
+    w.foff = A<int32_t>(mm, F, s, tmp, ok); w.cflag = A<int32_t>(mm, K, s, tmp, ok); w.cid = A<int32_t>(mm, K, s, tmp, ok);
+    w.tot = A<int32_t>(mm, 4, s, tmp, ok);
+    w.scratch = dev_alloc(mm, scan_scratch_bytes(std::max(std::max(V, F), std::max(K, (int64_t)1))), s, tmp);
+    ExOutHost o{};
+    o.face_off = A<int32_t>(mm, F + 1, s, tmp, ok); o.face_vtx = A<int32_t>(mm, S, s, tmp, ok);
+    o.vmap = A<int32_t>(mm, V, s, tmp, ok); o.fmap = A<int32_t>(mm, F, s, tmp, ok);
+    o.crease = A<int32_t>(mm, 2 * K, s, tmp, ok); o.pos = A<float>(mm, 3 * V, s, tmp, ok);
+    o.sigma = A<float>(mm, K, s, tmp, ok);
+    if (!ok || !w.scratch) { free_list(mm, tmp, s); return fail(ALSUB_E_NOMEM, "extraction buffers"); }
+    Launches L;
+    extract_level(h, vsel_dev, rings, w, o, s, L);
+    int32_t tot[4] = {0, 0, 0, 0};
+    CU(cudaMemcpyAsync(tot, w.tot, sizeof(tot), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    alsub_mesh *n = nullptr;
+    const alsub_allocator *al = m->custom ? &m->alloc : nullptr;
+    alsub_status st = create_impl(o.face_off, o.face_vtx, tot[1], o.pos, tot[0], o.crease, o.sigma, tot[3], al, stream,
+                                  &n, true);
+    if (st != ALSUB_OK) { free_list(mm, tmp, s); return st; }
+    n->ext_vmap = A<int32_t>(n, tot[0], s, n->mem_create, ok);
+    n->ext_fmap = A<int32_t>(n, tot[1], s, n->mem_create, ok);
+    if (!ok) { free_list(mm, tmp, s); alsub_mesh_destroy(n); return fail(ALSUB_E_NOMEM, "extraction maps"); }
+    if (tot[0] > 0) CU(cudaMemcpyAsync(n->ext_vmap, o.vmap, sizeof(int32_t) * tot[0], cudaMemcpyDeviceToDevice, s));
+    if (tot[1] > 0) CU(cudaMemcpyAsync(n->ext_fmap, o.fmap, sizeof(int32_t) * tot[1], cudaMemcpyDeviceToDevice, s));
+    n->extracted = true;
+    free_list(mm, tmp, s);
+    CU(cudaGetLastError());
+    *out = n;
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_extract_maps(const alsub_mesh *m, int32_t *vtx_map, int32_t *face_map, void *stream) {
+    if (!m) return fail(ALSUB_E_ARG, "null mesh");
+    if (!m->extracted) return fail(ALSUB_E_ARG, "not a handle made by alsub_mesh_extract");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (vtx_map && m->V0 > 0) CU(cudaMemcpyAsync(vtx_map, m->ext_vmap, sizeof(int32_t) * m->V0, cudaMemcpyDefault, s));
+    if (face_map && m->F0 > 0) CU(cudaMemcpyAsync(face_map, m->ext_fmap, sizeof(int32_t) * m->F0, cudaMemcpyDefault, s));
+    if ((vtx_map && !is_device_ptr(vtx_map)) || (face_map && !is_device_ptr(face_map))) CU(cudaStreamSynchronize(s));
     return ALSUB_OK;
 }
 

@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kThreads) k_b0_flags(const int32_t *__restrict
                                                      T0 tp, int32_t V, int32_t E, const uint32_t *__restrict__ bnd_word,
                                                      int32_t nw, float *__restrict__ edge_sigma,
                                                      int32_t *__restrict__ edge_cidx, int32_t *__restrict__ flag,
-                                                     int32_t *__restrict__ wcnt, int32_t *flags) {
+                                                     int32_t *__restrict__ wcnt, int32_t *flags, int32_t lenient) {
     ALSUB_GRID_WAIT();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < E && edge_hh[t].y < 0) atomicOr(flag + t, 1);
@@ -269,7 +269,10 @@ __global__ void __launch_bounds__(kThreads) k_b0_flags(const int32_t *__restrict
         if (m) { e = __shfl_sync(0xffffffffu, cand, __ffs(m) - 1); break; }
     }
     if (lane != 0) return;
-    if (e < 0) { atomicOr(flags, kFlagCrease); return; }
+    if (e < 0) {
+        if (!lenient) atomicOr(flags, kFlagCrease);
+        return;
+    }
     if (atomicCAS(edge_cidx + e, -1, (int32_t)k) != -1) { atomicOr(flags, kFlagCrease); return; }
     if (sg > 0.0f && edge_hh[e].y >= 0) {  // boundary edges are infinitely sharp anyway (R19)
         edge_sigma[e] = sg;
@@ -436,7 +439,7 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     const int64_t nf = std::max<int64_t>(std::max<int64_t>(E, 32 * (int64_t)b.K_in), nw);
     launch(L, "b0_flags", k_b0_flags, dim3(grid_for(nf)), dim3(kThreads), 0, s, b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
                                                  b.face_edge, b.edge_hh, tp, b.V, E, b.bnd_word, nw, b.edge_sigma,
-                                                 b.edge_cidx, b.sp_flag, b.bnd_wcnt, b.flags);
+                                                 b.edge_cidx, b.sp_flag, b.bnd_wcnt, b.flags, b.crease_lenient);
     scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, region(b, 3), s, L, b.zeroed);
     scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, region(b, 4), s, L, b.zeroed);
     if (E > 0) {

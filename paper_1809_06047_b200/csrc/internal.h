@@ -134,10 +134,33 @@ struct Build0 {
     void *scratch;
     bool zeroed = false;          // refine: every work array and scan region pre-initialised by k_zero
     bool no_special = false;      // refine of a closed, crease-free mesh: skip boundary/crease tables
+    int32_t crease_lenient = 0;   // 1: crease pairs that are not edges are dropped (extracted meshes)
 };
 size_t build0_scratch_bytes(int32_t V, int32_t S);
 // refine: add the level-0 work arrays / scan regions to z (one k_zero launch instead of memsets)
 void build0_zero_segments(Build0 &b, ZeroSegs &z);
+
+// ---- selective subdivision: extraction (extract.cu) ----
+struct ExSrcHost {
+    int32_t V, F, S, order;  // order 3 / 4 (face r = slots [order r, ...)) or 0 (face_off)
+    const int32_t *face_off, *face_vtx;
+    const float *pos;        // [V][3]
+    const SpEdge *sp;        // the level's special-edge list (creases + boundary)
+    int32_t nsp;
+};
+// device work arrays: n, x, vid [V]; q, fid, fo, foff [F]; cflag, cid [nsp]; tot [4] (V', F',
+// S', K'); scratch of scan_scratch_bytes(max(V, F, nsp))
+struct ExWork {
+    int32_t *n, *x, *vid, *q, *fid, *fo, *foff, *cflag, *cid, *tot;
+    void *scratch;
+};
+// device outputs sized V, F + 1, S, V, F, 2 nsp, 3 V, nsp
+struct ExOutHost {
+    int32_t *face_off, *face_vtx, *vmap, *fmap, *crease;
+    float *pos, *sigma;
+};
+void extract_level(const ExSrcHost &h, const uint8_t *vsel, int32_t rings, ExWork &w, ExOutHost &out, cudaStream_t s,
+                   Launches &L);
 void build0_validate(Build0 &b, cudaStream_t s, Launches &L);
 void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L);  // through edge_off + scalars[0]
 void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L);  // needs b.E

@@ -424,6 +424,7 @@ namespace alsub {
 // [V][C] channel rows <-> ceil(C/3) frames [g][V][3]; channel 3g + k of vertex v is component k
 // of frame g (the padding components of the last frame are zero)
 __global__ void k_pack_channels(const float *__restrict__ in, int64_t V, int32_t C, float *__restrict__ out) {
+    ALSUB_GRID_WAIT();
     const int32_t ng = (C + 2) / 3;
     const int64_t n = V * 3 * ng;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -433,6 +434,7 @@ __global__ void k_pack_channels(const float *__restrict__ in, int64_t V, int32_t
     }
 }
 __global__ void k_unpack_channels(const float *__restrict__ in, int64_t V, int32_t C, float *__restrict__ out) {
+    ALSUB_GRID_WAIT();
     const int64_t n = V * C;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = i / C;
