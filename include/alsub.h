@@ -156,6 +156,26 @@ alsub_status alsub_eval_attributes(alsub_mesh *mesh, int32_t levels, const float
 alsub_status alsub_level_positions_ptr(alsub_mesh *mesh, int32_t level, float **pos_dev);
 alsub_status alsub_reevaluate(alsub_mesh *mesh, int32_t from_level, void *stream);
 
+/* The refinement matrix R = R_{L-1} ... R_0:
+ * P_L = R P_0 for the topology of the last alsub_refine (CC or Loop).  Built by probing: each
+ * control face f owns the level-`levels` vertices of its descendant faces (smallest f wins), a row
+ * is supported on the 1-ring vertex set of its owner, and a colouring of the control vertices with
+ * no repeated colour inside any 1-ring lets ceil(colours / 3) probe frames through the static path
+ * (alsub_eval_frames) read every weight exactly once.  Rows in CSR, exact zeros dropped.
+ * Errors: E_ARG (levels outside 1 .. last refine), E_SCHEME (sqrt3), E_NOMEM, E_CUDA. */
+alsub_status alsub_build_refinement_matrix(alsub_mesh *mesh, int32_t levels, void *stream);
+/* levels, rows (= V_levels) and non-zeros of the built matrix; any pointer may be NULL. */
+alsub_status alsub_refinement_matrix_info(const alsub_mesh *mesh, int32_t *levels, int64_t *rows, int64_t *nnz);
+/* CSR export: row_off [rows+1], cols [nnz] (control vertex ids, ascending per row), vals [nnz];
+ * host or device pointers, any may be NULL; synchronises `stream`. */
+alsub_status alsub_refinement_matrix_csr(const alsub_mesh *mesh, int32_t *row_off, int32_t *cols, float *vals,
+                                         void *stream);
+/* Static evaluation by the single SpMM P_L = R P_0: frames_in [num_frames][V0][3],
+ * frames_out [num_frames][V_levels][3], DEVICE pointers; batches of 32 frames.
+ * Errors: E_ARG (no matrix built, host pointers). */
+alsub_status alsub_eval_frames_matrix(alsub_mesh *mesh, const float *frames_in, int32_t num_frames, float *frames_out,
+                                      void *stream);
+
 /* Selective / feature-adaptive subdivision, the extraction module (
  * P:L459-499, Fig. module_selective).  From level `level` of `mesh` (0, or 1 .. levels of its
  * last alsub_refine):

@@ -177,3 +177,23 @@ def loop_beta(n):
 
 def sqrt3_alpha(n):
     return lib().om_sqrt3_alpha(int(n))
+
+
+def refinement_matrix(mesh, scheme, levels):
+    """The refinement matrix R (P_L = R P_0) by its definition: refinement is linear in
+    the vertex data, so column j of R is the refinement of the unit vector e_j (three columns per
+    call, one per coordinate).  Dense float64 [V_levels, V0]; small meshes only."""
+    V0 = int(np.asarray(mesh["pos"]).reshape(-1, 3).shape[0])
+    cols = []
+    for j0 in range(0, V0, 3):
+        m = dict(mesh)
+        pos = np.zeros((V0, 3))
+        for c in range(3):
+            if j0 + c < V0:
+                pos[j0 + c, c] = 1.0
+        m["pos"] = pos
+        out = refine(m, scheme, levels)[-1]["pos"]
+        for c in range(3):
+            if j0 + c < V0:
+                cols.append(out[:, c])
+    return np.stack(cols, axis=1) if cols else np.zeros((0, 0))

@@ -71,6 +71,10 @@ def lib():
     L.alsub_reevaluate.argtypes = [vp, i32, vp]
     L.alsub_rcm_order.argtypes = [vp, vp, i32, i32, vp, vp]
     L.alsub_mesh_extract.argtypes = [vp, i32, vp, i32, vp, C.POINTER(vp)]
+    L.alsub_build_refinement_matrix.argtypes = [vp, i32, vp]
+    L.alsub_refinement_matrix_info.argtypes = [vp, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64)]
+    L.alsub_refinement_matrix_csr.argtypes = [vp, vp, vp, vp, vp]
+    L.alsub_eval_frames_matrix.argtypes = [vp, vp, i32, vp, vp]
     L.alsub_extract_maps.argtypes = [vp, vp, vp, vp]
     L.alsub_last_launch_count.argtypes = [vp]
     L.alsub_last_launch_count.restype = i64
@@ -81,7 +85,8 @@ def lib():
     for f in ("alsub_mesh_create", "alsub_set_positions", "alsub_refine", "alsub_refine_profile", "alsub_level_counts",
               "alsub_level_topology", "alsub_level_positions", "alsub_eval_frames", "alsub_eval_attributes",
               "alsub_level_positions_ptr", "alsub_reevaluate", "alsub_rcm_order", "alsub_mesh_extract",
-              "alsub_extract_maps"):
+              "alsub_extract_maps", "alsub_build_refinement_matrix", "alsub_refinement_matrix_info",
+              "alsub_refinement_matrix_csr", "alsub_eval_frames_matrix"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -178,6 +183,36 @@ class Mesh:
         self._h = h
         self.scheme = None
         self.levels = None
+
+    # -- refinement matrix R (NEXT-1) --
+    def build_refinement_matrix(self, levels, stream=None):
+        """P_L = R P_0 for the last refine's topology, R built by probing the static path."""
+        _check(self._lib.alsub_build_refinement_matrix(self._h, int(levels), _stream(stream)))
+        return self.refinement_matrix_info()
+
+    def refinement_matrix_info(self):
+        lv, rows, nnz = C.c_int32(), C.c_int64(), C.c_int64()
+        _check(self._lib.alsub_refinement_matrix_info(self._h, C.byref(lv), C.byref(rows), C.byref(nnz)))
+        return {"levels": lv.value, "rows": rows.value, "nnz": nnz.value}
+
+    def refinement_matrix_csr(self):
+        """(row_off, cols, vals) numpy arrays of R."""
+        info = self.refinement_matrix_info()
+        ro = np.empty(info["rows"] + 1, np.int32)
+        co = np.empty(info["nnz"], np.int32)
+        va = np.empty(info["nnz"], np.float32)
+        _check(self._lib.alsub_refinement_matrix_csr(self._h, _ptr(ro), _ptr(co), _ptr(va), _stream(None)))
+        return ro, co, va
+
+    def eval_frames_matrix(self, frames, out=None, stream=None):
+        """Static mode by the single SpMM P_L = R P_0: frames [B, V0, 3] (CUDA) -> [B, V_L, 3]."""
+        fr = frames.to(torch.float32).contiguous()
+        B = int(fr.shape[0])
+        rows = self.refinement_matrix_info()["rows"]
+        if out is None:
+            out = torch.empty((B, rows, 3), dtype=torch.float32, device="cuda")
+        _check(self._lib.alsub_eval_frames_matrix(self._h, _ptr(fr), B, _ptr(out), _stream(stream)))
+        return out
 
     def extract(self, level, vsel=None, rings=1, stream=None):
         """Selective / feature-adaptive subdivision, extraction module: the faces

@@ -7,6 +7,7 @@
 // asynchronous and replayable as a CUDA graph.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -104,6 +105,13 @@ struct alsub_mesh {
     cudaStream_t side_stream = nullptr;  // second branch for independent level kernels
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t last_launches = 0;
+    // refinement matrix R (NEXT-1): CSR rows of level rm_levels over the control vertices
+    std::vector<std::pair<void *, size_t>> mem_rm;
+    int32_t rm_levels = -1, rm_scheme = -1;
+    int64_t rm_nnz = 0;
+    int32_t *rm_row_off = nullptr;
+    int2 *rm_ent = nullptr;
+    float *rm_p0i = nullptr;
     // frames
     int frames_nb = 0;
     std::vector<float *> frame_buf;
@@ -965,6 +973,163 @@ extern "C" alsub_status alsub_eval_attributes(alsub_mesh *m, int32_t levels, con
     return ALSUB_OK;
 }
 
+// ---------------- refinement matrix R (NEXT-1) ----------------
+extern "C" alsub_status alsub_build_refinement_matrix(alsub_mesh *m, int32_t levels, void *stream) {
+    if (!m) return fail(ALSUB_E_ARG, "null mesh");
+    if (m->levels < 1 || levels < 1 || levels > m->levels) return fail(ALSUB_E_ARG, "levels outside 1 .. levels of the last alsub_refine");
+    if (m->scheme == ALSUB_SQRT3) return fail(ALSUB_E_SCHEME, "sqrt3 faces do not nest in their parents: no per-face support");
+    cudaStream_t s = (cudaStream_t)stream;
+    free_list(m, m->mem_rm, s);
+    m->rm_levels = -1;
+    const int32_t V0 = m->V0, F0 = m->F0;
+    const int64_t VL = m->lv[levels].V, FL = m->lv[levels].F;
+    // host: the control faces, their 1-ring vertex sets S_f and a colouring of the control vertices
+    // with no two vertices of one colour in any S_f
+    std::vector<int32_t> off((size_t)F0 + 1), fv((size_t)m->S0);
+    CU(cudaMemcpyAsync(off.data(), m->in_face_off, sizeof(int32_t) * off.size(), cudaMemcpyDeviceToHost, s));
+    if (m->S0 > 0) CU(cudaMemcpyAsync(fv.data(), m->in_face_vtx, sizeof(int32_t) * fv.size(), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    std::vector<int32_t> vf_off((size_t)V0 + 1, 0), vf;
+    for (int32_t h = 0; h < m->S0; ++h) ++vf_off[fv[h] + 1];
+    for (int32_t v = 0; v < V0; ++v) vf_off[v + 1] += vf_off[v];
+    vf.resize((size_t)m->S0);
+    {
+        std::vector<int32_t> cur(vf_off.begin(), vf_off.end() - 1);
+        for (int32_t r = 0; r < F0; ++r)
+            for (int32_t h = off[r]; h < off[r + 1]; ++h) vf[cur[fv[h]]++] = r;
+    }
+    std::vector<int32_t> sup_off((size_t)F0 + 1, 0), sup, mark((size_t)V0, -1);
+    for (int32_t r = 0; r < F0; ++r) {
+        const size_t b = sup.size();
+        for (int32_t h = off[r]; h < off[r + 1]; ++h)
+            for (int32_t q = vf_off[fv[h]]; q < vf_off[fv[h] + 1]; ++q) {
+                const int32_t g = vf[q];
+                for (int32_t k = off[g]; k < off[g + 1]; ++k)
+                    if (mark[fv[k]] != r) { mark[fv[k]] = r; sup.push_back(fv[k]); }
+            }
+        std::sort(sup.begin() + b, sup.end());
+        sup_off[r + 1] = (int32_t)sup.size();
+    }
+    // faces whose support holds v (the inverse lists), then greedy colouring in vertex order
+    std::vector<int32_t> fs_off((size_t)V0 + 1, 0), fs;
+    for (int32_t v : sup) ++fs_off[v + 1];
+    for (int32_t v = 0; v < V0; ++v) fs_off[v + 1] += fs_off[v];
+    fs.resize(sup.size());
+    {
+        std::vector<int32_t> cur(fs_off.begin(), fs_off.end() - 1);
+        for (int32_t r = 0; r < F0; ++r)
+            for (int32_t k = sup_off[r]; k < sup_off[r + 1]; ++k) fs[cur[sup[k]]++] = r;
+    }
+    std::vector<int32_t> colour((size_t)V0, -1), used;
+    int32_t ncol = 0;
+    for (int32_t v = 0; v < V0; ++v) {
+        used.assign((size_t)ncol + 1, 0);
+        for (int32_t q = fs_off[v]; q < fs_off[v + 1]; ++q)
+            for (int32_t k = sup_off[fs[q]]; k < sup_off[fs[q] + 1]; ++k)
+                if (colour[sup[k]] >= 0) used[colour[sup[k]]] = 1;
+        int32_t c = 0;
+        while (used[c]) ++c;
+        colour[v] = c;
+        ncol = std::max(ncol, c + 1);
+    }
+    const int32_t nprobe = (ncol + 2) / 3;
+    // device: probes through the static path, owners, two-pass CSR assembly
+    std::vector<std::pair<void *, size_t>> tmp;
+    bool ok = true;
+    int32_t *d_sup_off = A<int32_t>(m, F0 + 1, s, tmp, ok), *d_sup = A<int32_t>(m, (int64_t)sup.size(), s, tmp, ok);
+    int32_t *d_col = A<int32_t>(m, V0, s, tmp, ok), *d_owner = A<int32_t>(m, VL, s, tmp, ok);
+    int32_t *d_len = A<int32_t>(m, VL + 1, s, tmp, ok), *d_tot = A<int32_t>(m, 1, s, tmp, ok);
+    float *d_pin = A<float>(m, 3 * (int64_t)V0 * std::max(nprobe, 1), s, tmp, ok);
+    float *d_pout = A<float>(m, 3 * VL * std::max(nprobe, 1), s, tmp, ok);
+    void *scr = dev_alloc(m, scan_scratch_bytes(VL + 1), s, tmp);
+    m->rm_row_off = A<int32_t>(m, VL + 1, s, m->mem_rm, ok);
+    m->rm_p0i = A<float>(m, 3 * (int64_t)V0 * kRmLanes, s, m->mem_rm, ok);
+    if (!ok || !scr) { free_list(m, tmp, s); free_list(m, m->mem_rm, s); return fail(ALSUB_E_NOMEM, "refinement matrix buffers"); }
+    CU(cudaMemcpyAsync(d_sup_off, sup_off.data(), sizeof(int32_t) * sup_off.size(), cudaMemcpyHostToDevice, s));
+    if (!sup.empty()) CU(cudaMemcpyAsync(d_sup, sup.data(), sizeof(int32_t) * sup.size(), cudaMemcpyHostToDevice, s));
+    if (V0 > 0) CU(cudaMemcpyAsync(d_col, colour.data(), sizeof(int32_t) * V0, cudaMemcpyHostToDevice, s));
+    Launches L;
+    rm_probes(V0, d_col, nprobe, d_pin, s, L);
+    alsub_status st = nprobe > 0 ? alsub_eval_frames(m, levels, d_pin, nprobe, d_pout, stream) : ALSUB_OK;
+    if (st != ALSUB_OK) { free_list(m, tmp, s); free_list(m, m->mem_rm, s); return st; }
+    {
+        ZeroSegs z;
+        z.add(d_owner, VL, INT32_MAX);
+        z.add(d_len + VL, 1, 0);
+        zero_segments(z, s, L);
+    }
+    const int shift = m->scheme == ALSUB_CATMULL_CLARK ? 2 * (levels - 1) : 2 * levels;
+    rm_owner(m->lv[levels].face_vtx, (int32_t)FL, m->lv[levels].order, shift,
+             m->scheme == ALSUB_CATMULL_CLARK ? m->b0.slot_face : nullptr, d_owner, s, L);
+    rm_assemble((int32_t)VL, d_owner, d_sup_off, d_sup, d_col, d_pout, 3 * VL, false, d_len, nullptr, nullptr, s, L);
+    scan_exclusive(d_len, m->rm_row_off, VL + 1, d_tot, scr, s, L);
+    int32_t nnz = 0;
+    CU(cudaMemcpyAsync(&nnz, d_tot, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    m->rm_ent = A<int2>(m, std::max<int64_t>(nnz, 1), s, m->mem_rm, ok);
+    if (!ok) { free_list(m, tmp, s); free_list(m, m->mem_rm, s); return fail(ALSUB_E_NOMEM, "refinement matrix entries"); }
+    rm_assemble((int32_t)VL, d_owner, d_sup_off, d_sup, d_col, d_pout, 3 * VL, true, nullptr, m->rm_row_off, m->rm_ent, s, L);
+    free_list(m, tmp, s);
+    m->rm_levels = levels;
+    m->rm_scheme = m->scheme;
+    m->rm_nnz = nnz;
+    m->last_launches = L.n;
+    CU(cudaGetLastError());
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_refinement_matrix_info(const alsub_mesh *m, int32_t *levels, int64_t *rows, int64_t *nnz) {
+    if (!m) return fail(ALSUB_E_ARG, "null mesh");
+    if (m->rm_levels < 0) return fail(ALSUB_E_ARG, "no refinement matrix: call alsub_build_refinement_matrix");
+    if (levels) *levels = m->rm_levels;
+    if (rows) *rows = m->lv[m->rm_levels].V;
+    if (nnz) *nnz = m->rm_nnz;
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_refinement_matrix_csr(const alsub_mesh *m, int32_t *row_off, int32_t *cols, float *vals,
+                                                    void *stream) {
+    if (!m) return fail(ALSUB_E_ARG, "null mesh");
+    if (m->rm_levels < 0) return fail(ALSUB_E_ARG, "no refinement matrix: call alsub_build_refinement_matrix");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t VL = m->lv[m->rm_levels].V;
+    if (row_off) CU(cudaMemcpyAsync(row_off, m->rm_row_off, sizeof(int32_t) * (VL + 1), cudaMemcpyDefault, s));
+    if ((cols || vals) && m->rm_nnz > 0) {
+        std::vector<int2> e((size_t)m->rm_nnz);
+        CU(cudaMemcpyAsync(e.data(), m->rm_ent, sizeof(int2) * e.size(), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        std::vector<int32_t> c(e.size());
+        std::vector<float> v(e.size());
+        for (size_t i = 0; i < e.size(); ++i) {
+            c[i] = e[i].x;
+            memcpy(&v[i], &e[i].y, sizeof(float));
+        }
+        if (cols) CU(cudaMemcpyAsync(cols, c.data(), sizeof(int32_t) * c.size(), cudaMemcpyDefault, s));
+        if (vals) CU(cudaMemcpyAsync(vals, v.data(), sizeof(float) * v.size(), cudaMemcpyDefault, s));
+    }
+    CU(cudaStreamSynchronize(s));
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_eval_frames_matrix(alsub_mesh *m, const float *frames_in, int32_t num_frames,
+                                                 float *frames_out, void *stream) {
+    if (!m || num_frames < 0 || (num_frames > 0 && (!frames_in || !frames_out))) return fail(ALSUB_E_ARG, "bad argument");
+    if (m->rm_levels < 0) return fail(ALSUB_E_ARG, "no refinement matrix: call alsub_build_refinement_matrix");
+    if (num_frames > 0 && (!is_device_ptr(frames_in) || !is_device_ptr(frames_out)))
+        return fail(ALSUB_E_ARG, "alsub_eval_frames_matrix takes device pointers");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t V0 = m->V0, VL = m->lv[m->rm_levels].V;
+    Launches L;
+    for (int32_t f0 = 0; f0 < num_frames; f0 += kRmLanes) {
+        const int32_t n = std::min(kRmLanes, num_frames - f0);
+        rm_interleave(frames_in + 3 * V0 * (int64_t)f0, (int32_t)V0, n, m->rm_p0i, s, L);
+        rm_spmm((int32_t)VL, m->rm_row_off, m->rm_ent, m->rm_p0i, n, frames_out + 3 * VL * (int64_t)f0, s, L);
+    }
+    m->last_launches = L.n;
+    CU(cudaGetLastError());
+    return ALSUB_OK;
+}
+
 // ---------------- static mode: frames ----------------
 extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const float *frames_in, int32_t num_frames,
                                           float *frames_out, void *stream) {
@@ -1035,6 +1200,7 @@ extern "C" void alsub_mesh_destroy(alsub_mesh *m) {
     if (m->gexec) cudaGraphExecDestroy(m->gexec);
     m->gexec = nullptr;
     free_list(m, m->mem_frames, s);
+    free_list(m, m->mem_rm, s);
     free_list(m, m->mem_plan, s);
     free_list(m, m->mem_create, s);
     cudaStreamSynchronize(s);

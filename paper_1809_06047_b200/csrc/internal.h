@@ -140,6 +140,18 @@ size_t build0_scratch_bytes(int32_t V, int32_t S);
 // refine: add the level-0 work arrays / scan regions to z (one k_zero launch instead of memsets)
 void build0_zero_segments(Build0 &b, ZeroSegs &z);
 
+// ---- refinement matrix R (rmatrix.cu, NEXT-1) ----
+constexpr int kRmLanes = 32;  // frames per SpMM batch (= lanes)
+void rm_owner(const int32_t *face_vtx, int32_t FL, int order, int shift, const int32_t *slot_face, int32_t *owner,
+              cudaStream_t s, Launches &L);
+void rm_probes(int32_t V0, const int32_t *colour, int32_t nprobe, float *out, cudaStream_t s, Launches &L);
+void rm_assemble(int32_t VL, const int32_t *owner, const int32_t *sup_off, const int32_t *sup, const int32_t *colour,
+                 const float *probe, int64_t probe_stride, bool fill, int32_t *row_len, const int32_t *row_off,
+                 int2 *ent, cudaStream_t s, Launches &L);
+void rm_interleave(const float *in, int32_t V0, int32_t nb, float *out, cudaStream_t s, Launches &L);
+void rm_spmm(int32_t VL, const int32_t *row_off, const int2 *ent, const float *P0i, int32_t nb, float *out,
+             cudaStream_t s, Launches &L);
+
 // ---- selective subdivision: extraction (extract.cu) ----
 struct ExSrcHost {
     int32_t V, F, S, order;  // order 3 / 4 (face r = slots [order r, ...)) or 0 (face_off)
