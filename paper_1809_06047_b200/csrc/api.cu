@@ -263,22 +263,16 @@ static alsub_status create_impl(const int32_t *face_off, const int32_t *face_vtx
     b.crease_lenient = lenient ? 1 : 0;
     b.face_off = m->in_face_off; b.face_vtx = m->in_face_vtx; b.crease_in = m->in_crease; b.sigma_in = m->in_sigma;
     b.slot_face = A<int32_t>(m, S0, s, ML, ok);
-    b.sort_k = A<int32_t>(m, S0, s, ML, ok);
-    b.sort_v = A<int32_t>(m, S0, s, ML, ok);
-    b.sort_k2 = A<int32_t>(m, S0, s, ML, ok);
-    b.sort_v2 = A<int32_t>(m, S0, s, ML, ok);
+    b.vtx_slot = A<int32_t>(m, S0, s, ML, ok);
     b.vtx_off = A<int32_t>(m, (int64_t)num_verts + 1, s, ML, ok);
-    b.vtx_slot = b.sort_v;  // the radix sort's value output is M^T's row index array
     b.vtx_cnt = A<int32_t>(m, (int64_t)num_verts + 1, s, ML, ok);
-    b.digits = A<int32_t>(m, 4 * 256, s, ML, ok);
     b.edge_cnt = A<int32_t>(m, num_verts, s, ML, ok);
     b.edge_off = A<int32_t>(m, num_verts, s, ML, ok);
     b.face_edge = A<int32_t>(m, S0, s, ML, ok);
     b.face_twin = A<int32_t>(m, S0, s, ML, ok);
     b.vtx_slot0 = A<int32_t>(m, num_verts, s, ML, ok);
     b.vbnd = A<int32_t>(m, num_verts, s, ML, ok);
-    b.v_mark = A<int32_t>(m, num_verts, s, ML, ok);
-    b.v_idx = A<int32_t>(m, num_verts, s, ML, ok);
+    b.vtx_cur = A<int32_t>(m, num_verts, s, ML, ok);
     b.flags = A<int32_t>(m, 8, s, ML, ok);
     b.scalars = A<int32_t>(m, 8, s, ML, ok);
     m->scratch_bytes = build0_scratch_bytes(num_verts, S0);

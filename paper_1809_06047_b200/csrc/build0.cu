@@ -18,47 +18,52 @@
 
 namespace alsub {
 
-using T0 = Topo<0>;
 
 // a1 + the inputs of a2: validation, slot -> face, the (vertex, slot) sort input, the row
 // lengths of M^T (vertex valences n = M 1, Eq. vo) and the digit histograms of every radix pass.
 __global__ void __launch_bounds__(kThreads) k_b0_prep(const int32_t *__restrict__ face_off,
                                                     const int32_t *__restrict__ face_vtx, int32_t F, int32_t V,
-                                                    int passes, int32_t *__restrict__ slot_face,
-                                                    int32_t *__restrict__ sk, int32_t *__restrict__ sv,
-                                                    int32_t *__restrict__ vtx_cnt, int32_t *__restrict__ digits,
+                                                    int32_t *__restrict__ slot_face, int32_t *__restrict__ vtx_cnt,
                                                     int32_t *flags) {
     ALSUB_GRID_WAIT();
-    __shared__ int h[4][256];
-    for (int p = 0; p < passes; ++p) h[p][threadIdx.x] = 0;
-    __syncthreads();
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < F) {
-        const int32_t o = face_off[r], c = face_off[r + 1] - o;
-        if (c < 3) atomicOr(flags, kFlagMesh);
-        for (int32_t t = 0; t < c; ++t) {
-            int32_t v = face_vtx[o + t];
-            slot_face[o + t] = r;
-            sv[o + t] = o + t;
-            if (v < 0 || v >= V) { atomicOr(flags, kFlagMesh); v = 0; }
-            sk[o + t] = v;
-            atomicAdd(vtx_cnt + v, 1);
-            for (int p = 0; p < passes; ++p) atomicAdd(&h[p][((uint32_t)v >> (8 * p)) & 255u], 1);
-            for (int32_t u = 0; u < t; ++u)
-                if (face_vtx[o + u] == face_vtx[o + t]) atomicOr(flags, kFlagMesh);
-        }
+    if (r >= F) return;
+    const int32_t o = face_off[r], c = face_off[r + 1] - o;
+    if (c < 3) atomicOr(flags, kFlagMesh);
+    for (int32_t t = 0; t < c; ++t) {
+        const int32_t v = face_vtx[o + t];
+        slot_face[o + t] = r;
+        if (v < 0 || v >= V) { atomicOr(flags, kFlagMesh); continue; }
+        atomicAdd(vtx_cnt + v, 1);
+        for (int32_t u = 0; u < t; ++u)
+            if (face_vtx[o + u] == v) atomicOr(flags, kFlagMesh);
     }
-    __syncthreads();
-    for (int p = 0; p < passes; ++p)
-        if (h[p][threadIdx.x]) atomicAdd(digits + 256 * p + threadIdx.x, h[p][threadIdx.x]);
+}
+
+// a2: M^T by a counting sort -- the histogram is the row lengths (prep), their scan the row
+// offsets, and every slot is scattered into its vertex's row through a per-row cursor.  The rows
+// come out in arbitrary order; k_edge_count sorts each one by slot (ascending, as a stable sort by
+// vertex would leave them) before anything reads them.
+__global__ void __launch_bounds__(kThreads) k_b0_scatter(const int32_t *__restrict__ face_vtx, int32_t S, int32_t V,
+                                                       const int32_t *__restrict__ vtx_off,
+                                                       int32_t *__restrict__ cur, int32_t *__restrict__ vtx_slot) {
+    ALSUB_GRID_WAIT();
+    const int32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= S) return;
+    const int32_t v = __ldg(face_vtx + h);
+    if (v < 0 || v >= V) return;
+    vtx_slot[vtx_off[v] + atomicAdd(cur + v, 1)] = h;
 }
 
 // Candidate q of vertex j's collision list: slot vtx_slot[o0 + q/2], neighbour next (q even) or prev.
+// NC = false: the rows were written earlier in the same kernel (k_edge_count sorts them), so they
+// are read through L1 rather than the read-only path
+template <int ORDER, bool NC = true>
 struct Cand {
     const int32_t *face_vtx, *vtx_slot;
-    T0 tp;
+    Topo<ORDER> tp;
     int32_t o0;
-    ALSUB_D int32_t slot(int32_t q) const { return __ldg(vtx_slot + o0 + (q >> 1)); }
+    ALSUB_D int32_t slot(int32_t q) const { return NC ? __ldg(vtx_slot + o0 + (q >> 1)) : vtx_slot[o0 + (q >> 1)]; }
     ALSUB_D int32_t vert(int32_t q) const {
         int32_t h = slot(q);
         return __ldg(face_vtx + ((q & 1) ? tp.prev(h) : tp.next(h)));
@@ -82,10 +87,11 @@ struct WarpCand {
     unsigned peers;
 };
 
-ALSUB_D WarpCand warp_cand(const int32_t *face_vtx, const int32_t *vtx_slot, T0 tp, int32_t o0, int32_t n, int lane) {
+template <int ORDER, bool NC = true>
+ALSUB_D WarpCand warp_cand(const int32_t *face_vtx, const int32_t *vtx_slot, Topo<ORDER> tp, int32_t o0, int32_t n, int lane) {
     WarpCand c{INT32_MAX, -1, false, 0u};
     if (lane < 2 * n) {
-        const int32_t h = __ldg(vtx_slot + o0 + (lane >> 1));
+        const int32_t h = NC ? __ldg(vtx_slot + o0 + (lane >> 1)) : vtx_slot[o0 + (lane >> 1)];
         if (lane & 1) {
             const int32_t hp = tp.prev(h);
             c.x = __ldg(face_vtx + hp);
@@ -102,21 +108,36 @@ ALSUB_D WarpCand warp_cand(const int32_t *face_vtx, const int32_t *vtx_slot, T0 
 
 // symbolic pass: number of distinct neighbours i < j of vertex j (non-zeros of E's column j above
 // the diagonal)
+template <int ORDER>
 __global__ void k_edge_count(const int32_t *__restrict__ face_vtx, const int32_t *__restrict__ vtx_off,
-                             const int32_t *__restrict__ vtx_slot, T0 tp, int32_t V, int32_t *__restrict__ cnt) {
+                             const int32_t *vtx_slot, Topo<ORDER> tp, int32_t V, int32_t *__restrict__ cnt) {
     ALSUB_GRID_WAIT();
     const int32_t j = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (j >= V) return;
     const int32_t o0 = vtx_off[j], n = vtx_off[j + 1] - o0;
+    int32_t *row = const_cast<int32_t *>(vtx_slot) + o0;
     if (n <= 16) {
-        const WarpCand c = warp_cand(face_vtx, vtx_slot, tp, o0, n, lane);
+        // sort the row by slot: lane q moves its slot to its rank (slots are distinct)
+        const int32_t sq = lane < n ? row[lane] : INT32_MAX;
+        int32_t rank = 0;
+        for (int p = 0; p < 16; ++p) rank += __shfl_sync(0xffffffffu, sq, p) < sq;
+        __syncwarp();
+        if (lane < n) row[rank] = sq;
+        __syncwarp();
+        const WarpCand c = warp_cand<ORDER, false>(face_vtx, vtx_slot, tp, o0, n, lane);
         const unsigned b = __ballot_sync(0xffffffffu, c.first && c.x < j);
         if (lane == 0) cnt[j] = __popc(b);
         return;
     }
     if (lane != 0) return;
-    Cand cd{face_vtx, vtx_slot, tp, o0};
+    for (int32_t a = 1; a < n; ++a) {  // long rows: insertion sort on one lane
+        const int32_t x = row[a];
+        int32_t b = a - 1;
+        while (b >= 0 && row[b] > x) { row[b + 1] = row[b]; --b; }
+        row[b + 1] = x;
+    }
+    Cand<ORDER, false> cd{face_vtx, vtx_slot, tp, o0};
     int32_t k = 0;
     for (int32_t q = 0; q < 2 * n; ++q) {
         int32_t x = cd.vert(q);
@@ -141,8 +162,9 @@ ALSUB_D void emit_edge(int32_t e, int32_t s_ij, int32_t s_ji, int32_t i, int32_t
 }
 
 // numeric pass: ids, F(i,j) / F(j,i) as twin slots, multiplicity checks, boundary bits
+template <int ORDER>
 __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t *__restrict__ vtx_off,
-                            const int32_t *__restrict__ vtx_slot, T0 tp, int32_t V,
+                            const int32_t *__restrict__ vtx_slot, Topo<ORDER> tp, int32_t V,
                             const int32_t *__restrict__ edge_off, int32_t *__restrict__ face_edge,
                             int32_t *__restrict__ face_twin, int2 *__restrict__ edge_hh,
                             uint32_t *__restrict__ bnd_word, int32_t *__restrict__ vbnd,
@@ -157,7 +179,7 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
         const WarpCand c = warp_cand(face_vtx, vtx_slot, tp, o0, n, lane);
         const bool mine = c.first && c.x < j;
         int32_t rank = 0;
-        for (int k = 0; k < 32; ++k) {
+        for (int k = 0; k < 2 * n; ++k) {  // candidates live in lanes < 2n (n is warp-uniform)
             const int32_t xk = __shfl_sync(0xffffffffu, c.x, k);
             const unsigned b = __ballot_sync(0xffffffffu, c.first && c.x < xk);
             if (lane == k) rank = __popc(b);
@@ -175,7 +197,7 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
         return;
     }
     if (lane != 0) return;
-    Cand cd{face_vtx, vtx_slot, tp, o0};
+    Cand<ORDER> cd{face_vtx, vtx_slot, tp, o0};
     const int32_t nq = 2 * n;
     for (int32_t q = 0; q < nq; ++q) {
         int32_t i = cd.vert(q);
@@ -199,8 +221,9 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
 
 // a vertex whose interior faces form a closed fan that misses some incident face is non-manifold
 // (reading R18); open fans (bowties) are allowed and end up as corners.
+template <int ORDER>
 __global__ void k_check_fans(const int32_t *__restrict__ face_twin, const int32_t *__restrict__ vtx_off,
-                             const int32_t *__restrict__ slot0, T0 tp, int32_t V, int32_t *flags) {
+                             const int32_t *__restrict__ slot0, Topo<ORDER> tp, int32_t V, int32_t *flags) {
     ALSUB_GRID_WAIT();
     int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= V) return;
@@ -229,12 +252,13 @@ __global__ void k_check_fans(const int32_t *__restrict__ face_twin, const int32_
 // ------------------------------------------------------------------------------------------
 // crease matrix C: pairs -> edge ids and the special flags (boundary = inf crease,
 // reading R6); also the popcounts of the boundary words
+template <int ORDER>
 __global__ void __launch_bounds__(kThreads) k_b0_flags(const int32_t *__restrict__ crease, const float *__restrict__ sigma,
                                                      int32_t K, const int32_t *__restrict__ face_vtx,
                                                      const int32_t *__restrict__ vtx_off,
                                                      const int32_t *__restrict__ vtx_slot,
                                                      const int32_t *__restrict__ face_edge, const int2 *__restrict__ edge_hh,
-                                                     T0 tp, int32_t V, int32_t E, const uint32_t *__restrict__ bnd_word,
+                                                     Topo<ORDER> tp, int32_t V, int32_t E, const uint32_t *__restrict__ bnd_word,
                                                      int32_t nw, float *__restrict__ edge_sigma,
                                                      int32_t *__restrict__ edge_cidx, int32_t *__restrict__ flag,
                                                      int32_t *__restrict__ wcnt, int32_t *flags, int32_t lenient) {
@@ -281,10 +305,11 @@ __global__ void __launch_bounds__(kThreads) k_b0_flags(const int32_t *__restrict
 }
 
 // special-edge list in ascending edge id (compaction by the scanned flags) + list lengths
+template <int ORDER>
 __global__ void __launch_bounds__(kThreads) k_b0_special(const int2 *__restrict__ edge_hh, const int32_t *__restrict__ face_vtx,
                                                        const float *__restrict__ edge_sigma,
                                                        const int32_t *__restrict__ flag, const int32_t *__restrict__ off,
-                                                       T0 tp, int32_t E, SpEdge *__restrict__ sp,
+                                                       Topo<ORDER> tp, int32_t E, SpEdge *__restrict__ sp,
                                                        int32_t *__restrict__ sv_cnt, uint32_t *__restrict__ spw,
                                                        int32_t *__restrict__ spwpre) {
     ALSUB_GRID_WAIT();
@@ -344,31 +369,20 @@ __global__ void __launch_bounds__(kThreads) k_b0_svsort(int32_t V, const int32_t
 }
 
 // ------------------------------------------------------------------------------------------
-static int bits_for(int32_t V) {
-    int bits = 1;
-    while (bits < 31 && (1ll << bits) < (long long)V) ++bits;
-    return bits;
-}
-
-static int passes_for(int32_t V) { return (bits_for(V) + 7) / 8; }
-
-// scratch arena: [one-sweep statuses | 5 scan status regions], each region 256-byte aligned, so a
-// single k_zero launch can initialise all of them for a refine
+// scratch arena: 5 scan status regions, each 256-byte aligned, so a single k_zero launch can
+// initialise all of them for a refine
 static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 static size_t region_bytes(int32_t V, int32_t S) { return al(scan_scratch_bytes(std::max(V, S) + 1)); }
 static void *region(const Build0 &b, int k) {
     if (!b.zeroed) return b.scratch;  // create: one region reused (memset before every use)
-    const size_t os = al(onesweep_scratch_bytes(b.S, passes_for(b.V)));
-    return (char *)b.scratch + (k == 0 ? 0 : os + (size_t)(k - 1) * region_bytes(b.V, b.S));
+    return (char *)b.scratch + (size_t)(k - 1) * region_bytes(b.V, b.S);
 }
-size_t build0_scratch_bytes(int32_t V, int32_t S) {
-    return al(onesweep_scratch_bytes(S, passes_for(V))) + 5 * region_bytes(V, S);
-}
+size_t build0_scratch_bytes(int32_t V, int32_t S) { return 5 * region_bytes(V, S); }
 
 void build0_zero_segments(Build0 &b, ZeroSegs &z) {
     const int32_t E = b.E, nw = (int32_t)ceil_div(E > 0 ? E : 1, 32);
     z.add(b.vtx_cnt, (int64_t)b.V + 1);
-    z.add(b.digits, 256 * 4);
+    z.add(b.vtx_cur, b.V);
     z.add(b.scalars + 1, 3);
     z.add(b.bnd_word, nw);
     z.add(b.vbnd, b.V);
@@ -381,35 +395,39 @@ void build0_zero_segments(Build0 &b, ZeroSegs &z) {
     b.zeroed = true;
 }
 
-// a1: validation + sort input + M^T row lengths + radix digit histograms
+// a1: validation + M^T row lengths
 void build0_validate(Build0 &b, cudaStream_t s, Launches &L) {
-    if (!b.zeroed) {
-        cudaMemsetAsync(b.vtx_cnt, 0, sizeof(int32_t) * ((size_t)b.V + 1), s);
-        cudaMemsetAsync(b.digits, 0, sizeof(int32_t) * 256 * 4, s);
-    }
-    if (b.F > 0) {
-        launch(L, "b0_prep", k_b0_prep, dim3(grid_for(b.F)), dim3(kThreads), 0, s, b.face_off, b.face_vtx, b.F, b.V, passes_for(b.V), b.slot_face,
-                                                     b.sort_k, b.sort_v, b.vtx_cnt, b.digits, b.flags);
-    }
+    if (!b.zeroed) cudaMemsetAsync(b.vtx_cnt, 0, sizeof(int32_t) * ((size_t)b.V + 1), s);
+    if (b.F > 0)
+        launch(L, "b0_prep", k_b0_prep, dim3(grid_for(b.F)), dim3(kThreads), 0, s, b.face_off, b.face_vtx, b.F, b.V,
+               b.slot_face, b.vtx_cnt, b.flags);
 }
 
-// a2 + symbolic a3: M^T (run lengths scanned into vtx_off, slots sorted by vertex with the
-// one-sweep radix sort -> vtx_slot aliases sort_v), then the per-vertex upper-triangle counts of E
-void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L) {
-    T0 tp{b.face_off, b.slot_face};
+// a2 + symbolic a3: M^T (row lengths scanned into vtx_off, slots scattered into their rows, rows
+// sorted inside k_edge_count), then the per-vertex upper-triangle counts of E
+template <int ORDER>
+static void count_edges(Build0 &b, cudaStream_t s, Launches &L) {
+    const Topo<ORDER> tp{b.face_off, b.slot_face};
     scan_exclusive(b.vtx_cnt, b.vtx_off, (int64_t)b.V + 1, nullptr, region(b, 1), s, L, b.zeroed);
-    radix_sort_onesweep(b.sort_k, b.sort_v, b.sort_k2, b.sort_v2, b.S, bits_for(b.V), b.digits, true, region(b, 0), s,
-                        L, b.zeroed);
-    if (b.V > 0) {
-        launch(L, "b0_edge_count", k_edge_count, dim3(grid_for(32 * (int64_t)b.V)), dim3(kThreads), 0, s, b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
-                                                                        b.edge_cnt);
-    }
+    if (!b.zeroed && b.V > 0) cudaMemsetAsync(b.vtx_cur, 0, sizeof(int32_t) * b.V, s);
+    if (b.S > 0)
+        launch(L, "b0_scatter", k_b0_scatter, dim3(grid_for(b.S)), dim3(kThreads), 0, s, b.face_vtx, b.S, b.V, b.vtx_off,
+               b.vtx_cur, b.vtx_slot);
+    if (b.V > 0)
+        launch(L, "b0_edge_count", k_edge_count<ORDER>, dim3(grid_for(32 * (int64_t)b.V)), dim3(kThreads), 0, s, b.face_vtx,
+               b.vtx_off, b.vtx_slot, tp, b.V, b.edge_cnt);
     scan_exclusive(b.edge_cnt, b.edge_off, b.V, b.scalars + 0, region(b, 2), s, L, b.zeroed);
+}
+void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L) {
+    if (b.order == 3) count_edges<3>(b, s, L);
+    else if (b.order == 4) count_edges<4>(b, s, L);
+    else count_edges<0>(b, s, L);
 }
 
 // numeric a3 + crease matrix + special lists
-void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
-    T0 tp{b.face_off, b.slot_face};
+template <int ORDER>
+static void fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
+    const Topo<ORDER> tp{b.face_off, b.slot_face};
     const int32_t E = b.E;
     const int32_t nw = (int32_t)ceil_div(E > 0 ? E : 1, 32);
     if (!b.zeroed) {
@@ -418,12 +436,12 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
         if (b.V > 0) cudaMemsetAsync(b.vbnd, 0, sizeof(int32_t) * b.V, s);
     }
     if (b.V > 0) {
-        launch(L, "b0_edge_fill", k_edge_fill, dim3(grid_for(32 * (int64_t)b.V)), dim3(kThreads), 0, s, b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
+        launch(L, "b0_edge_fill", k_edge_fill<ORDER>, dim3(grid_for(32 * (int64_t)b.V)), dim3(kThreads), 0, s, b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.V,
                                                                        b.edge_off, b.face_edge, b.face_twin, b.edge_hh,
                                                                        b.bnd_word, b.vbnd, b.scalars, b.flags,
                                                                        b.vtx_slot0);
         if (check_fans) {
-            launch(L, "b0_check_fans", k_check_fans, dim3(grid_for(b.V)), dim3(kThreads), 0, s, b.face_twin, b.vtx_off, b.vtx_slot0, tp, b.V, b.flags);
+            launch(L, "b0_check_fans", k_check_fans<ORDER>, dim3(grid_for(b.V)), dim3(kThreads), 0, s, b.face_twin, b.vtx_off, b.vtx_slot0, tp, b.V, b.flags);
         }
     }
     if (E > 0 && !b.zeroed) {
@@ -437,13 +455,13 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     }
     if (b.zeroed && b.no_special) return;  // closed and crease-free: no special lists, no boundary words
     const int64_t nf = std::max<int64_t>(std::max<int64_t>(E, 32 * (int64_t)b.K_in), nw);
-    launch(L, "b0_flags", k_b0_flags, dim3(grid_for(nf)), dim3(kThreads), 0, s, b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
+    launch(L, "b0_flags", k_b0_flags<ORDER>, dim3(grid_for(nf)), dim3(kThreads), 0, s, b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
                                                  b.face_edge, b.edge_hh, tp, b.V, E, b.bnd_word, nw, b.edge_sigma,
                                                  b.edge_cidx, b.sp_flag, b.bnd_wcnt, b.flags, b.crease_lenient);
     scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, region(b, 3), s, L, b.zeroed);
     scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, region(b, 4), s, L, b.zeroed);
     if (E > 0) {
-        launch(L, "b0_special", k_b0_special, dim3(grid_for(E)), dim3(kThreads), 0, s, b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp, E,
+        launch(L, "b0_special", k_b0_special<ORDER>, dim3(grid_for(E)), dim3(kThreads), 0, s, b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp, E,
                                                       b.sp, b.sv_cnt, b.spw, b.spwpre);
     }
     scan_exclusive(b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V, region(b, 5), s, L, b.zeroed);
@@ -453,6 +471,12 @@ void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     if (b.V > 0) {
         launch(L, "b0_sv_sort", k_b0_svsort, dim3(grid_for(b.V)), dim3(kThreads), 0, s, b.V, b.sv_off, b.sv_list, b.sv_vtx, b.scalars);
     }
+}
+
+void build0_fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
+    if (b.order == 3) fill<3>(b, check_fans, s, L);
+    else if (b.order == 4) fill<4>(b, check_fans, s, L);
+    else fill<0>(b, check_fans, s, L);
 }
 
 }  // namespace alsub

@@ -109,10 +109,9 @@ struct Build0 {
     const float *sigma_in;
     // outputs / work
     int32_t *slot_face;           // [S] (all orders: used for validation & mixed topology)
-    int32_t *sort_k, *sort_v, *sort_k2, *sort_v2;  // [S]
-    int32_t *vtx_off, *vtx_slot;  // [V+1], [S] (M^T in CSR; vtx_slot aliases sort_v)
+    int32_t *vtx_off, *vtx_slot;  // [V+1], [S] (M^T in CSR, rows ascending by slot)
     int32_t *vtx_cnt;             // [V+1] row lengths of M^T
-    int32_t *digits;              // [4][256] radix digit histograms
+    int32_t *vtx_cur;             // [V] scatter cursors of the M^T counting sort
     int32_t *edge_cnt, *edge_off; // [V], [V]
     int32_t *face_edge, *face_twin, *vtx_slot0;  // [S], [S], [V]
     int2 *edge_hh;                // [E] (smallest slot of the edge, the other slot or -1)
@@ -122,7 +121,6 @@ struct Build0 {
     float *edge_sigma;            // [E]
     int32_t *edge_cidx;           // [E] crease index claiming the edge, -1
     int32_t *sp_flag, *sp_off;    // [E]
-    int32_t *v_mark, *v_idx;      // [V]
     SpEdge *sp;                   // [cap] special edges
     int32_t *sv_vtx;              // [cap] special vertices
     int32_t *sv_cnt, *sv_off, *sv_cur, *sv_list;  // special-vertex CSR (level 0)
