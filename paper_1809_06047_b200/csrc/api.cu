@@ -528,7 +528,7 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     L.side = m->side_stream;
     L.ev_fork = m->ev_fork;
     L.ev_join = m->ev_join;
-    // a1-a3: level-0 mesh matrix, M^T by radix sort, edge index, creases
+    // a1-a3: level-0 mesh matrix, M^T by counting sort, edge index, creases
     L.level = -1;
     {
         ZeroSegs z;

@@ -1,8 +1,8 @@
 // build0.cu -- level-0 topology from arbitrary face lists.
 //
 // a1  mesh matrix M (CSC: face_off / face_vtx) + validation
-// a2  M^T by a stable device radix sort of (vertex, slot) pairs + run-length offsets;
-//     vertex valence n = M 1 (Eq. vo) = row length
+// a2  M^T by a counting sort of the slots by vertex (histogram = row lengths, scan, scatter, rows
+//     sorted by slot); vertex valence n = M 1 (Eq. vo) = row length
 // a3  the implicit mapped SpGEMMs E = M M^T {Q_c + Q_c^{c-1}}[lambda] and F = M M^T {Q_c}[gamma]
 //      evaluated as in the paper's implicit SpGEMM: every collision of
 //     vertex j with its face neighbours next(h) = Q_c and prev(h) = Q_c^{c-1} is visited from j's
@@ -19,8 +19,8 @@
 namespace alsub {
 
 
-// a1 + the inputs of a2: validation, slot -> face, the (vertex, slot) sort input, the row
-// lengths of M^T (vertex valences n = M 1, Eq. vo) and the digit histograms of every radix pass.
+// a1 + the input of a2: validation, slot -> face and the row
+// lengths of M^T (vertex valences n = M 1, Eq. vo).
 __global__ void __launch_bounds__(kThreads) k_b0_prep(const int32_t *__restrict__ face_off,
                                                     const int32_t *__restrict__ face_vtx, int32_t F, int32_t V,
                                                     int32_t *__restrict__ slot_face, int32_t *__restrict__ vtx_cnt,

@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
 // S(p) = (1 - 2/n) p + 1/n^2 sum_{incident slots x} (p_{v(next(x))} + f_{face(x)})
 // (Eq. pos_update split: s2 = F P and s3 = M f as gathers over M's row of p).
 // The row of M of a level-l vertex is closed-form from the level it was born at (VSegs):
-//   level-0 vertex v : 4^l x its level-0 slots (M^T from the radix sort)
+//   level-0 vertex v : 4^l x its level-0 slots (M^T from the counting sort)
 //   face point of face r of level m-1 : 4^(l-m) x {4 (off_r + t) + 2}
 //   edge point of edge (h, tw) of level m-1 : 4^(l-m) x {4h+1, 4 next(h)+3, 4tw+1, 4 next(tw)+3}
 // so no twin walk (no dependent chain) is needed; all loads of a vertex are issued together.

@@ -84,21 +84,6 @@ void zero_segments(const ZeroSegs &z, cudaStream_t s, Launches &L);
 // [V][C] vertex channels <-> ceil(C/3) frames of [V][3] (alsub_eval_attributes)
 void pack_channels(const float *in, int64_t V, int32_t C, float *out, cudaStream_t s, Launches &L);
 void unpack_channels(const float *in, int64_t V, int32_t C, float *out, cudaStream_t s, Launches &L);
-// LSD radix sort of (key, value) int32 pairs, keys in [0, 2^bits).  Stable.  Result in
-// keys/vals; keys_alt/vals_alt are ping-pong buffers of n entries.
-size_t sort_scratch_bytes(int64_t n);
-void radix_sort_pairs(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *vals_alt, int64_t n,
-                      int bits, void *scratch, cudaStream_t s, Launches &L);
-// One-sweep LSD radix sort (one kernel per 8-bit pass, decoupled look-back per digit).
-// counts = [passes][256] digit histograms (computed here unless counts_ready).  Result in
-// keys/vals when the number of passes is even, else copied back.
-size_t onesweep_scratch_bytes(int64_t n, int passes);
-void radix_sort_onesweep(int32_t *keys, int32_t *vals, int32_t *keys_alt, int32_t *vals_alt, int64_t n, int bits,
-                         int32_t *counts, bool counts_ready, void *scratch, cudaStream_t s, Launches &L,
-                         bool prezeroed = false);
-// CSR offsets of sorted keys: off[v] = first i with key[i] >= v, v in [0, nkeys] (run-length).
-void offsets_from_sorted(const int32_t *keys, int64_t n, int32_t *off, int32_t nkeys, cudaStream_t s,
-                         Launches &L);
 
 // ---------------- level-0 build (build0.cu) ----------------
 struct Build0 {
