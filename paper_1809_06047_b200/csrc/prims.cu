@@ -78,25 +78,35 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t *__restrict
     __syncthreads();
     const int block_total = s_warp[kScanThreads / 32 - 1];
     int excl = incl - sum + (warp > 0 ? s_warp[warp - 1] : 0);
-    if (tid == 0) {
+    if (warp == 0) {
+        // warp-wide look-back: lane l inspects predecessor tile - 1 - l (32 status words per round)
         long long prefix = 0;
         if (tile == 0) {
-            atomicExch(&stat[0], kStatInc | (unsigned long long)block_total);
+            if (lane == 0) atomicExch(&stat[0], kStatInc | (unsigned long long)block_total);
         } else {
-            atomicExch(&stat[tile], kStatAgg | (unsigned long long)block_total);
-            int p = tile - 1;
+            if (lane == 0) atomicExch(&stat[tile], kStatAgg | (unsigned long long)block_total);
+            int p0 = tile - 1;
             while (true) {
-                unsigned long long w;
-                do {
-                    w = atomicAdd(&stat[p], 0ull);
-                } while ((w >> 62) == 0);
-                prefix += (long long)(w & kStatMask);
-                if ((w >> 62) == 2) break;
-                --p;
+                const int p = p0 - lane;
+                unsigned long long w = 0;
+                if (p >= 0) {
+                    do {
+                        w = *(volatile unsigned long long *)&stat[p];
+                    } while ((w >> 62) == 0);
+                }
+                // nearest inclusive predecessor among the 32 (tile 0 is always inclusive)
+                const unsigned inc = __ballot_sync(0xffffffffu, p >= 0 && (w >> 62) == 2);
+                const int stop = inc ? __ffs(inc) - 1 : 31;
+                long long v = (p >= 0 && lane <= stop) ? (long long)(w & kStatMask) : 0;
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+                prefix += v;
+                if (inc) break;
+                p0 -= 32;
             }
-            atomicExch(&stat[tile], kStatInc | (unsigned long long)(prefix + block_total));
+            if (lane == 0) atomicExch(&stat[tile], kStatInc | (unsigned long long)(prefix + block_total));
         }
-        s_prefix = prefix;
+        if (lane == 0) s_prefix = prefix;
     }
     __syncthreads();
     int run = (int)s_prefix + excl;
