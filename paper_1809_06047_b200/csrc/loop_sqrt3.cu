@@ -221,17 +221,30 @@ void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool top
                 cudaStream_t s, Launches &L) {
     (void)scratch;
     const bool A = adj && topo;
+    // face (topology), edge and vertex kernels only read level-l data: the edge kernel runs as a
+    // parallel branch next to face -> vertex
+    const bool fork = L.can_fork();
+    cudaStream_t se = s;
+    if (fork) {
+        cudaEventRecord(L.ev_fork, s);
+        cudaStreamWaitEvent(L.side, L.ev_fork, 0);
+        se = L.side;
+    }
     if (topo && p.F > 0) {
         if (A) launch(L, "loop_face", k_loop_face<true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c);
         else launch(L, "loop_face", k_loop_face<false>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c);
     }
     if (p.E > 0) {
-        if (A) launch(L, "loop_edge", k_loop_edge<true>, dim3(grid_for(p.E)), dim3(kThreads), 0, s, p, c, fr);
-        else launch(L, "loop_edge", k_loop_edge<false>, dim3(grid_for(p.E)), dim3(kThreads), 0, s, p, c, fr);
+        if (A) launch(L, "loop_edge", k_loop_edge<true>, dim3(grid_for(p.E)), dim3(kThreads), 0, se, p, c, fr);
+        else launch(L, "loop_edge", k_loop_edge<false>, dim3(grid_for(p.E)), dim3(kThreads), 0, se, p, c, fr);
     }
     if (p.V > 0) {
         if (A) launch(L, "loop_vertex", k_loop_vertex<true>, dim3(grid_for(p.V)), dim3(kThreads), 0, s, p, c, fr);
         else launch(L, "loop_vertex", k_loop_vertex<false>, dim3(grid_for(p.V)), dim3(kThreads), 0, s, p, c, fr);
+    }
+    if (fork) {
+        cudaEventRecord(L.ev_join, L.side);
+        cudaStreamWaitEvent(s, L.ev_join, 0);
     }
 }
 
@@ -394,6 +407,16 @@ void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool to
                  cudaStream_t s, Launches &L) {
     const bool A = adj && topo;
     const bool one = fr.nb == 1;
+    // the vertex kernel reads only level-l positions and writes the old vertices, the face kernel
+    // the new face points: independent, so they run as parallel branches (gather-bound vertex
+    // kernel next to the bandwidth-bound face kernel)
+    const bool fork = L.can_fork();
+    cudaStream_t sv = s;
+    if (fork) {
+        cudaEventRecord(L.ev_fork, s);
+        cudaStreamWaitEvent(L.side, L.ev_fork, 0);
+        sv = L.side;
+    }
     if (p.F > 0) {
         if (A) {
             if (one) launch(L, "s3_face", k_s3_face<true, 1>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo);
@@ -406,8 +429,12 @@ void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool to
     if (p.V > 0) {
         const unsigned nblk = (unsigned)std::max<int64_t>(grid_for(p.V, 4 * kThreads),
                                                           std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
-        if (one) launch(L, "s3_vertex", k_s3_vertex<1>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
-        else launch(L, "s3_vertex", k_s3_vertex<0>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g);
+        if (one) launch(L, "s3_vertex", k_s3_vertex<1>, dim3(nblk), dim3(kThreads), 0, sv, p, fr, g);
+        else launch(L, "s3_vertex", k_s3_vertex<0>, dim3(nblk), dim3(kThreads), 0, sv, p, fr, g);
+    }
+    if (fork) {
+        cudaEventRecord(L.ev_join, L.side);
+        cudaStreamWaitEvent(s, L.ev_join, 0);
     }
 }
 
