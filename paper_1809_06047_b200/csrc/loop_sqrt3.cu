@@ -383,6 +383,10 @@ __global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, V
             list = g.vtx_list0 + o;
         }
         const float alpha = n > 0 ? sqrt3_alpha(n) : 0.0f;
+        // level >= 1: every neighbour of an old vertex is a face point born at this level, the one
+        // of the level-(l-1) face (slot / 9) holding the vertex's level-l slot -- no face lookup
+        const bool closed = g.level >= 1;
+        const int32_t vfp = g.start[g.nseg - 1];  // first face point born at this level (= V_{l-1})
         for (int f = 0; f < nb; ++f) {
             const PR P = fr.rd(f);
             const PW Pn = fr.wr(f);
@@ -390,11 +394,14 @@ __global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, V
             if (n == 0) { st3(Pn, v, pv); continue; }
             P3 acc = p3zero();
             if (list) {
-                for (int32_t k = 0; k < n; ++k) acc = acc + ld3(P, __ldg(p.face_vtx + tri_next(__ldg(list + k) * mult)));
+                for (int32_t k = 0; k < n; ++k) {
+                    const int32_t sk = __ldg(list + k) * mult;
+                    acc = acc + ld3(P, closed ? vfp + sk / 9 : __ldg(p.face_vtx + tri_next(sk)));
+                }
             } else {
                 int32_t nbv[6];
 #pragma unroll
-                for (int k = 0; k < 6; ++k) nbv[k] = __ldg(p.face_vtx + tri_next(sl[k]));
+                for (int k = 0; k < 6; ++k) nbv[k] = closed ? vfp + sl[k] / 9 : __ldg(p.face_vtx + tri_next(sl[k]));
 #pragma unroll
                 for (int k = 0; k < 6; ++k) acc = acc + ld3(P, nbv[k]);
             }
