@@ -26,13 +26,16 @@ def diag_of(mesh):
     return float(np.linalg.norm(p.max(0) - p.min(0)))
 
 
-def compare(mesh, scheme, levels, edges=True, creases=True, oracle_recs=None):
+def compare(mesh, scheme, levels, edges=True, creases=True, oracle_recs=None, graph=False):
     Mesh = _gpu()
     want = oracle_recs or oracle.refine(mesh, scheme, levels)
     diag = diag_of(mesh)
     worst = 0.0
     with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
         m.refine(scheme, levels)
+        if graph:  # bench.py's launch configuration: the CUDA-graph replay (2nd refine on)
+            m.refine(scheme, levels)
+            m.refine(scheme, levels)
         torch.cuda.synchronize()
         for lv in range(levels + 1):
             c = m.counts(lv)
@@ -119,10 +122,35 @@ def test_parity_ico_loop_L6():
 
 
 def test_parity_armor9k_L6_full():
-    """Config 3 at full size (35M faces), same launch configuration as bench.py."""
+    """Config 3 at full size (35M faces), same launch configuration as bench.py (graph replay)."""
     mesh = mg.armor9k()
-    worst = compare(mesh, "cc", 6, edges=False)
+    worst = compare(mesh, "cc", 6, edges=False, graph=True)
     assert worst < TOL
+
+
+def test_parity_torus100k_sqrt3_L5_full():
+    """Config 4 at full size (24.3M faces), graph replay as in bench.py's other_configs."""
+    worst = compare(mg.torus100k(), "sqrt3", 5, edges=False, graph=True)
+    assert worst < TOL
+
+
+def test_parity_config5_frames_sampled():
+    """Config 5 at full size: armor50k CC L4 static eval in bench.py's batches of 8 frames;
+    sampled frames against the oracle refining those frames' positions."""
+    Mesh = _gpu()
+    mesh = mg.armor50k()
+    frames = torch.stack([torch.from_numpy(mg.frame_positions(mesh["pos"], t, 4096)) for t in range(8)]).cuda()
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine("cc", 4)
+        m.refine("cc", 4)
+        out = m.eval_frames(frames, 4)
+        diag = diag_of(mesh)
+        for t in (0, 5):
+            m2 = dict(mesh)
+            m2["pos"] = mg.frame_positions(mesh["pos"], t, 4096)
+            want = oracle.refine(m2, "cc", 4)[-1]["pos"]
+            err = float(np.abs(out[t].cpu().numpy().astype(np.float64) - want).max()) / diag
+            assert err <= TOL, f"frame {t}: {err:.3e}"
 
 
 def test_graph_and_eager_bitwise_equal(monkeypatch):
