@@ -491,3 +491,41 @@ def test_parity_large_creased_grid_unfused_levels():
     mesh["crease"] = np.asarray(pairs, np.int32)
     mesh["sigma"] = np.asarray(sig, np.float32)
     compare(mesh, "cc", 2)
+
+
+def _random_creased_grid(seed):
+    """Seeded fuzz mesh: open grid of random size with random triangle splits, random crease
+    polylines (sigma in {0.5, 1, 2.5, inf}) and jittered positions."""
+    rng = np.random.default_rng(1000 + seed)
+    nx, ny = int(rng.integers(3, 11)), int(rng.integers(3, 11))
+    cells = [(i, j) for i in range(nx) for j in range(ny) if rng.random() < 0.25]
+    g = mg.grid(nx, ny, tri_cells=cells, z=lambda i, j: 0.0, name=f"fuzz{seed}")
+    g["pos"] = (g["pos"] + rng.normal(0, 0.1, g["pos"].shape)).astype(np.float32)
+    vid = lambda i, j: j * (nx + 1) + i
+    creases = {}  # edge -> sigma, first polyline wins
+    for _ in range(int(rng.integers(1, 4))):
+        j = int(rng.integers(1, ny))
+        i0, i1 = sorted(int(x) for x in rng.integers(0, nx + 1, 2))
+        s = float(rng.choice([0.5, 1.0, 2.5, np.inf]))
+        for i in range(i0, i1):
+            creases.setdefault((vid(i, j), vid(i + 1, j)), s)
+    if creases:
+        g["crease"] = np.array(list(creases.keys()), np.int32).reshape(-1, 2)
+        g["sigma"] = np.array(list(creases.values()), np.float32)
+    return g
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fuzz_creased_grids_cc(seed):
+    """Seeded random open meshes with semi-sharp / sharp crease polylines, CC levels 1-3: full
+    topology bit-exact and positions within tolerance at every level."""
+    g = _random_creased_grid(seed)
+    compare(g, "cc", 1 + seed % 3)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fuzz_triangle_tori_loop_sqrt3(seed):
+    rng = np.random.default_rng(2000 + seed)
+    t = mg.torus_tris(int(rng.integers(4, 12)), int(rng.integers(4, 10)), seed=3000 + seed)
+    compare(t, "loop", 1 + seed % 3)
+    compare(t, "sqrt3", 1 + (seed + 1) % 3, edges=False)
