@@ -59,7 +59,7 @@ struct LevelHost {
     int2 *edge_hh = nullptr;
     uint32_t *bnd_word = nullptr;
     int32_t *bnd_wpre = nullptr;
-    int32_t *loop_cnt = nullptr, *loop_base = nullptr;
+    int32_t *loop_stat = nullptr, *loop_base = nullptr;  // Loop: child-edge base scan (status words, bases)
     SpEdge *sp = nullptr;       // special edges of this level [nsp]
     int64_t nsp = 0;            // = 2^l K_0
     int32_t *sv_list = nullptr; // [2 nsp] incident special edges of the special vertices
@@ -450,9 +450,8 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
             }
         }
         if (scheme == ALSUB_LOOP && has_child && (adj || special)) {
-            c.loop_cnt = A<int32_t>(m, c.E, s, ML, ok);
+            c.loop_stat = A<int32_t>(m, (int64_t)(scan_scratch_bytes(c.E) / 4), s, ML, ok);
             c.loop_base = A<int32_t>(m, c.E, s, ML, ok);
-            max_scan = std::max<int64_t>(max_scan, c.E);
         }
     }
     size_t need = std::max(build0_scratch_bytes(m->V0, m->S0), scan_scratch_bytes(max_scan));
@@ -537,6 +536,8 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
             if (m->lv[l].bnd_word) z.add(m->lv[l].bnd_word, ceil_div(m->lv[l].E > 0 ? m->lv[l].E : 1, 32));
             if (m->lv[l].spw) z.add(m->lv[l].spw, ceil_div(m->lv[l].E > 0 ? m->lv[l].E : 1, 32));
         }
+        for (int l = 0; l < levels; ++l)  // Loop child-edge base scans: status words
+            if (m->lv[l].loop_stat) z.add(m->lv[l].loop_stat, (int64_t)(scan_scratch_bytes(m->lv[l].E) / 4));
         zero_segments(z, s, L);
     }
     build0_validate(m->b0, s, L);
@@ -567,7 +568,7 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
             cc_level(p, c, fr, true, adj, g, use_gp ? &gp : nullptr, s, L);
             if (special && !p.crease) crease_level(p, c, fr, (int32_t)(P.V + P.F), 0, true, s, L);
         } else if (scheme == ALSUB_LOOP) {
-            if (adj || special) loop_edge_base(p, P.loop_cnt, P.loop_base, m->scratch, s, L);
+            if (adj || special) loop_edge_base(p, P.loop_stat, P.loop_base, s, L);
             loop_level(p, c, fr, true, adj, m->scratch, s, L);
             if (special) crease_level(p, c, fr, (int32_t)P.V, 1, true, s, L);
         } else {

@@ -70,14 +70,16 @@ inline unsigned grid_for(int64_t n, int threads = kThreads) {
 size_t scan_scratch_bytes(int64_t n);
 void scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *total, void *scratch,
                     cudaStream_t s, Launches &L, bool prezeroed = false);
-// initialise up to 16 int32 arrays in one launch
+// initialise up to kZeroSegs int32 arrays in one launch (the level-0 build's ~11 plus up to 3 per
+// refined level: boundary words, special words, Loop scan status)
+constexpr int kZeroSegs = 64;
 struct ZeroSegs {
     int n = 0;
-    int32_t *ptr[32];
-    int64_t words[32];
-    int32_t value[32];
+    int32_t *ptr[kZeroSegs];
+    int64_t words[kZeroSegs];
+    int32_t value[kZeroSegs];
     void add(void *p, int64_t w, int32_t v = 0) {
-        if (p && w > 0) { ptr[n] = (int32_t *)p; words[n] = w; value[n] = v; ++n; }
+        if (p && w > 0 && n < kZeroSegs) { ptr[n] = (int32_t *)p; words[n] = w; value[n] = v; ++n; }
     }
 };
 void zero_segments(const ZeroSegs &z, cudaStream_t s, Launches &L);
@@ -256,7 +258,7 @@ void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool to
 void crease_level(const LevelDev &p, const ChildDev &c, const Frames &fr, int32_t ep_base, int scheme, bool inherit,
                   cudaStream_t s, Launches &L);
 // Loop child-edge counts -> loop_base (scan); cnt [E] scratch
-void loop_edge_base(const LevelDev &p, int32_t *cnt, int32_t *base, void *scratch, cudaStream_t s, Launches &L);
+void loop_edge_base(const LevelDev &p, int32_t *stat, int32_t *base, cudaStream_t s, Launches &L);
 // topology export helper: edge_vtx / edge_face from the edge pairs
 void export_edges(const LevelDev &p, int32_t *edge_vtx, int32_t *edge_face, cudaStream_t s, Launches &L);
 

@@ -13,6 +13,7 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "scan.cuh"
 
 namespace alsub {
 
@@ -55,31 +56,37 @@ ALSUB_D void other_edges(const int32_t *face_edge, int32_t h, int32_t &x, int32_
     y = __ldg(face_edge + tri_prev(h));
 }
 
-__global__ void __launch_bounds__(kThreads) k_loop_count(LevelDev p, int32_t *__restrict__ cnt) {
-    ALSUB_GRID_WAIT();
-    const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= p.E) return;
-    const int2 hh = __ldg(p.edge_hh + e);
-    const int32_t h = hh.x, tw = hh.y;
-    int32_t n[4];
-    other_edges(p.face_edge, h, n[0], n[1]);
-    n[2] = n[3] = INT32_MAX;
-    if (tw >= 0) other_edges(p.face_edge, tw, n[2], n[3]);
-    int32_t c = 2;
+// child-edge count of parent edge e: its two halves + one inner edge per distinct neighbour edge
+// x < e of its faces; the exclusive scan of these counts is the block base of e's children
+struct LoopCountSrc {
+    LevelDev p;
+    ALSUB_D int32_t operator()(int64_t ei) const {
+        const int32_t e = (int32_t)ei;
+        const int2 hh = __ldg(p.edge_hh + e);
+        const int32_t h = hh.x, tw = hh.y;
+        int32_t n[4];
+        other_edges(p.face_edge, h, n[0], n[1]);
+        n[2] = n[3] = INT32_MAX;
+        if (tw >= 0) other_edges(p.face_edge, tw, n[2], n[3]);
+        int32_t c = 2;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        bool dup = false;
+        for (int i = 0; i < 4; ++i) {
+            bool dup = false;
 #pragma unroll
-        for (int k = 0; k < i; ++k) dup |= (n[k] == n[i]);
-        c += (n[i] < e && !dup);
+            for (int k = 0; k < i; ++k) dup |= (n[k] == n[i]);
+            c += (n[i] < e && !dup);
+        }
+        return c;
     }
-    cnt[e] = c;
-}
+};
 
-void loop_edge_base(const LevelDev &p, int32_t *cnt, int32_t *base, void *scratch, cudaStream_t s, Launches &L) {
+// counts fused into the scan's load phase (one launch); `stat` = scan status words, zeroed by the
+// refine's k_zero
+void loop_edge_base(const LevelDev &p, int32_t *stat, int32_t *base, cudaStream_t s, Launches &L) {
     if (p.E <= 0) return;
-    launch(L, "loop_count", k_loop_count, dim3(grid_for(p.E)), dim3(kThreads), 0, s, p, cnt);
-    scan_exclusive(cnt, base, p.E, nullptr, scratch, s, L);
+    const int64_t tiles = ceil_div(p.E, kScanTile);
+    launch(L, "loop_base", k_scan<LoopCountSrc>, dim3((unsigned)tiles), dim3(kScanThreads), 0, s, LoopCountSrc{p}, base,
+           (int64_t)p.E, reinterpret_cast<unsigned long long *>(stat), (int32_t *)nullptr);
 }
 
 // id of the child edge between ep_x and ep_m inside a face (x < m): base_m + 2 + rank of x among
