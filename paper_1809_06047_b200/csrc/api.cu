@@ -568,8 +568,7 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
             cc_level(p, c, fr, true, adj, g, use_gp ? &gp : nullptr, s, L);
             if (special && !p.crease) crease_level(p, c, fr, (int32_t)(P.V + P.F), 0, true, s, L);
         } else if (scheme == ALSUB_LOOP) {
-            if (adj || special) loop_edge_base(p, P.loop_stat, P.loop_base, s, L);
-            loop_level(p, c, fr, true, adj, m->scratch, s, L);
+            loop_level(p, c, fr, true, adj, P.loop_stat, (adj || special) ? P.loop_base : nullptr, s, L);
             if (special) crease_level(p, c, fr, (int32_t)P.V, 1, true, s, L);
         } else {
             VSegs g = make_segs_s3(m, l);
@@ -900,7 +899,7 @@ static void static_level(alsub_mesh *m, int l, const Frames &fr, cudaStream_t s,
         cc_level(p, c, fr, false, false, g, use_gp ? &gp : nullptr, s, L);
         if (special && !p.crease) crease_level(p, c, fr, (int32_t)(Pl.V + Pl.F), 0, false, s, L);
     } else if (scheme == ALSUB_LOOP) {
-        loop_level(p, c, fr, false, false, m->scratch, s, L);
+        loop_level(p, c, fr, false, false, nullptr, nullptr, s, L);
         if (special) crease_level(p, c, fr, (int32_t)Pl.V, 1, false, s, L);
     } else {
         VSegs g = make_segs_s3(m, l);

@@ -224,30 +224,35 @@ __global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c
     }
 }
 
-void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, void *scratch,
-                cudaStream_t s, Launches &L) {
-    (void)scratch;
+// stat / base: the child-edge base scan of this level (nullptr: not needed -- last level without
+// creases).  Dependencies: face and edge kernels need the bases, the vertex kernel does not, so it
+// starts at once on the side branch and the edge kernel joins it there after the scan.
+void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, int32_t *stat,
+                int32_t *base, cudaStream_t s, Launches &L) {
     const bool A = adj && topo;
-    // face (topology), edge and vertex kernels only read level-l data: the edge kernel runs as a
-    // parallel branch next to face -> vertex
     const bool fork = L.can_fork();
-    cudaStream_t se = s;
+    cudaStream_t sv = s;
     if (fork) {
         cudaEventRecord(L.ev_fork, s);
         cudaStreamWaitEvent(L.side, L.ev_fork, 0);
-        se = L.side;
+        sv = L.side;
+    }
+    if (p.V > 0) {
+        if (A) launch(L, "loop_vertex", k_loop_vertex<true>, dim3(grid_for(p.V)), dim3(kThreads), 0, sv, p, c, fr);
+        else launch(L, "loop_vertex", k_loop_vertex<false>, dim3(grid_for(p.V)), dim3(kThreads), 0, sv, p, c, fr);
+    }
+    if (base) loop_edge_base(p, stat, base, s, L);
+    if (fork) {  // the edge kernel (side branch) waits for the bases
+        cudaEventRecord(L.ev_fork, s);
+        cudaStreamWaitEvent(L.side, L.ev_fork, 0);
+    }
+    if (p.E > 0) {
+        if (A) launch(L, "loop_edge", k_loop_edge<true>, dim3(grid_for(p.E)), dim3(kThreads), 0, sv, p, c, fr);
+        else launch(L, "loop_edge", k_loop_edge<false>, dim3(grid_for(p.E)), dim3(kThreads), 0, sv, p, c, fr);
     }
     if (topo && p.F > 0) {
         if (A) launch(L, "loop_face", k_loop_face<true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c);
         else launch(L, "loop_face", k_loop_face<false>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c);
-    }
-    if (p.E > 0) {
-        if (A) launch(L, "loop_edge", k_loop_edge<true>, dim3(grid_for(p.E)), dim3(kThreads), 0, se, p, c, fr);
-        else launch(L, "loop_edge", k_loop_edge<false>, dim3(grid_for(p.E)), dim3(kThreads), 0, se, p, c, fr);
-    }
-    if (p.V > 0) {
-        if (A) launch(L, "loop_vertex", k_loop_vertex<true>, dim3(grid_for(p.V)), dim3(kThreads), 0, s, p, c, fr);
-        else launch(L, "loop_vertex", k_loop_vertex<false>, dim3(grid_for(p.V)), dim3(kThreads), 0, s, p, c, fr);
     }
     if (fork) {
         cudaEventRecord(L.ev_join, L.side);
