@@ -458,7 +458,14 @@ static void fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     launch(L, "b0_flags", k_b0_flags<ORDER>, dim3(grid_for(nf)), dim3(kThreads), 0, s, b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
                                                  b.face_edge, b.edge_hh, tp, b.V, E, b.bnd_word, nw, b.edge_sigma,
                                                  b.edge_cidx, b.sp_flag, b.bnd_wcnt, b.flags, b.crease_lenient);
-    scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, region(b, 3), s, L, b.zeroed);
+    // the boundary-word prefix is only read by the level kernels: a parallel branch next to the
+    // special-list chain (fork / join events become graph branches under capture)
+    const bool fork = L.can_fork() && b.zeroed;
+    if (fork) {
+        cudaEventRecord(L.ev_fork, s);
+        cudaStreamWaitEvent(L.side, L.ev_fork, 0);
+    }
+    scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, region(b, 3), fork ? L.side : s, L, b.zeroed);
     scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, region(b, 4), s, L, b.zeroed);
     if (E > 0) {
         launch(L, "b0_special", k_b0_special<ORDER>, dim3(grid_for(E)), dim3(kThreads), 0, s, b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp, E,
@@ -470,6 +477,10 @@ static void fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     }
     if (b.V > 0) {
         launch(L, "b0_sv_sort", k_b0_svsort, dim3(grid_for(b.V)), dim3(kThreads), 0, s, b.V, b.sv_off, b.sv_list, b.sv_vtx, b.scalars);
+    }
+    if (fork) {
+        cudaEventRecord(L.ev_join, L.side);
+        cudaStreamWaitEvent(s, L.ev_join, 0);
     }
 }
 
