@@ -193,3 +193,23 @@ def test_gpu_extract_errors():
         sub, vm, fm = m.extract(0)
         with sub:
             assert sub.counts(0)["faces"] == 6
+
+
+@pytest.mark.gpu
+def test_gpu_extract_loop_level1_matches_oracle():
+    """Loop: extraction from level 1 of a creased tetrahedron around a caller mask."""
+    from paper_1809_06047_b200 import Mesh
+    mesh = mg.tetrahedron(creased=True)
+    rec = oracle.refine(mesh, "loop", 1)[1]
+    vsel = np.zeros(len(rec["pos"]), np.uint8)
+    vsel[[0, 5]] = 1
+    want, wvm, wfm = ox.extract(rec, vsel=vsel, rings=1)
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine("loop", 1)
+        sub, vm, fm = m.extract(1, vsel=vsel, rings=1)
+        with sub:
+            assert np.array_equal(vm.cpu().numpy(), np.asarray(wvm, np.int32))
+            assert np.array_equal(fm.cpu().numpy(), np.asarray(wfm, np.int32))
+            sub.refine("loop", 0)
+            t = sub.topology(0)
+            assert np.array_equal(t["face_vtx"].cpu().numpy(), want["face_vtx"])

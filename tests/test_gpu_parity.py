@@ -529,3 +529,18 @@ def test_fuzz_triangle_tori_loop_sqrt3(seed):
     t = mg.torus_tris(int(rng.integers(4, 12)), int(rng.integers(4, 10)), seed=3000 + seed)
     compare(t, "loop", 1 + seed % 3)
     compare(t, "sqrt3", 1 + (seed + 1) % 3, edges=False)
+
+
+def test_eval_attributes_loop_and_sqrt3():
+    """Extra channels through the Loop (creased, boundary-free) and sqrt3 static paths."""
+    Mesh = _gpu()
+    for mesh, scheme in ((mg.tetrahedron(creased=True), "loop"), (mg.torus_tris(8, 6), "sqrt3")):
+        attr = mg.vertex_channels(mesh, 2)
+        with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+            m.refine(scheme, 3)
+            got = m.eval_attributes(torch.from_numpy(attr).cuda(), 3).cpu().numpy()
+        pad = np.zeros((attr.shape[0], 3), np.float32)
+        pad[:, :2] = attr
+        want = oracle.refine(dict(mesh, pos=pad), scheme, 3)[-1]["pos"][:, :2]
+        scale = float(np.linalg.norm(pad.max(0) - pad.min(0)))
+        assert np.abs(got - want).max() / scale <= TOL, scheme
