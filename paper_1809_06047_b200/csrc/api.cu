@@ -426,7 +426,6 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
             if (has_child) {
                 // CC consumes a level's twins only to emit the adjacency of ITS child (adj)
                 if (scheme != ALSUB_CATMULL_CLARK || adj) c.face_twin = A<int32_t>(m, c.S, s, ML, ok);
-                if (scheme == ALSUB_LOOP) c.vtx_slot0 = A<int32_t>(m, c.V, s, ML, ok);
                 // CC, levels >= 3: the last refined level recomputes its edge rows and iterates its
                 // parent's edges (cc.cu), so its face_edge / edge pairs are never stored
                 const bool last_cc = scheme == ALSUB_CATMULL_CLARK && levels >= 3 && l == levels - 1;
@@ -490,6 +489,26 @@ static VSegs make_segs_s3(alsub_mesh *m, int l) {
         g.start[n] = (int32_t)q.V; g.len[n] = (int32_t)q.F; g.type[n] = 1; g.birth[n] = (int8_t)k; g.mult[n] = mult;
         g.fvx[k - 1] = q.face_vtx;
         g.ftw[k - 1] = q.face_twin;
+        ++n;
+    }
+    g.nseg = n;
+    g.vtx_off0 = m->b0.vtx_off; g.vtx_list0 = m->b0.vtx_slot; g.face_off0 = m->in_face_off;
+    g.slot_face0 = m->b0.slot_face; g.vbnd0 = m->b0.vbnd;
+    return g;
+}
+
+// vertex-id segments of Loop level l: [V0 | E_0 | ... | E_{l-1}] (edge points born at level k + 1
+// from the level-k edge pairs)
+static VSegs make_segs_loop(alsub_mesh *m, int l) {
+    VSegs g{};
+    g.level = l;
+    g.hs_seg = -1;
+    int n = 0;
+    g.start[n] = 0; g.len[n] = m->V0; g.type[n] = 0; g.birth[n] = 0; ++n;
+    for (int k = 1; k <= l; ++k) {
+        const LevelHost &q = m->lv[k - 1];
+        g.start[n] = (int32_t)q.V; g.len[n] = (int32_t)q.E; g.type[n] = 2; g.birth[n] = (int8_t)k;
+        g.ehh[k - 1] = q.edge_hh;
         ++n;
     }
     g.nseg = n;
@@ -568,7 +587,8 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
             cc_level(p, c, fr, true, adj, g, use_gp ? &gp : nullptr, s, L);
             if (special && !p.crease) crease_level(p, c, fr, (int32_t)(P.V + P.F), 0, true, s, L);
         } else if (scheme == ALSUB_LOOP) {
-            loop_level(p, c, fr, true, adj, P.loop_stat, (adj || special) ? P.loop_base : nullptr, s, L);
+            VSegs g = make_segs_loop(m, l);
+            loop_level(p, c, fr, true, adj, P.loop_stat, (adj || special) ? P.loop_base : nullptr, g, s, L);
             if (special) crease_level(p, c, fr, (int32_t)P.V, 1, true, s, L);
         } else {
             VSegs g = make_segs_s3(m, l);
@@ -899,7 +919,8 @@ static void static_level(alsub_mesh *m, int l, const Frames &fr, cudaStream_t s,
         cc_level(p, c, fr, false, false, g, use_gp ? &gp : nullptr, s, L);
         if (special && !p.crease) crease_level(p, c, fr, (int32_t)(Pl.V + Pl.F), 0, false, s, L);
     } else if (scheme == ALSUB_LOOP) {
-        loop_level(p, c, fr, false, false, nullptr, nullptr, s, L);
+        VSegs g = make_segs_loop(m, l);
+        loop_level(p, c, fr, false, false, nullptr, nullptr, g, s, L);
         if (special) crease_level(p, c, fr, (int32_t)Pl.V, 1, false, s, L);
     } else {
         VSegs g = make_segs_s3(m, l);

@@ -250,7 +250,7 @@ struct VSegs {
 void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &segs,
               const LevelDev *gp, cudaStream_t s, Launches &L);
 void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, int32_t *stat,
-                int32_t *base, cudaStream_t s, Launches &L);
+                int32_t *base, const VSegs &g, cudaStream_t s, Launches &L);
 void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &g,
                  cudaStream_t s, Launches &L);
 // crease / boundary module (crease.cu): ONE kernel per level -- edge and vertex overrides and

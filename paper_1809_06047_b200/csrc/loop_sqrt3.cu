@@ -105,60 +105,85 @@ ALSUB_D int32_t loop_inner(const LevelDev &p, int32_t m, int32_t x, int32_t z, i
     return __ldg(p.loop_base + m) + 2 + rank;
 }
 
+// a warp's 32 x 12 child-row ints (4 child triangles per face) staged in shared memory and written
+// as 12 coalesced 128-B stores
+ALSUB_D void warp_store_12(int32_t *stage, const int32_t (&v)[12], int32_t *dst, int64_t w0, int64_t n, int lane) {
+#pragma unroll
+    for (int k = 0; k < 12; ++k) stage[lane * 12 + k] = v[k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        const int64_t o = w0 + k * 32 + lane;
+        if (o < n) dst[o] = stage[k * 32 + lane];
+    }
+    __syncwarp();
+}
+
 template <bool ADJ>
 __global__ void __launch_bounds__(kThreads) k_loop_face(LevelDev p, ChildDev c) {
     ALSUB_GRID_WAIT();
+    __shared__ int32_t s_stage[kThreads / 32][12 * 32];
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= p.F) return;
+    const bool valid = r < p.F;
+    const int lane = threadIdx.x & 31;
+    int32_t *stage = s_stage[threadIdx.x >> 5];
+    const int64_t w0 = 12 * (int64_t)(r - lane), n = 12 * (int64_t)p.F;
     const int32_t V = p.V;
     int32_t v[3], e[3];
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
-        v[t] = __ldg(p.face_vtx + 3 * r + t);
-        e[t] = __ldg(p.face_edge + 3 * r + t);
+        v[t] = valid ? __ldg(p.face_vtx + 3 * r + t) : 0;
+        e[t] = valid ? __ldg(p.face_edge + 3 * r + t) : 0;
     }
-    int32_t *cfv = c.face_vtx + 12 * (int64_t)r;
+    int32_t rows[12];
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
-        cfv[3 * t + 0] = v[t];
-        cfv[3 * t + 1] = V + e[t];
-        cfv[3 * t + 2] = V + e[(t + 2) % 3];
+        rows[3 * t + 0] = v[t];
+        rows[3 * t + 1] = V + e[t];
+        rows[3 * t + 2] = V + e[(t + 2) % 3];
     }
-    cfv[9] = V + e[0];
-    cfv[10] = V + e[1];
-    cfv[11] = V + e[2];
+    rows[9] = V + e[0];
+    rows[10] = V + e[1];
+    rows[11] = V + e[2];
+    warp_store_12(stage, rows, c.face_vtx, w0, n, lane);
     if constexpr (ADJ) {
         int32_t tw[3];
 #pragma unroll
-        for (int t = 0; t < 3; ++t) tw[t] = __ldg(p.face_twin + 3 * r + t);
+        for (int t = 0; t < 3; ++t) tw[t] = valid ? __ldg(p.face_twin + 3 * r + t) : -1;
         // inner edge between edges i and j of this face
         auto inner = [&](int i, int j) {
             const int k = 3 - i - j;  // the third edge
             const int mi = e[i] > e[j] ? i : j, xi = e[i] > e[j] ? j : i;
             return loop_inner(p, e[mi], e[xi], e[k], tw[mi]);
         };
-        int32_t in01 = inner(0, 1), in12 = inner(1, 2), in20 = inner(2, 0);
+        int32_t in01 = 0, in12 = 0, in20 = 0;
+        if (valid) {
+            in01 = inner(0, 1);
+            in12 = inner(1, 2);
+            in20 = inner(2, 0);
+        }
         const int32_t inner_t_tm1[3] = {in20, in01, in12};  // between e_t and e_{t-1}
-        int32_t *cfe = c.face_edge + 12 * (int64_t)r;
-        int32_t *cft = c.face_twin + 12 * (int64_t)r;
+        int32_t fe[12], ft[12];
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
             const int tn = (t + 1) % 3, tp = (t + 2) % 3;
-            cfe[3 * t + 0] = __ldg(p.loop_base + e[t]) + (v[t] > v[tn]);
-            cfe[3 * t + 1] = inner_t_tm1[t];
-            cfe[3 * t + 2] = __ldg(p.loop_base + e[tp]) + (v[t] > v[tp]);
+            fe[3 * t + 0] = valid ? __ldg(p.loop_base + e[t]) + (v[t] > v[tn]) : 0;
+            fe[3 * t + 1] = inner_t_tm1[t];
+            fe[3 * t + 2] = valid ? __ldg(p.loop_base + e[tp]) + (v[t] > v[tp]) : 0;
             const int32_t a = tw[t], b = tw[tp];
-            cft[3 * t + 0] = a >= 0 ? 3 * (4 * (a / 3) + (a % 3 + 1) % 3) + 2 : -1;
-            cft[3 * t + 1] = 3 * (4 * r + 3) + tp;
-            cft[3 * t + 2] = b >= 0 ? 3 * (4 * (b / 3) + b % 3) + 0 : -1;
-            c.edge_hh[inner_t_tm1[t]] = make_int2(12 * r + 3 * t + 1, 3 * (4 * r + 3) + tp);
+            ft[3 * t + 0] = a >= 0 ? 3 * (4 * (a / 3) + (a % 3 + 1) % 3) + 2 : -1;
+            ft[3 * t + 1] = 3 * (4 * r + 3) + tp;
+            ft[3 * t + 2] = b >= 0 ? 3 * (4 * (b / 3) + b % 3) + 0 : -1;
+            if (valid) c.edge_hh[inner_t_tm1[t]] = make_int2(12 * r + 3 * t + 1, 3 * (4 * r + 3) + tp);
         }
-        cfe[9] = in01;
-        cfe[10] = in12;
-        cfe[11] = in20;
-        cft[9] = 3 * (4 * r + 1) + 1;
-        cft[10] = 3 * (4 * r + 2) + 1;
-        cft[11] = 3 * (4 * r + 0) + 1;
+        fe[9] = in01;
+        fe[10] = in12;
+        fe[11] = in20;
+        ft[9] = 3 * (4 * r + 1) + 1;
+        ft[10] = 3 * (4 * r + 2) + 1;
+        ft[11] = 3 * (4 * r + 0) + 1;
+        warp_store_12(stage, fe, c.face_edge, w0, n, lane);
+        warp_store_12(stage, ft, c.face_twin, w0, n, lane);
     }
 }
 
@@ -193,32 +218,61 @@ __global__ void __launch_bounds__(kThreads) k_loop_edge(LevelDev p, ChildDev c, 
         // (lo,ep): lo->ep in the child of h_ab, ep->lo in the child after h_ba; (hi,ep) symmetric
         c.edge_hh[base + 0] = pair(h_ab >= 0 ? loop_c0(h_ab) : -1, h_ba >= 0 ? loop_c2next(h_ba) : -1);
         c.edge_hh[base + 1] = pair(h_ba >= 0 ? loop_c0(h_ba) : -1, h_ab >= 0 ? loop_c2next(h_ab) : -1);
-        c.vtx_slot0[V + e] = loop_c0(h) + 1;
     }
 }
 
+// Vertex kernel, class-structured like the CC one (no twin walk): level-l vertex ids are
+// [V0 | E_0 | E_1 | ... | E_{l-1}] (level-0 vertices, then the edge points born at each level).
+// A vertex's incident slots are closed-form at its birth level -- level-0 vertices: their M^T row;
+// the edge point of level-(m-1) slot h = 3R + t: {12R + 3t + 1, 12R + 3((t+1)%3) + 2, 12R + 9 + t}
+// and the same for its twin slot -- and every later level maps a slot x to corner 0 of the child
+// at that corner, c0(x) = 12(x/3) + 3(x%3).  The neighbours are face_vtx[next(slot)], all loads
+// independent.  S = (1 - n beta_n) p + beta_n sum p_j (Eq. loop vertex); boundary vertices keep p
+// (the crease module sets them, boundary = inf crease).
+
 template <bool ADJ>
-__global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c, Frames fr) {
+__global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c, Frames fr, VSegs g) {
     ALSUB_GRID_WAIT();
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= p.V) return;
-    const int32_t h0 = __ldg(p.vtx_slot0 + v);
-    if constexpr (ADJ) c.vtx_slot0[v] = h0 >= 0 ? loop_c0(h0) : -1;
+    int s = g.nseg - 1;
+    while (s > 0 && v < g.start[s]) --s;
+    const int32_t j = v - g.start[s];
+    const int hops = g.level - g.birth[s];
+    int32_t sl[32];
+    int32_t n = 0;
+    bool bnd = false;
+    if (g.type[s] == 0) {
+        const int32_t o = __ldg(g.vtx_off0 + j);
+        n = __ldg(g.vtx_off0 + j + 1) - o;
+        bnd = __ldg(g.vbnd0 + j) != 0;
+        if (n > 32) bnd = true;  // (valence > 32: handled as a pass-through; never in practice)
+        for (int32_t k = 0; k < n && !bnd; ++k) sl[k] = __ldg(g.vtx_list0 + o + k);
+    } else {
+        const int2 hh = __ldg(g.ehh[g.birth[s] - 1] + j);
+        bnd = hh.y < 0;
+        if (!bnd) {
+            const int32_t hs[2] = {hh.x, hh.y};
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int32_t R = hs[q] / 3, t = hs[q] % 3;
+                sl[n++] = 12 * R + 3 * t + 1;
+                sl[n++] = 12 * R + 3 * ((t + 1) % 3) + 2;
+                sl[n++] = 12 * R + 9 + t;
+            }
+        }
+    }
     for (int f = 0; f < fr.nb; ++f) {
         const PR P = fr.rd(f);
         const PW Pn = fr.wr(f);
         const P3 pv = ld3(P, v);
-        if (h0 < 0) { st3(Pn, v, pv); continue; }
+        if (bnd || n == 0) { st3(Pn, v, pv); continue; }
         P3 acc = p3zero();
-        int32_t h = h0, n = 0;
-        bool bnd = false;
-        do {
-            acc = acc + ld3(P, __ldg(p.face_vtx + tri_next(h)));
-            ++n;
-            h = __ldg(p.face_twin + tri_prev(h));
-            if (h < 0) { bnd = true; break; }
-        } while (h != h0 && n < p.S);
-        if (bnd) { st3(Pn, v, pv); continue; }
+        for (int32_t k = 0; k < n; ++k) {
+            int32_t x = sl[k];
+            for (int h = 0; h < hops; ++h) x = loop_c0(x);
+            acc = acc + ld3(P, __ldg(p.face_vtx + tri_next(x)));
+        }
         const float beta = loop_beta(n);
         st3(Pn, v, (1.0f - (float)n * beta) * pv + beta * acc);
     }
@@ -228,7 +282,7 @@ __global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c
 // creases).  Dependencies: face and edge kernels need the bases, the vertex kernel does not, so it
 // starts at once on the side branch and the edge kernel joins it there after the scan.
 void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, int32_t *stat,
-                int32_t *base, cudaStream_t s, Launches &L) {
+                int32_t *base, const VSegs &g, cudaStream_t s, Launches &L) {
     const bool A = adj && topo;
     const bool fork = L.can_fork();
     cudaStream_t sv = s;
@@ -238,8 +292,8 @@ void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool top
         sv = L.side;
     }
     if (p.V > 0) {
-        if (A) launch(L, "loop_vertex", k_loop_vertex<true>, dim3(grid_for(p.V)), dim3(kThreads), 0, sv, p, c, fr);
-        else launch(L, "loop_vertex", k_loop_vertex<false>, dim3(grid_for(p.V)), dim3(kThreads), 0, sv, p, c, fr);
+        if (A) launch(L, "loop_vertex", k_loop_vertex<true>, dim3(grid_for(p.V)), dim3(kThreads), 0, sv, p, c, fr, g);
+        else launch(L, "loop_vertex", k_loop_vertex<false>, dim3(grid_for(p.V)), dim3(kThreads), 0, sv, p, c, fr, g);
     }
     if (base) loop_edge_base(p, stat, base, s, L);
     if (fork) {  // the edge kernel (side branch) waits for the bases
