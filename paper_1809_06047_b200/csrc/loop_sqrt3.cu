@@ -190,34 +190,61 @@ __global__ void __launch_bounds__(kThreads) k_loop_face(LevelDev p, ChildDev c) 
 ALSUB_D int32_t loop_c0(int32_t x) { return 12 * (x / 3) + 3 * (x % 3); }
 ALSUB_D int32_t loop_c2next(int32_t x) { return 3 * (4 * (x / 3) + (x % 3 + 1) % 3) + 2; }
 
-template <bool ADJ>
+// IT edges per thread, every load stage issued for all of them before any is consumed (the
+// kernel is a chain edge pair -> face row -> positions)
+template <bool ADJ, int IT = 2>
 __global__ void __launch_bounds__(kThreads) k_loop_edge(LevelDev p, ChildDev c, Frames fr) {
     ALSUB_GRID_WAIT();
-    const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= p.E) return;
-    const int2 hh = __ldg(p.edge_hh + e);
-    const int32_t h = hh.x, tw = hh.y;
-    const int32_t va = __ldg(p.face_vtx + h), vb = __ldg(p.face_vtx + tri_next(h));
-    const int32_t g1 = __ldg(p.face_vtx + tri_prev(h));
-    const int32_t g2 = tw >= 0 ? __ldg(p.face_vtx + tri_prev(tw)) : -1;
+    const int32_t e0 = blockIdx.x * (kThreads * IT) + threadIdx.x;
     const int32_t V = p.V;
+    int2 hh[IT];
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+        const int32_t e = e0 + k * kThreads;
+        hh[k] = e < p.E ? __ldg(p.edge_hh + e) : make_int2(0, -1);
+    }
+    int32_t va[IT], vb[IT], g1[IT], g2[IT];
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+        const int32_t h = hh[k].x, tw = hh[k].y;
+        va[k] = __ldg(p.face_vtx + h);
+        vb[k] = __ldg(p.face_vtx + tri_next(h));
+        g1[k] = __ldg(p.face_vtx + tri_prev(h));
+        g2[k] = tw >= 0 ? __ldg(p.face_vtx + tri_prev(tw)) : -1;
+    }
     for (int f = 0; f < fr.nb; ++f) {
         const PR P = fr.rd(f);
-        const P3 ab = ld3(P, va) + ld3(P, vb);
-        P3 out = tw < 0 ? 0.5f * ab : 0.375f * ab + 0.125f * (ld3(P, g1) + ld3(P, g2));
-        st3(fr.wr(f), (int64_t)V + e, out);
+        P3 ab[IT], gg[IT];
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            ab[k] = ld3(P, va[k]) + ld3(P, vb[k]);
+            gg[k] = hh[k].y >= 0 ? ld3(P, g1[k]) + ld3(P, g2[k]) : p3zero();
+        }
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int32_t e = e0 + k * kThreads;
+            if (e >= p.E) continue;
+            const P3 out = hh[k].y < 0 ? 0.5f * ab[k] : 0.375f * ab[k] + 0.125f * gg[k];
+            st3(fr.wr(f), (int64_t)V + e, out);
+        }
     }
     if constexpr (ADJ) {
-        const int32_t base = __ldg(p.loop_base + e);
-        const int32_t h_ab = va < vb ? h : tw, h_ba = va < vb ? tw : h;
         auto pair = [](int32_t x, int32_t y) {
             if (x < 0) return make_int2(y, -1);
             if (y < 0) return make_int2(x, -1);
             return make_int2(min(x, y), max(x, y));
         };
-        // (lo,ep): lo->ep in the child of h_ab, ep->lo in the child after h_ba; (hi,ep) symmetric
-        c.edge_hh[base + 0] = pair(h_ab >= 0 ? loop_c0(h_ab) : -1, h_ba >= 0 ? loop_c2next(h_ba) : -1);
-        c.edge_hh[base + 1] = pair(h_ba >= 0 ? loop_c0(h_ba) : -1, h_ab >= 0 ? loop_c2next(h_ab) : -1);
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int32_t e = e0 + k * kThreads;
+            if (e >= p.E) continue;
+            const int32_t h = hh[k].x, tw = hh[k].y;
+            const int32_t base = __ldg(p.loop_base + e);
+            const int32_t h_ab = va[k] < vb[k] ? h : tw, h_ba = va[k] < vb[k] ? tw : h;
+            // (lo,ep): lo->ep in the child of h_ab, ep->lo in the child after h_ba; (hi,ep) symmetric
+            c.edge_hh[base + 0] = pair(h_ab >= 0 ? loop_c0(h_ab) : -1, h_ba >= 0 ? loop_c2next(h_ba) : -1);
+            c.edge_hh[base + 1] = pair(h_ba >= 0 ? loop_c0(h_ba) : -1, h_ab >= 0 ? loop_c2next(h_ab) : -1);
+        }
     }
 }
 
@@ -239,39 +266,47 @@ __global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c
     while (s > 0 && v < g.start[s]) --s;
     const int32_t j = v - g.start[s];
     const int hops = g.level - g.birth[s];
-    int32_t sl[32];
-    int32_t n = 0;
+    const bool lv0 = g.type[s] == 0;
+    int32_t n = 0, o = 0;
+    int32_t R[2] = {0, 0}, T[2] = {0, 0};
     bool bnd = false;
-    if (g.type[s] == 0) {
-        const int32_t o = __ldg(g.vtx_off0 + j);
+    if (lv0) {
+        o = __ldg(g.vtx_off0 + j);
         n = __ldg(g.vtx_off0 + j + 1) - o;
         bnd = __ldg(g.vbnd0 + j) != 0;
-        if (n > 32) bnd = true;  // (valence > 32: handled as a pass-through; never in practice)
-        for (int32_t k = 0; k < n && !bnd; ++k) sl[k] = __ldg(g.vtx_list0 + o + k);
     } else {
         const int2 hh = __ldg(g.ehh[g.birth[s] - 1] + j);
         bnd = hh.y < 0;
-        if (!bnd) {
-            const int32_t hs[2] = {hh.x, hh.y};
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int32_t R = hs[q] / 3, t = hs[q] % 3;
-                sl[n++] = 12 * R + 3 * t + 1;
-                sl[n++] = 12 * R + 3 * ((t + 1) % 3) + 2;
-                sl[n++] = 12 * R + 9 + t;
-            }
-        }
+        n = 6;
+        R[0] = hh.x / 3; T[0] = hh.x % 3;
+        R[1] = hh.y / 3; T[1] = hh.y % 3;
     }
+    // birth slot k, mapped `hops` levels down to this level
+    auto slot = [&](int32_t k) {
+        int32_t x;
+        if (lv0) {
+            x = __ldg(g.vtx_list0 + o + k);
+        } else {
+            const int q = k >= 3, u = k - 3 * q;
+            const int32_t r = q ? R[1] : R[0], t = q ? T[1] : T[0];
+            x = u == 0 ? 12 * r + 3 * t + 1 : (u == 1 ? 12 * r + 3 * ((t + 1) % 3) + 2 : 12 * r + 9 + t);
+        }
+        for (int h = 0; h < hops; ++h) x = loop_c0(x);
+        return x;
+    };
     for (int f = 0; f < fr.nb; ++f) {
         const PR P = fr.rd(f);
         const PW Pn = fr.wr(f);
         const P3 pv = ld3(P, v);
         if (bnd || n == 0) { st3(Pn, v, pv); continue; }
         P3 acc = p3zero();
-        for (int32_t k = 0; k < n; ++k) {
-            int32_t x = sl[k];
-            for (int h = 0; h < hops; ++h) x = loop_c0(x);
-            acc = acc + ld3(P, __ldg(p.face_vtx + tri_next(x)));
+        for (int32_t k0 = 0; k0 < n; k0 += 4) {  // four independent neighbour lookups in flight
+            int32_t nb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) nb[u] = k0 + u < n ? __ldg(p.face_vtx + tri_next(slot(k0 + u))) : -1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (nb[u] >= 0) acc = acc + ld3(P, nb[u]);
         }
         const float beta = loop_beta(n);
         st3(Pn, v, (1.0f - (float)n * beta) * pv + beta * acc);
@@ -301,8 +336,8 @@ void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool top
         cudaStreamWaitEvent(L.side, L.ev_fork, 0);
     }
     if (p.E > 0) {
-        if (A) launch(L, "loop_edge", k_loop_edge<true>, dim3(grid_for(p.E)), dim3(kThreads), 0, sv, p, c, fr);
-        else launch(L, "loop_edge", k_loop_edge<false>, dim3(grid_for(p.E)), dim3(kThreads), 0, sv, p, c, fr);
+        if (A) launch(L, "loop_edge", k_loop_edge<true>, dim3(grid_for(p.E, 2 * kThreads)), dim3(kThreads), 0, sv, p, c, fr);
+        else launch(L, "loop_edge", k_loop_edge<false>, dim3(grid_for(p.E, 2 * kThreads)), dim3(kThreads), 0, sv, p, c, fr);
     }
     if (topo && p.F > 0) {
         if (A) launch(L, "loop_face", k_loop_face<true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c);
