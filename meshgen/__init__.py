@@ -391,3 +391,15 @@ def permuted(mesh, perm_vtx, perm_face):
     pos = np.asarray(mesh["pos"])[perm_vtx]
     crease = newid[mesh["crease"]].astype(np.int32) if len(mesh["crease"]) else mesh["crease"]
     return _pack(faces, pos, crease, mesh["sigma"], name=mesh.get("name", "mesh") + "_perm")
+
+
+def bipyramid(n=40, seed=SEED_TOPO):
+    """Closed n-gonal bipyramid: two apices of valence n (long M^T rows, high-valence rules) and
+    an equator of valence-4 vertices; 2n outward CCW triangles, slightly jittered."""
+    rng = np.random.default_rng(seed)
+    pos = [(math.cos(2 * math.pi * k / n), math.sin(2 * math.pi * k / n), 0.0) for k in range(n)]
+    pos += [(0.0, 0.0, 1.0), (0.0, 0.0, -1.0)]
+    pos = np.asarray(pos) + rng.normal(0, 0.01, (n + 2, 3))
+    top, bot = n, n + 1
+    faces = [(k, (k + 1) % n, top) for k in range(n)] + [((k + 1) % n, k, bot) for k in range(n)]
+    return _pack(faces, pos, name=f"bipyramid{n}")

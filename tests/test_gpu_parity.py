@@ -544,3 +544,10 @@ def test_eval_attributes_loop_and_sqrt3():
         want = oracle.refine(dict(mesh, pos=pad), scheme, 3)[-1]["pos"][:, :2]
         scale = float(np.linalg.norm(pad.max(0) - pad.min(0)))
         assert np.abs(got - want).max() / scale <= TOL, scheme
+
+
+@pytest.mark.parametrize("scheme", ["cc", "loop", "sqrt3"])
+def test_high_valence_vertices(scheme):
+    """Valence-40 apices: M^T rows longer than a warp's fast path (serial fallbacks), valence
+    constants beyond the common range, long crease-free rings."""
+    compare(mg.bipyramid(40), scheme, 2, edges=scheme != "sqrt3")
