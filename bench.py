@@ -281,6 +281,9 @@ def run_alsub(args):
     total_ms = max_over_ranks(sum(step_ms))
     ms_per_step = total_ms / K
     value = world * Fout * K / (total_ms / 1000.0)
+    srt = sorted(step_ms)
+    step_pct = {"p10": srt[int(0.1 * (K - 1))], "median": srt[(K - 1) // 2], "p90": srt[int(0.9 * (K - 1))],
+                "note": "this rank's per-step CUDA-event times (SURVEY 8(d) timing protocol)"}
 
     # ---- per-kernel timing (CUDA events between launches, eager), averaged over reps ----
     reps = max(3, min(10, K))
@@ -357,6 +360,7 @@ def run_alsub(args):
                            "graph": True},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches_per_step * K), "launches_per_step": int(launches_per_step),
+                "step_ms": step_pct,
                 "clocks": sampler.summary(), "levels": per_level, "profile_step_ms": prof_step,
                 "other_configs": others, "frames_config5_sample": frames,
                 "paper_context": PAPER_CONTEXT}
