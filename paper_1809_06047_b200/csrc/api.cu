@@ -407,7 +407,7 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
     m->sv_off = A<int32_t>(m, sv_total, s, ML, ok);
     m->hs_elems = 0;
     if (scheme == ALSUB_CATMULL_CLARK)
-        for (int l = 2; l < levels; ++l) m->hs_elems = std::max<int64_t>(m->hs_elems, 3 * lv[l].F);
+        for (int l = 2; l + 1 < levels; ++l) m->hs_elems = std::max<int64_t>(m->hs_elems, 3 * lv[l].F);
     m->hs = m->hs_elems ? A<float>(m, m->hs_elems, s, ML, ok) : nullptr;
     m->c0_elems = 0;
     if (scheme == ALSUB_CATMULL_CLARK)
@@ -580,7 +580,10 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
             VSegs g = make_segs(m, l);
             LevelDev gp{};
             const bool use_gp = l >= 2 && P.edge_hh == nullptr;
-            if (use_gp) gp = dev_of(m->lv[l - 1]);
+            if (use_gp) {
+                gp = dev_of(m->lv[l - 1]);
+                g.len[g.hs_seg] = 0;  // the edge kernel smooths the edge points born at level l
+            }
             // crease module fused into the level kernels on small levels (the latency of a separate
             // pass dominates there), a separate kernel on large ones (fusion costs occupancy)
             p.crease = (special && !use_gp && P.V < kFuseCreaseMaxV) ? 1 : 0;
@@ -914,7 +917,10 @@ static void static_level(alsub_mesh *m, int l, const Frames &fr, cudaStream_t s,
         VSegs g = make_segs(m, l);
         LevelDev gp{};
         const bool use_gp = l >= 2 && Pl.edge_hh == nullptr;
-        if (use_gp) gp = dev_of(m->lv[l - 1]);
+        if (use_gp) {
+            gp = dev_of(m->lv[l - 1]);
+            g.len[g.hs_seg] = 0;  // the edge kernel smooths the edge points born at level l
+        }
         p.crease = (special && !use_gp && Pl.V < kFuseCreaseMaxV) ? 1 : 0;
         cc_level(p, c, fr, false, false, g, use_gp ? &gp : nullptr, s, L);
         if (special && !p.crease) crease_level(p, c, fr, (int32_t)(Pl.V + Pl.F), 0, false, s, L);

@@ -88,13 +88,16 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
             // (1) the edge point of parent slot r (born at this level) sits at corner 1 of child
             // r and corner 3 of child r+1 (mod 4): its half ring sum from this parent face is
             // (p2 + f_r) + (p0 + f_{r+1}); the vertex kernel adds the two halves of the edge
-            const P3 q = p0 + fc;
-            const int src = (lane & ~3) | ((lane + 1) & 3);
-            P3 qn;
-            qn.x = __shfl_sync(0xffffffffu, q.x, src);
-            qn.y = __shfl_sync(0xffffffffu, q.y, src);
-            qn.z = __shfl_sync(0xffffffffu, q.z, src);
-            if (valid) st3(fr.hsw(f), r, p2 + fc + qn);
+            // (at the last level the edge kernel finishes these vertices itself, see k_cc_edge_gp)
+            if constexpr (!GPE) {
+                const P3 q = p0 + fc;
+                const int src = (lane & ~3) | ((lane + 1) & 3);
+                P3 qn;
+                qn.x = __shfl_sync(0xffffffffu, q.x, src);
+                qn.y = __shfl_sync(0xffffffffu, q.y, src);
+                qn.z = __shfl_sync(0xffffffffu, q.z, src);
+                if (valid) st3(fr.hsw(f), r, p2 + fc + qn);
+            }
             // (2) corner 2 of the four children of a quad is the parent's face point (born at this
             // level, valence 4): its vertex point needs exactly these four faces' f and their
             // corner-3 vertices -- reduce over the 4 sibling lanes (no gather, no vertex pass)
@@ -297,7 +300,12 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
 // level-(l-1) edge e' = (h', tw'): (lo,ep), (hi,ep), (fp_R,ep), (fp_S,ep) with ids base(e')+k and
 // faces {h_ab, next(h_ba)}, {h_ba, next(h_ab)}, {h', next(h')}, {tw', next(tw')} (level-l face
 // index = level-(l-1) slot).  Five position gathers and four face points serve all four edge
-// points, and the level-l edge pairs never need to be stored.
+// points, and the level-l edge pairs never need to be stored.  The same values are exactly the
+// 1-ring of the level-l vertex ep (an edge point born at level l, valence 4: neighbours lo, hi,
+// fp_R, fp_S; faces h, next(h), tw, next(tw)), so its vertex point
+//   S(ep) = 1/2 p_ep + 1/16 (p_lo + p_hi + p_R + p_S + f_h + f_next(h) + f_tw + f_next(tw))
+// (Eq. pos_update with n = 4) is stored here too, at id ep (coalesced: consecutive e).
+// Boundary edge points keep p; the crease pass overwrites every special vertex afterwards.
 template <int NBC>
 __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp, ChildDev c, Frames fr) {
     ALSUB_GRID_WAIT();
@@ -342,6 +350,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
             if (tw < 0) {
                 q[0] = 0.5f * (plo + pep);
                 q[1] = 0.5f * (phi + pep);
+                st3(Pn, ep, pep);
             } else {
                 const P3 pS = ld3(P, fpS), ft = ld3c(Pn, V + tw), fnt = ld3c(Pn, V + nt);
                 const P3 fa = (f0a == h ? fh : ft) + (f0b == nh ? fnh : fnt);
@@ -349,6 +358,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
                 q[0] = 0.25f * (plo + pep + fa);
                 q[1] = 0.25f * (phi + pep + fb);
                 q[3] = 0.25f * (pS + pep + ft + fnt);
+                st3(Pn, ep, 0.5f * pep + 0.0625f * ((plo + phi) + (pR + pS) + (fh + fnh) + (ft + fnt)));
             }
 
             for (int k = 0; k < nch; ++k) {
