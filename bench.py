@@ -72,7 +72,8 @@ def kernel_bytes_cc(name, c, prev, lvl, levels):
     if name == "cc_face":
         rd = 4 * S + 12 * V + (48 * Fp if gp_last else 4 * S) + (4 * S if adj else 0)
         wr = 12 * F + 16 * S + (16 * S if child_rows else 0) + (16 * S if child_twin else 0)
-        wr += (12 * Fp + 12 * F) if fpv else 0    # new face-point vertices + half ring sums
+        wr += 12 * Fp if fpv else 0               # new face-point vertices
+        wr += 12 * F if (fpv and not gp_last) else 0  # half ring sums (the last level has none)
         wr += 12 * F if lvl >= 1 else 0             # corner-0 contributions c0
     elif name == "cc_edge":
         if gp_last:
@@ -80,7 +81,11 @@ def kernel_bytes_cc(name, c, prev, lvl, levels):
         else:
             rd = 8 * E + 4 * S + 12 * V + 12 * F
         wr = 12 * E + (8 * (2 * E + S) if child_rows else 0)
+        wr += 12 * Ep if gp_last else 0           # vertex points of the edge points born at lvl
     elif name == "cc_vertex":
+        if gp_last:  # vertices born before lvl only: p + their faces' c0 (each read once)
+            nv = V - Fp - Ep
+            return 12 * nv + 12 * F + 12 * nv
         if lvl >= 1:  # c0 sums for vertices born earlier, half sums for new edge points
             rd = 12 * V + 12 * F + 8 * Ep + (12 * F if fpv else 0) + (0 if fpv else 4 * S + 12 * F)
         else:
@@ -178,6 +183,26 @@ def dist_max(x, device=None):
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gather_summaries(local, nframes, world, rank, device=None):
+    """All-gather every rank's per-frame summary records (int32 [per_rank][8], frames f_lo .. f_hi
+    of shard()) into one [nframes][8] table in frame order -- the only data-path collective of the
+    sharded frames job (32 B per frame over NCCL instead of the frames)."""
+    import torch
+    import torch.distributed as dist
+    per_max = max(hi - lo for lo, hi in (shard(nframes, world, r) for r in range(world)))
+    buf = torch.zeros((per_max, 8), dtype=torch.int32, device=device)
+    buf[:local.shape[0]] = local
+    if world == 1 or not (dist.is_available() and dist.is_initialized()):
+        return buf[:nframes]
+    out = torch.empty((world * per_max, 8), dtype=torch.int32, device=device)
+    dist.all_gather_into_tensor(out, buf)
+    parts = []
+    for r in range(world):
+        lo, hi = shard(nframes, world, r)
+        parts.append(out[r * per_max:r * per_max + (hi - lo)])
+    return torch.cat(parts)
 
 
 def cpu_oracle_baseline(mesh, levels, label):
@@ -448,7 +473,7 @@ def run_e2e(args, mesh, levels, Fout, Vout, dev, flush):
 def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, peak_src, emit=True):
     """Config 5: static-mode frames, armor50k CC level 4, 4096 frames sharded over ranks."""
     import torch
-    from paper_1809_06047_b200 import Mesh
+    from paper_1809_06047_b200 import Mesh, frame_summary
     levels = 4
     nframes = args.frames
     mesh = mg.armor50k()
@@ -464,9 +489,33 @@ def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, pea
     Vout, Fout = cnt[-1]["V"], cnt[-1]["F"]
     outs = [torch.empty((nb, Vout, 3), dtype=torch.float32, device=dev) for _ in range(2)]
     nsteps = per_rank // nb
-    for i in range(min(args.warmup, nsteps)):
-        m.eval_frames(frames[i * nb:(i + 1) * nb], levels, out=outs[i % 2])
+    # per-frame result records (bbox + checksum, alsub_frame_summary), gathered over NCCL at the end
+    summ = torch.zeros((per_rank, 8), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
+    # the summary of batch i runs on a side stream, overlapped with the evaluation of batch i + 1
+    # (the level kernels leave DRAM bandwidth unused); batch i + 2 reuses the buffer only after it
+    side = torch.cuda.Stream(device=dev)
+    done = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_s = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
+
+    def batch(i, timed_last=False):
+        k = i % 2
+        if i >= 2:
+            stream.wait_event(done[k])
+        m.eval_frames(frames[i * nb:(i + 1) * nb], levels, out=outs[k])
+        ready = torch.cuda.Event()
+        ready.record(stream)
+        side.wait_event(ready)
+        with torch.cuda.stream(side):
+            if timed_last:
+                ev_s[0][0].record(side)
+            frame_summary(outs[k], out=summ[i * nb:(i + 1) * nb], stream=side)
+            if timed_last:
+                ev_s[0][1].record(side)
+            done[k].record(side)
+
+    for i in range(min(args.warmup, nsteps)):
+        batch(i)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(dev.index)
     barrier()
@@ -474,11 +523,15 @@ def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, pea
     with sampler:
         e0.record(stream)
         for i in range(nsteps):
-            m.eval_frames(frames[i * nb:(i + 1) * nb], levels, out=outs[i % 2])
+            batch(i, timed_last=i == nsteps - 1)
+        stream.wait_stream(side)
+        table = gather_summaries(summ[:nsteps * nb], nsteps * nb * world, world, rank, device=dev)
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
+    summary_ms = ev_s[0][0].elapsed_time(ev_s[0][1]) if nsteps else 0.0
+    table_rows = int(table.shape[0])
     total_frames = nsteps * nb * world
     value = total_frames * Fout / (ms / 1000.0)
     bytes_per_frame = sum(12 * cnt[l]["V"] + 12 * cnt[l + 1]["V"] for l in range(levels))
@@ -486,6 +539,7 @@ def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, pea
     if not emit:
         m.close()
         return {"frames": total_frames, "faces_per_frame": Fout, "ms_per_batch_of_8": ms / nsteps,
+                "summary_ms_per_batch": summary_ms,
                 "faces_per_s": value, "position_GBps": gbps, "position_frac": gbps / peak if gbps else None}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "faces/s", "n_gpus": world, "steps": nsteps,
@@ -498,7 +552,9 @@ def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, pea
                 "roofline": {"bound": "hbm", "achieved": gbps, "peak": peak, "unit": "GB/s",
                              "frac": gbps / peak if gbps else None, "traffic": None,
                              "kernel": "whole static eval (position bytes only)", "peak_source": peak_src},
-                "cpu_baseline": None, "e2e": None, "gpu_launches": int(m.last_launch_count * nsteps),
+                "summaries": {"frames_gathered": table_rows, "bytes_per_frame": 32, "collective": "all_gather (NCCL)"
+                              if world > 1 else "none (1 rank)", "summary_ms_per_batch": summary_ms},
+                "cpu_baseline": None, "e2e": None, "gpu_launches": int((m.last_launch_count + 3) * nsteps),
                 "clocks": sampler.summary()}
         print(json.dumps(line), flush=True)
     m.close()

@@ -207,6 +207,17 @@ alsub_status alsub_extract_maps(const alsub_mesh *mesh, int32_t *vtx_map, int32_
 alsub_status alsub_rcm_order(const int32_t *face_off, const int32_t *face_vtx, int32_t num_faces, int32_t num_verts,
                              int32_t *perm_vtx, int32_t *perm_face);
 
+/* Per-frame result summary of a batch of frames (what the sharded config-5 job
+ * gathers over NCCL -- 32 B per frame instead of the frame).  frames: DEVICE fp32 [num_frames]
+ * [num_verts][3] (e.g. the output of alsub_eval_frames); summary: DEVICE, num_frames records of
+ * 32 bytes = { float lo[3], hi[3]; uint64_t sum; } with lo/hi the bounding box (exact fp32 min /
+ * max; -0 orders below +0) and sum = sum_i bits(x_i) * (2 i + 1) mod 2^64 over the frame's 3V
+ * floats in memory order (exact and order-independent, so the record is deterministic).
+ * Stream-ordered, no host sync.  Errors: E_ARG (negative counts, null or host pointers,
+ * num_frames > 65535), E_CUDA. */
+alsub_status alsub_frame_summary(const float *frames, int32_t num_frames, int64_t num_verts, void *summary,
+                                 void *stream);
+
 /* Number of kernel launches issued by the last alsub_refine / alsub_eval_frames call
  * (a graph replay counts the kernels inside it). */
 int64_t alsub_last_launch_count(const alsub_mesh *mesh);

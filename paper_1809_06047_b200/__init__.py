@@ -6,4 +6,4 @@
     P6 = m.positions(6); T6 = m.topology(6)             # alsub_level_positions / _topology
 """
 from .alsub import (AlsubError, CATMULL_CLARK, LOOP, SQRT3, SCHEMES, Mesh, lib, rcm_order, version,  # noqa: F401
-                    exported_symbols, LIB_PATH)
+                    frame_summary, split_summary, exported_symbols, LIB_PATH)

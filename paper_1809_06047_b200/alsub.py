@@ -76,6 +76,7 @@ def lib():
     L.alsub_refinement_matrix_csr.argtypes = [vp, vp, vp, vp, vp]
     L.alsub_eval_frames_matrix.argtypes = [vp, vp, i32, vp, vp]
     L.alsub_extract_maps.argtypes = [vp, vp, vp, vp]
+    L.alsub_frame_summary.argtypes = [vp, i32, i64, vp, vp]
     L.alsub_last_launch_count.argtypes = [vp]
     L.alsub_last_launch_count.restype = i64
     L.alsub_mesh_destroy.argtypes = [vp]
@@ -86,7 +87,7 @@ def lib():
               "alsub_level_topology", "alsub_level_positions", "alsub_eval_frames", "alsub_eval_attributes",
               "alsub_level_positions_ptr", "alsub_reevaluate", "alsub_rcm_order", "alsub_mesh_extract",
               "alsub_extract_maps", "alsub_build_refinement_matrix", "alsub_refinement_matrix_info",
-              "alsub_refinement_matrix_csr", "alsub_eval_frames_matrix"):
+              "alsub_refinement_matrix_csr", "alsub_eval_frames_matrix", "alsub_frame_summary"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -360,6 +361,25 @@ def rcm_order(face_off, face_vtx, num_verts):
     pf = np.empty(F, dtype=np.int32)
     _check(lib().alsub_rcm_order(_ptr(fo), _ptr(fv), F, int(num_verts), _ptr(pv), _ptr(pf)))
     return pv, pf
+
+
+def frame_summary(frames, out=None, stream=None):
+    """Per-frame summary records of a CUDA fp32 batch [B][V][3] (alsub_frame_summary): returns an
+    int32 CUDA tensor [B][8]; use split_summary() for (bbox float32 [B][6], checksum uint64 [B])."""
+    if not (isinstance(frames, torch.Tensor) and frames.is_cuda):
+        raise TypeError("frame_summary needs a CUDA tensor")
+    fr = frames.contiguous()
+    B, V = int(fr.shape[0]), int(fr.shape[1])
+    if out is None:
+        out = torch.empty((B, 8), dtype=torch.int32, device=fr.device)
+    _check(lib().alsub_frame_summary(_ptr(fr), B, V, _ptr(out), _stream(stream)))
+    return out
+
+
+def split_summary(rec):
+    """(bbox float32 [B][6] = lo.xyz, hi.xyz; checksum uint64 [B]) of summary records (numpy)."""
+    a = np.ascontiguousarray(rec.cpu().numpy() if isinstance(rec, torch.Tensor) else rec, dtype=np.int32)
+    return a[:, :6].view(np.float32), a[:, 6:8].copy().view(np.uint64).reshape(-1)
 
 
 def version():

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "lib", "libalsub.so")
-SOURCES = ["prims.cu", "build0.cu", "cc.cu", "crease.cu", "loop_sqrt3.cu", "api.cu", "extract.cu", "rmatrix.cu", "reorder.cpp"]
+SOURCES = ["prims.cu", "build0.cu", "cc.cu", "crease.cu", "loop_sqrt3.cu", "api.cu", "extract.cu", "rmatrix.cu", "summary.cu", "reorder.cpp"]
 HEADERS = ["common.cuh", "internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

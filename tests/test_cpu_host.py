@@ -68,9 +68,20 @@ def _gloo_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     lo, hi = bench.shard(4096, world, rank)
     m = bench.dist_max(10.0 + rank)
+    # the frames job's one data collective: every rank's summary records, gathered in frame order
+    import torch
+    n = 4096
+    local = torch.arange(lo, hi, dtype=torch.int32)[:, None] * 8 + torch.arange(8, dtype=torch.int32)
+    table = bench.gather_summaries(local, n, world, rank)
+    table_ok = bool(torch.equal(table, torch.arange(8 * n, dtype=torch.int32).view(n, 8)))
+    # uneven shards (odd frame count) are padded for the collective and trimmed again
+    lo2, hi2 = bench.shard(7, world, rank)
+    local2 = torch.arange(lo2, hi2, dtype=torch.int32)[:, None].repeat(1, 8)
+    t2 = bench.gather_summaries(local2, 7, world, rank)
+    table_ok = table_ok and bool(torch.equal(t2[:, 0], torch.arange(7, dtype=torch.int32)))
     dist.barrier()
     dist.destroy_process_group()
-    q.put((rank, lo, hi, m))
+    q.put((rank, lo, hi, m, table_ok))
 
 
 def test_gloo_sharding_and_max_over_ranks():
@@ -87,6 +98,7 @@ def test_gloo_sharding_and_max_over_ranks():
         p.join(timeout=60)
     assert res[0][1:3] == (0, 2048) and res[1][1:3] == (2048, 4096)
     assert res[0][3] == res[1][3] == 11.0
+    assert res[0][4] and res[1][4]
 
 
 def test_shard_covers_all_units():

@@ -551,3 +551,59 @@ def test_high_valence_vertices(scheme):
     """Valence-40 apices: M^T rows longer than a warp's fast path (serial fallbacks), valence
     constants beyond the common range, long crease-free rings."""
     compare(mg.bipyramid(40), scheme, 2, edges=scheme != "sqrt3")
+
+
+def _summary_np(frames):
+    """Plain numpy definition of alsub_frame_summary (include/alsub.h): bbox and the wrapping
+    checksum sum_i bits(x_i) (2 i + 1) mod 2^64 over each frame's floats in memory order."""
+    B = frames.shape[0]
+    flat = np.ascontiguousarray(frames, dtype=np.float32).reshape(B, -1)
+    bits = flat.view(np.uint32).astype(np.uint64)
+    w = 2 * np.arange(flat.shape[1], dtype=np.uint64) + np.uint64(1)
+    with np.errstate(over="ignore"):
+        cs = (bits * w[None, :]).sum(axis=1, dtype=np.uint64)
+    xyz = flat.reshape(B, -1, 3)
+    return xyz.min(axis=1), xyz.max(axis=1), cs
+
+
+def test_frame_summary_matches_numpy():
+    """The per-frame records the sharded frames job gathers (bench.py --config 5): exact bbox and
+    checksum, for ragged sizes (V not a multiple of the block), one vertex, signed zeros."""
+    from paper_1809_06047_b200 import frame_summary, split_summary
+    g = np.random.default_rng(1809)
+    for B, V in ((1, 1), (3, 257), (5, 100_003), (2, 1_000_000)):
+        fr = g.standard_normal((B, V, 3)).astype(np.float32)
+        if V > 2:
+            fr[0, 1] = [-0.0, 0.0, -0.0]
+        rec = frame_summary(torch.from_numpy(fr).cuda())
+        bb, cs = split_summary(rec)
+        lo, hi, want = _summary_np(fr)
+        assert np.array_equal(bb[:, :3], lo) and np.array_equal(bb[:, 3:], hi), (B, V)
+        assert np.array_equal(cs, want), (B, V)
+    # a frame batch that starts off 16-B alignment (scalar path) and one with V % 4 == 0 (float4 path)
+    big = torch.from_numpy(g.standard_normal(4 * 1000 * 3 + 1).astype(np.float32)).cuda()
+    for fr_t in (big[1:].view(4, 1000, 3), big[:-1].view(4, 1000, 3)):
+        bb, cs = split_summary(frame_summary(fr_t))
+        lo, hi, want = _summary_np(fr_t.cpu().numpy())
+        assert np.array_equal(cs, want) and np.array_equal(bb[:, :3], lo) and np.array_equal(bb[:, 3:], hi)
+    # deterministic: two calls give identical records; a one-ulp change moves the checksum
+    fr = torch.from_numpy(g.standard_normal((4, 5000, 3)).astype(np.float32)).cuda()
+    a, b = frame_summary(fr), frame_summary(fr)
+    assert torch.equal(a, b)
+    fr2 = fr.clone()
+    fr2.view(torch.int32)[2, 1234, 1] += 1
+    c = frame_summary(fr2)
+    assert torch.equal(a[[0, 1, 3]], c[[0, 1, 3]]) and not torch.equal(a[2], c[2])
+
+
+def test_frame_summary_of_eval_frames_output():
+    """Summaries of a refined frame batch equal numpy's over the same output."""
+    from paper_1809_06047_b200 import Mesh, frame_summary, split_summary
+    mesh = mg.armor(6, 5, 6, 1, 1, 2, name="armor_small")
+    frames = np.stack([mg.frame_positions(mesh["pos"], t, 8) for t in range(8)])
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine("cc", 3)
+        out = m.eval_frames(torch.from_numpy(frames).cuda(), 3)
+        bb, cs = split_summary(frame_summary(out))
+        lo, hi, want = _summary_np(out.cpu().numpy())
+        assert np.array_equal(cs, want) and np.array_equal(bb[:, :3], lo) and np.array_equal(bb[:, 3:], hi)
