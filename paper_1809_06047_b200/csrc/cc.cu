@@ -29,15 +29,20 @@ ALSUB_D int32_t cc_base(const uint32_t *w, const int32_t *wp, int32_t e) {
 // ---------------- face kernel: reduced quad matrix (levels >= 1, or all-quad input) --------
 // Each thread owns one parent quad and produces 4 child rows (64 B) per output array; a warp's
 // 32 x 64 B = 2 KB are staged in shared memory and written back as 4 fully coalesced 512 B
-// stores (child rows 4 r0 .. 4 r0 + 127 are contiguous).
+// stores (child rows 4 r0 .. 4 r0 + 127 are contiguous).  Row t of lane l sits at slot
+// 4 l + ((t + l/2) mod 4): with the plain slot 4 l + t the 32 lanes' 16-B stores of one t fall on
+// 8 of the 32 banks (16 wavefronts instead of 4 -- ncu showed the kernel L1-data-pipe bound on
+// these conflicts); the rotation spreads them over all banks, and the read-back (four lanes per
+// source lane, a permutation of its 4 slots) stays conflict-free.
 ALSUB_D void warp_store_rows(int4 *stage, const int4 (&rows)[4], int4 *dst, int64_t row0, int64_t nrows, int lane) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) stage[lane * 4 + t] = rows[t];
+    for (int t = 0; t < 4; ++t) stage[lane * 4 + ((t + (lane >> 1)) & 3)] = rows[t];
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int64_t rr = row0 + k * 32 + lane;
-        if (rr < nrows) dst[rr] = stage[k * 32 + lane];
+        const int src = k * 8 + (lane >> 2), t = lane & 3;
+        if (rr < nrows) dst[rr] = stage[src * 4 + ((t + (src >> 1)) & 3)];
     }
     __syncwarp();
 }
@@ -310,8 +315,12 @@ template <int NBC>
 __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp, ChildDev c, Frames fr) {
     ALSUB_GRID_WAIT();
     // the block's children are the contiguous id range [base(e_first), base(e_last) + nch): staged
-    // in shared memory and written back as one coalesced float run
-    __shared__ float s_out[4 * kThreads * 3];
+    // in shared memory and written back as one coalesced float run.  Staging is one array per
+    // coordinate, child a at a + a/32 (thread t's children start near 4 t, so without the skew a
+    // warp's stores of one child k land on 8 banks); rows kSo floats apart (kSo = 11 mod 32) so the
+    // read-back's x/y/z of neighbouring children fall on different banks
+    constexpr int kSo = 4 * kThreads + 4 * kThreads / 32 + 11;
+    __shared__ float s_out[3 * kSo];
     __shared__ int32_t s_base0, s_end;
     const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = e < gp.E;
@@ -362,18 +371,24 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
             }
 
             for (int k = 0; k < nch; ++k) {
-                s_out[3 * (o + k) + 0] = q[k].x;
-                s_out[3 * (o + k) + 1] = q[k].y;
-                s_out[3 * (o + k) + 2] = q[k].z;
+                const int a = o + k, sa = a + (a >> 5);
+                s_out[sa] = q[k].x;
+                s_out[kSo + sa] = q[k].y;
+                s_out[2 * kSo + sa] = q[k].z;
             }
         }
         __syncthreads();
         if (Pn.vs == 3) {
             float *dst = Pn.p + 3 * ((int64_t)V + F + base0);
-            for (int32_t i = threadIdx.x; i < 3 * n; i += blockDim.x) dst[i] = s_out[i];
+            for (int32_t i = threadIdx.x; i < 3 * n; i += blockDim.x) {
+                const int32_t a = i / 3, cc = i - 3 * a;
+                dst[i] = s_out[cc * kSo + a + (a >> 5)];
+            }
         } else {
-            for (int32_t i = threadIdx.x; i < n; i += blockDim.x)
-                st3(Pn, (int64_t)V + F + base0 + i, P3{s_out[3 * i], s_out[3 * i + 1], s_out[3 * i + 2]});
+            for (int32_t a = threadIdx.x; a < n; a += blockDim.x) {
+                const int32_t sa = a + (a >> 5);
+                st3(Pn, (int64_t)V + F + base0 + a, P3{s_out[sa], s_out[kSo + sa], s_out[2 * kSo + sa]});
+            }
         }
         __syncthreads();
     }

@@ -107,14 +107,20 @@ ALSUB_D int32_t loop_inner(const LevelDev &p, int32_t m, int32_t x, int32_t z, i
 
 // a warp's 32 x 12 child-row ints (4 child triangles per face) staged in shared memory and written
 // as 12 coalesced 128-B stores
+// word q of the warp's 384 sits at q + q / 96: the stores of one k from lanes l, l + 8, l + 16,
+// l + 24 (96 words apart) would otherwise share a bank (4-way conflicts)
 ALSUB_D void warp_store_12(int32_t *stage, const int32_t (&v)[12], int32_t *dst, int64_t w0, int64_t n, int lane) {
 #pragma unroll
-    for (int k = 0; k < 12; ++k) stage[lane * 12 + k] = v[k];
+    for (int k = 0; k < 12; ++k) {
+        const int q = lane * 12 + k;
+        stage[q + q / 96] = v[k];
+    }
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
         const int64_t o = w0 + k * 32 + lane;
-        if (o < n) dst[o] = stage[k * 32 + lane];
+        const int q = k * 32 + lane;
+        if (o < n) dst[o] = stage[q + q / 96];
     }
     __syncwarp();
 }
@@ -122,7 +128,7 @@ ALSUB_D void warp_store_12(int32_t *stage, const int32_t (&v)[12], int32_t *dst,
 template <bool ADJ>
 __global__ void __launch_bounds__(kThreads) k_loop_face(LevelDev p, ChildDev c) {
     ALSUB_GRID_WAIT();
-    __shared__ int32_t s_stage[kThreads / 32][12 * 32];
+    __shared__ int32_t s_stage[kThreads / 32][12 * 32 + 4];
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = r < p.F;
     const int lane = threadIdx.x & 31;
