@@ -62,9 +62,14 @@ ALSUB_D int4 child_edge_row(const LevelDev &gp, int32_t r) {
                      bq + (v[t] > v[tp]));
 }
 
+// fpo >= 0 (levels l >= 3): first id of the face points born at level l-1.  The face point of
+// level-(l-2) quad j is corner 0 of exactly the four level-l faces 16 j + 4 t + 2 (t = 0..3, the
+// corner-2 children of its four level-(l-1) faces), i.e. lanes 2, 6, 10, 14 of a 16-lane group:
+// its vertex point 1/2 p + 1/16 sum_t c0[16 j + 4 t + 2] is a shuffle reduction here instead of
+// four c0 gathers in the vertex kernel.
 template <bool ADJ, bool BND, int NBC, bool GPE>
 __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev c, Frames fr, bool topo, bool fpv,
-                                                         LevelDev gp) {
+                                                         LevelDev gp, int32_t fpo) {
     ALSUB_GRID_WAIT();
     __shared__ int4 s_stage[kThreads / 32][128];
     const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -89,6 +94,16 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
         const P3 fc = 0.25f * (p0 + p1 + p2 + p3);
         if (valid) st3(Pn, V + r, fc);
         if (valid && fr.c0) st3(fr.c0w(f), r, p1 + fc);
+        if (fpo >= 0) {
+            P3 acc = p1 + fc;
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 4);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 4);
+            acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 4);
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 8);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 8);
+            acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 8);
+            if (valid && (lane & 15) == 2) st3(Pn, (int64_t)fpo + (r >> 4), 0.5f * p0 + 0.0625f * acc);
+        }
         if (fpv) {
             // (1) the edge point of parent slot r (born at this level) sits at corner 1 of child
             // r and corner 3 of child r+1 (mod 4): its half ring sum from this parent face is
@@ -671,19 +686,29 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
 
 // ------------------------------------------------------------------------------------------
 template <int ORDER, bool ADJ, bool BND>
-static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, const VSegs &g,
+static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, const VSegs &g0,
                       const LevelDev *gp, cudaStream_t s, Launches &L) {
-    const bool fpv = g.level >= 2;  // face points born at this level are smoothed by the face kernel
+    const bool fpv = g0.level >= 2;  // face points born at this level are smoothed by the face kernel
     const bool one = fr.nb == 1;
     const LevelDev gpd = gp ? *gp : LevelDev{};
+    // levels >= 3 (quad kernel, c0 stored): the face points born at level l-1 are smoothed by the
+    // face kernel too (a shuffle over the 4 faces around each); the vertex kernel skips them
+    VSegs g = g0;
+    int32_t fpo = -1;
+    if (ORDER == 4 && fr.c0 && g.level >= 3)
+        for (int k = 0; k < g.nseg; ++k)
+            if (g.type[k] == 1 && g.birth[k] == g.level - 1 && g.len[k] > 0) {
+                fpo = g.start[k];
+                g.len[k] = 0;
+            }
     if (p.F > 0) {
         if constexpr (ORDER == 4) {
             if (gp) {
-                if (one) launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 1, true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd);
-                else launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 0, true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd);
+                if (one) launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 1, true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd, fpo);
+                else launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 0, true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd, fpo);
             } else {
-                if (one) launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 1, false>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd);
-                else launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 0, false>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd);
+                if (one) launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 1, false>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd, fpo);
+                else launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 0, false>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd, fpo);
             }
         } else {
             if (one) launch(L, "cc_face", k_cc_face_gen<ORDER, ADJ, BND, 1>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo);

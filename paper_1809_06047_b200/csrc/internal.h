@@ -1,5 +1,6 @@
 // internal.h -- host-side declarations shared by the AlSub CUDA translation units.
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -17,7 +18,11 @@ struct Launches {
     // inside stream capture this becomes parallel graph branches)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    bool can_fork() const { return side != nullptr && !timing; }
+    bool can_fork() const { return side != nullptr && !timing && !no_fork(); }
+    static bool no_fork() {  // ALSUB_NO_FORK=1: one branch (experiments)
+        static const bool v = [] { const char *e = getenv("ALSUB_NO_FORK"); return e && e[0] == '1'; }();
+        return v;
+    }
     // optional per-kernel timing (alsub_refine_profile): an event after every launch
     bool timing = false;
     int level = -1;
