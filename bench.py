@@ -55,7 +55,7 @@ def level_counts(m, levels):
     return out
 
 
-def kernel_bytes_cc(name, c, prev, lvl, levels):
+def kernel_bytes_cc(name, c, prev, lvl, levels, prev2=None):
     """Algorithmic bytes of one launch of a CC level kernel: every array the
     kernel reads or writes, counted once.  c = counts of the parent level lvl, prev = level lvl-1.
     Mirrors the plan in api.cu: the last refined level (lvl = levels-1 >= 2) recomputes its edge
@@ -64,6 +64,8 @@ def kernel_bytes_cc(name, c, prev, lvl, levels):
     V, F, S, E = c["V"], c["F"], c["S"], c["E"]
     Fp = prev["F"] if prev else 0
     Ep = prev["E"] if prev else 0
+    Fq = prev2["F"] if (prev2 and lvl >= 3) else 0   # face points born at lvl-1 (face-kernel shuffle)
+    Eq = prev2["E"] if (prev2 and lvl >= 2) else 0   # edge points born at lvl-1 (last level: edge kernel)
     adj = lvl < levels - 1                        # this level emits child adjacency
     gp_last = levels >= 3 and lvl == levels - 1   # grandparent path at the last level
     child_rows = adj and not (levels >= 3 and lvl + 1 == levels - 1)  # child face_edge / edge pairs stored
@@ -73,6 +75,7 @@ def kernel_bytes_cc(name, c, prev, lvl, levels):
         rd = 4 * S + 12 * V + (48 * Fp if gp_last else 4 * S) + (4 * S if adj else 0)
         wr = 12 * F + 16 * S + (16 * S if child_rows else 0) + (16 * S if child_twin else 0)
         wr += 12 * Fp if fpv else 0               # new face-point vertices
+        wr += 12 * Fq                             # face points born at lvl-1
         wr += 12 * F if (fpv and not gp_last) else 0  # half ring sums (the last level has none)
         wr += 12 * F if lvl >= 1 else 0             # corner-0 contributions c0
     elif name == "cc_edge":
@@ -81,13 +84,15 @@ def kernel_bytes_cc(name, c, prev, lvl, levels):
         else:
             rd = 8 * E + 4 * S + 12 * V + 12 * F
         wr = 12 * E + (8 * (2 * E + S) if child_rows else 0)
-        wr += 12 * Ep if gp_last else 0           # vertex points of the edge points born at lvl
+        wr += 12 * (Ep + Eq) if gp_last else 0    # vertex points of the edge points born at lvl, lvl-1
     elif name == "cc_vertex":
-        if gp_last:  # vertices born before lvl only: p + their faces' c0 (each read once)
-            nv = V - Fp - Ep
-            return 12 * nv + 12 * F + 12 * nv
+        if gp_last:  # vertices born before lvl-1 only: p + their faces' c0 (each read once)
+            nv = V - Fp - Ep - Fq - Eq
+            return 12 * nv + 12 * (F - 4 * Fq - 4 * Eq) + 12 * nv
+        if Fq:  # the face points born at lvl-1 are done by the face kernel
+            V = V - Fq
         if lvl >= 1:  # c0 sums for vertices born earlier, half sums for new edge points
-            rd = 12 * V + 12 * F + 8 * Ep + (12 * F if fpv else 0) + (0 if fpv else 4 * S + 12 * F)
+            rd = 12 * V + 12 * (F - 4 * Fq) + 8 * Ep + (12 * F if fpv else 0) + (0 if fpv else 4 * S + 12 * F)
         else:
             rd = 4 * S + 12 * V + 12 * F
         wr = 12 * (V - (Fp if fpv else 0))
@@ -332,14 +337,16 @@ def run_alsub(args):
             row["survey_frac"] = row["survey_GBps"] / peak if row["survey_GBps"] else None
             kk = {}
             for n, t in ks.items():
-                b = kernel_bytes_cc(n, c, cnt[lvl - 1] if lvl > 0 else None, lvl, levels)
+                b = kernel_bytes_cc(n, c, cnt[lvl - 1] if lvl > 0 else None, lvl, levels,
+                                    cnt[lvl - 2] if lvl > 1 else None)
                 kk[n] = {"ms": t, "alg_bytes": b, "GBps": (b / (t * 1e6)) if b else None,
                          "frac": (b / (t * 1e6) / peak) if b else None}
             row["kernels"] = kk
         per_level.append(row)
     # dominant kernel = the largest share of the step
     (dname, dlvl), dms = max(kt.items(), key=lambda kv: kv[1])
-    dbytes = kernel_bytes_cc(dname, cnt[dlvl], cnt[dlvl - 1] if dlvl > 0 else None, dlvl, levels) \
+    dbytes = kernel_bytes_cc(dname, cnt[dlvl], cnt[dlvl - 1] if dlvl > 0 else None, dlvl, levels,
+                             cnt[dlvl - 2] if dlvl > 1 else None) \
         if dlvl >= 0 else None
     achieved = dbytes / (dms * 1e6) if dbytes else None
     traffic = None

@@ -533,6 +533,8 @@ static VSegs make_segs(alsub_mesh *m, int l) {
         g.spw[k - 1] = q.spw;
         g.spwpre[k - 1] = q.spwpre;
         g.nsvb[k - 1] = (int32_t)q.nsv;
+        g.bw[k - 1] = q.B > 0 ? q.bnd_word : nullptr;
+        g.bwp[k - 1] = q.B > 0 ? q.bnd_wpre : nullptr;
     }
     g.nseg = n;
     g.hs_seg = l >= 2 ? n - 1 : -1;  // the last segment = edge points born at level l

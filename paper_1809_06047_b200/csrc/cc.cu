@@ -326,8 +326,17 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
 //   S(ep) = 1/2 p_ep + 1/16 (p_lo + p_hi + p_R + p_S + f_h + f_next(h) + f_tw + f_next(tw))
 // (Eq. pos_update with n = 4) is stored here too, at id ep (coalesced: consecutive e).
 // Boundary edge points keep p; the crease pass overwrites every special vertex afterwards.
+// epo >= 0: first id of the edge points born at level l-1 (ids [epo, V_{l-1})).  Such a vertex x =
+// ep(e'') of a level-(l-2) edge e'' is the max endpoint of exactly the level-(l-1) edges
+// base(e'') .. base(e'') + 3 (interior e''), consecutive threads here, and each of those threads
+// holds one ring term: x's next vertex in one incident level-l face is the thread's edge point,
+// and the thread's two faces at x are two of x's four (each counted by two threads).  So
+//   S(x) = 1/2 p_x + 1/16 sum_k (p_ep_k + 1/2 (f_a_k + f_b_k))
+// is a block-shared sum over the group when all four threads are in one block (the vertex kernel
+// does the few groups that straddle a block boundary, and boundary e'').
 template <int NBC>
-__global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp, ChildDev c, Frames fr) {
+__global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp, ChildDev c, Frames fr,
+                                                       int32_t epo) {
     ALSUB_GRID_WAIT();
     // the block's children are the contiguous id range [base(e_first), base(e_last) + nch): staged
     // in shared memory and written back as one coalesced float run.  Staging is one array per
@@ -349,7 +358,8 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
     const int32_t Vg = gp.V, Fg = gp.F;
     const int32_t ep = Vg + Fg + e, fpR = Vg + R, fpS = tw >= 0 ? Vg + (tw >> 2) : 0;
     const int32_t nh = (h & ~3) | ((h + 1) & 3), nt = tw >= 0 ? ((tw & ~3) | ((tw + 1) & 3)) : 0;
-    const int32_t base = valid ? 4 * e - (gp.B > 0 ? bprefix(gp.bnd_word, gp.bnd_wpre, e) : 0) : 0;
+    const int32_t bp = (valid && gp.B > 0) ? bprefix(gp.bnd_word, gp.bnd_wpre, e) : 0;
+    const int32_t base = valid ? 4 * e - bp : 0;
     const int32_t nch = tw < 0 ? 3 : 4;
     const int32_t last = min((int32_t)(blockIdx.x * blockDim.x + blockDim.x), gp.E) - 1;
     if (threadIdx.x == 0) s_base0 = base;
@@ -360,14 +370,25 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
     const int32_t f1a = fwd ? tw : h, f1b = fwd ? nh : nt;  // faces of (hi, ep)
     const int32_t V = p.V, F = p.F;
     const int nb = NBC ? NBC : fr.nb;
+    // ring-sum group of hi (an edge point born at level l-1): position k in its group
+    // (bprefix(e) = 2 bprefix''(e'') inside an interior group, so k = e - base(e''))
+    __shared__ float s_ring[3][kThreads + 1];
+    __shared__ int32_t s_hi[kThreads];
+    const bool inx = valid && epo >= 0 && hi >= epo && hi < Vg && tw >= 0;
+    s_hi[threadIdx.x] = inx ? hi : -1;
     __syncthreads();
+    bool lead = false;
+    if (inx && e - 4 * (hi - epo) + (bp >> 1) == 0 && threadIdx.x + 3 < blockDim.x)
+        lead = s_hi[threadIdx.x + 1] == hi && s_hi[threadIdx.x + 2] == hi && s_hi[threadIdx.x + 3] == hi;
     const int32_t base0 = s_base0, n = s_end - base0;
     const int32_t o = base - base0;
     for (int f = 0; f < nb; ++f) {
         const PR P = fr.rd(f);
         const PW Pn = fr.wr(f);
+        P3 phx = p3zero();
         if (valid) {
             const P3 plo = ld3(P, lo), phi = ld3(P, hi), pep = ld3(P, ep), pR = ld3(P, fpR);
+            phx = phi;
             const P3 fh = ld3c(Pn, V + h), fnh = ld3c(Pn, V + nh);
             P3 q[4];
             q[2] = 0.25f * (pR + pep + fh + fnh);
@@ -383,6 +404,13 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
                 q[1] = 0.25f * (phi + pep + fb);
                 q[3] = 0.25f * (pS + pep + ft + fnt);
                 st3(Pn, ep, 0.5f * pep + 0.0625f * ((plo + phi) + (pR + pS) + (fh + fnh) + (ft + fnt)));
+                if (inx) {
+                    const P3 fx = fwd ? (fnh + ft) : (fh + fnt);  // this edge's two faces at hi
+                    const P3 rt = pep + 0.5f * fx;
+                    s_ring[0][threadIdx.x] = rt.x;
+                    s_ring[1][threadIdx.x] = rt.y;
+                    s_ring[2][threadIdx.x] = rt.z;
+                }
             }
 
             for (int k = 0; k < nch; ++k) {
@@ -393,6 +421,13 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
             }
         }
         __syncthreads();
+        if (lead) {
+            const int t0 = threadIdx.x;
+            const P3 acc{(s_ring[0][t0] + s_ring[0][t0 + 1]) + (s_ring[0][t0 + 2] + s_ring[0][t0 + 3]),
+                         (s_ring[1][t0] + s_ring[1][t0 + 1]) + (s_ring[1][t0 + 2] + s_ring[1][t0 + 3]),
+                         (s_ring[2][t0] + s_ring[2][t0 + 1]) + (s_ring[2][t0 + 2] + s_ring[2][t0 + 3])};
+            st3(Pn, hi, 0.5f * phx + 0.0625f * acc);
+        }
         if (Pn.vs == 3) {
             float *dst = Pn.p + 3 * ((int64_t)V + F + base0);
             for (int32_t i = threadIdx.x; i < 3 * n; i += blockDim.x) {
@@ -679,28 +714,51 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
         }
         for (int k = 0; k < PL; ++k) {
             const int32_t j = j0 + 32 * k;
-            if (j < len) cc_vertex_one<ORDER, CR>(x, fr, g, p, csv_list, s, j);
+            if (j >= len) continue;
+            if (s == g.gp_skip_seg) {
+                // done by k_cc_edge_gp when the 4 child edges of interior edge j (ids base ..
+                // base + 3) are in one of its blocks
+                const int m1 = g.birth[s] - 1;
+                if (__ldg(g.ehh[m1] + j).y >= 0) {
+                    const int32_t base = 4 * j - (g.bw[m1] ? bprefix(g.bw[m1], g.bwp[m1], j) : 0);
+                    if ((base & (kThreads - 1)) <= kThreads - 4) continue;
+                }
+            }
+            cc_vertex_one<ORDER, CR>(x, fr, g, p, csv_list, s, j);
         }
     }
 }
 
 // ------------------------------------------------------------------------------------------
 template <int ORDER, bool ADJ, bool BND>
-static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, const VSegs &g0,
+static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, bool topo, const VSegs &g0,
                       const LevelDev *gp, cudaStream_t s, Launches &L) {
     const bool fpv = g0.level >= 2;  // face points born at this level are smoothed by the face kernel
-    const bool one = fr.nb == 1;
+    const bool one = fr0.nb == 1;
     const LevelDev gpd = gp ? *gp : LevelDev{};
     // levels >= 3 (quad kernel, c0 stored): the face points born at level l-1 are smoothed by the
     // face kernel too (a shuffle over the 4 faces around each); the vertex kernel skips them
     VSegs g = g0;
     int32_t fpo = -1;
-    if (ORDER == 4 && fr.c0 && g.level >= 3)
+    if (ORDER == 4 && g.level >= 3)
         for (int k = 0; k < g.nseg; ++k)
             if (g.type[k] == 1 && g.birth[k] == g.level - 1 && g.len[k] > 0) {
                 fpo = g.start[k];
                 g.len[k] = 0;
             }
+    // the last level (grandparent path): the edge points born at l-1 come from the edge kernel's
+    // block sums (the face points born at l-1 from the face kernel's shuffle, above); the older
+    // vertices sum their faces' corner sums c0 (dropping c0 at this level and gathering their rings
+    // directly was measured slower: 0.715 -> 0.731 ms on config 3)
+    const Frames &fr = fr0;
+    int32_t epo = -1;
+    if (gp) {
+        for (int k = 0; k < g.nseg; ++k)
+            if (g.type[k] == 2 && g.birth[k] == g.level - 1 && g.len[k] > 0) {
+                epo = g.start[k];
+                g.gp_skip_seg = k;
+            }
+    }
     if (p.F > 0) {
         if constexpr (ORDER == 4) {
             if (gp) {
@@ -724,8 +782,8 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr, bo
         se = L.side;
     }
     if (gp && gp->E > 0) {
-        if (one) launch(L, "cc_edge", k_cc_edge_gp<1>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, c, fr);
-        else launch(L, "cc_edge", k_cc_edge_gp<0>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, c, fr);
+        if (one) launch(L, "cc_edge", k_cc_edge_gp<1>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, c, fr, epo);
+        else launch(L, "cc_edge", k_cc_edge_gp<0>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, c, fr, epo);
     } else if (p.E > 0) {
         constexpr int IT = 2;
         const unsigned gdim = grid_for(p.E, kThreads * IT);

@@ -245,6 +245,12 @@ struct VSegs {
     const uint32_t *spw[kMaxLevels];
     const int32_t *spwpre[kMaxLevels];
     int32_t nsvb[kMaxLevels];
+    // boundary words / per-word prefix of level m (for the structured child-edge ids 4e - bprefix)
+    const uint32_t *bw[kMaxLevels];
+    const int32_t *bwp[kMaxLevels];
+    // last refined level: segment of the edge points born at level l-1 whose vertex points the
+    // grandparent edge kernel already wrote (those whose 4 child edges fall in one of its blocks)
+    int32_t gp_skip_seg = -1;
 };
 
 // mode: adj = emit child adjacency (not the last level); topo = emit child faces;
