@@ -8,7 +8,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import meshgen as mg  # noqa: E402
-from paper_1809_06047_b200 import Mesh, rcm_order  # noqa: E402
+from paper_1809_06047_b200 import Mesh, frame_summary, rcm_order  # noqa: E402
 
 arm = mg.armor(6, 5, 6, 1, 1, 2, name="armor_small")
 with Mesh(arm["face_off"], arm["face_vtx"], arm["pos"], arm["crease"], arm["sigma"]) as m:
@@ -16,7 +16,9 @@ with Mesh(arm["face_off"], arm["face_vtx"], arm["pos"], arm["crease"], arm["sigm
     m.topology(3, edges=True, creases=True)
     m.topology(4, creases=True)
     fr = torch.stack([torch.from_numpy(mg.frame_positions(arm["pos"], t, 16)) for t in range(9)]).cuda()
-    m.eval_frames(fr, 4)
+    out4 = m.eval_frames(fr, 4)
+    frame_summary(out4)
+    frame_summary(out4[:, 1:].contiguous())
     m.eval_attributes(torch.from_numpy(mg.vertex_channels(arm, 4)).cuda(), 3)
     v = m.level_positions_view(2)
     v += 0.01
