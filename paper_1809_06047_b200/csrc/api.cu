@@ -105,6 +105,12 @@ struct alsub_mesh {
     cudaStream_t side_stream = nullptr;  // second branch for independent level kernels
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t last_launches = 0;
+    // the last refined level's special lists (crease pairs / sigma of level L and the level-L rows
+    // of the special-vertex table) are only read by exports and extraction: the refine skips their
+    // inheritance step and ensure_last_lists() builds them on first use (lazy_lists = plan property,
+    // lists_pending = not built since the last refine)
+    bool lazy_lists = false;
+    bool lists_pending = false;
     // refinement matrix R (NEXT-1): CSR rows of level rm_levels over the control vertices
     std::vector<std::pair<void *, size_t>> mem_rm;
     int32_t rm_levels = -1, rm_scheme = -1;
@@ -543,8 +549,29 @@ static VSegs make_segs(alsub_mesh *m, int l) {
     return g;
 }
 
+// build the last refined level's special lists (inheritance half of the crease module only: no
+// position writes, nb = 0) if the refine skipped them
+static void ensure_last_lists(alsub_mesh *m, cudaStream_t s) {
+    if (!m->lists_pending || m->levels < 1) return;
+    const int l = m->levels - 1;
+    LevelHost &P = m->lv[l];
+    LevelDev p = dev_of(P);
+    p.sv_vtx = m->sv_vtx;
+    p.sv_off = m->sv_off;
+    p.inherit = 1;
+    ChildDev c = child_of(m->lv[l + 1]);
+    c.sv_vtx = m->sv_vtx;
+    c.sv_off = m->sv_off;
+    Frames fr{nullptr, nullptr, 0, 0, 0, nullptr, 0};
+    Launches L;
+    const bool cc = m->scheme == ALSUB_CATMULL_CLARK;
+    crease_level(p, c, fr, cc ? (int32_t)(P.V + P.F) : (int32_t)P.V, cc ? 0 : 1, true, s, L);
+    m->lists_pending = false;
+}
+
 static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     const int scheme = m->scheme, levels = m->levels;
+    m->lazy_lists = false;
     L.side = m->side_stream;
     L.ev_fork = m->ev_fork;
     L.ev_join = m->ev_join;
@@ -590,11 +617,17 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
             // pass dominates there), a separate kernel on large ones (fusion costs occupancy)
             p.crease = (special && !use_gp && P.V < kFuseCreaseMaxV) ? 1 : 0;
             cc_level(p, c, fr, true, adj, g, use_gp ? &gp : nullptr, s, L);
-            if (special && !p.crease) crease_level(p, c, fr, (int32_t)(P.V + P.F), 0, true, s, L);
+            if (special && !p.crease) {
+                if (!adj) m->lazy_lists = true;  // last level: lists built on demand
+                crease_level(p, c, fr, (int32_t)(P.V + P.F), 0, adj, s, L);
+            }
         } else if (scheme == ALSUB_LOOP) {
             VSegs g = make_segs_loop(m, l);
             loop_level(p, c, fr, true, adj, P.loop_stat, (adj || special) ? P.loop_base : nullptr, g, s, L);
-            if (special) crease_level(p, c, fr, (int32_t)P.V, 1, true, s, L);
+            if (special) {
+                if (!adj) m->lazy_lists = true;
+                crease_level(p, c, fr, (int32_t)P.V, 1, adj, s, L);
+            }
         } else {
             VSegs g = make_segs_s3(m, l);
             sqrt3_level(p, c, fr, true, adj, g, s, L);
@@ -646,6 +679,7 @@ extern "C" alsub_status alsub_refine(alsub_mesh *m, alsub_scheme scheme, int32_t
         enqueue_refine(m, s, L);
         m->last_launches = L.n;
     }
+    m->lists_pending = m->lazy_lists;
     CU(cudaGetLastError());
     return ALSUB_OK;
 }
@@ -687,6 +721,7 @@ extern "C" alsub_status alsub_refine_profile(alsub_mesh *m, alsub_scheme scheme,
     cudaEventDestroy(start);
     if (n_out) *n_out = n;
     m->last_launches = L.n;
+    m->lists_pending = m->lazy_lists;
     return ALSUB_OK;
 }
 
@@ -784,6 +819,7 @@ extern "C" alsub_status alsub_level_topology(const alsub_mesh *mc, int32_t level
         if (df != edge_face) CU(copy_out(edge_face, df, sizeof(int32_t) * 2 * (size_t)L->E, s));
     }
     if (crease_pairs || crease_sigma || num_creases) {
+        if (level == m->levels) ensure_last_lists(m, s);
         int32_t cnt = (int32_t)L->nsp;
         std::vector<SpEdge> sp;
         if (L->sp && cnt > 0) {
@@ -846,6 +882,7 @@ extern "C" alsub_status alsub_mesh_extract(const alsub_mesh *m, int32_t level, c
     } else {
         const LevelHost &L = m->lv[level];
         const bool special = m->scheme != ALSUB_SQRT3 && m->K0 > 0;
+        if (special && level == m->levels) ensure_last_lists(const_cast<alsub_mesh *>(m), (cudaStream_t)stream);
         h = ExSrcHost{(int32_t)L.V, (int32_t)L.F, (int32_t)L.S, L.order, nullptr, L.face_vtx, L.pos,
                       special ? L.sp : nullptr, special ? (int32_t)L.nsp : 0};
     }

@@ -112,7 +112,9 @@ def test_oracle_locality_loop_masked():
 
 # ------------------------------------------------------------------------------------------ GPU
 @pytest.mark.gpu
-@pytest.mark.parametrize("level,mask,rings", [(0, None, 1), (0, "random", 2), (2, None, 1), (2, "random", 1)])
+# level 3 of a 3-level refine: the last level's crease lists are built lazily (on first use)
+@pytest.mark.parametrize("level,mask,rings", [(0, None, 1), (0, "random", 2), (2, None, 1), (2, "random", 1),
+                                              (3, "random", 1)])
 def test_gpu_extract_matches_oracle(level, mask, rings):
     from paper_1809_06047_b200 import Mesh
     mesh = _armor()
