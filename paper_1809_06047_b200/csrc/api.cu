@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/alsub.h"
 #include "internal.h"
 
@@ -549,6 +551,16 @@ static VSegs make_segs(alsub_mesh *m, int l) {
     return g;
 }
 
+// NVTX range (eager launches; `ncu --nvtx --nvtx-include "alsub level 5->6/"` selects a level)
+struct Nvtx {
+    Nvtx(const char *fmt, int a, int b) {
+        char buf[64];
+        snprintf(buf, sizeof buf, fmt, a, b);
+        nvtxRangePushA(buf);
+    }
+    ~Nvtx() { nvtxRangePop(); }
+};
+
 // build the last refined level's special lists (inheritance half of the crease module only: no
 // position writes, nb = 0) if the refine skipped them
 static void ensure_last_lists(alsub_mesh *m, cudaStream_t s) {
@@ -577,6 +589,7 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     L.ev_join = m->ev_join;
     // a1-a3: level-0 mesh matrix, M^T by counting sort, edge index, creases
     L.level = -1;
+    nvtxRangePushA("alsub level-0 build");
     {
         ZeroSegs z;
         build0_zero_segments(m->b0, z);
@@ -591,12 +604,14 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     build0_validate(m->b0, s, L);
     build0_count_edges(m->b0, s, L);
     build0_fill(m->b0, false, s, L);
+    nvtxRangePop();
     const bool special = scheme != ALSUB_SQRT3 && m->K0 > 0;
     for (int l = 0; l < levels; ++l) {
         LevelHost &P = m->lv[l];
         LevelHost &C = m->lv[l + 1];
         const bool adj = l + 1 < levels;
         L.level = l;
+        Nvtx range_level("alsub level %d->%d", l, l + 1);
         LevelDev p = dev_of(P);
         p.sv_vtx = m->sv_vtx;
         p.sv_off = m->sv_off;
