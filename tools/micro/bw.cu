@@ -1,7 +1,7 @@
 // micro-benchmark: HBM bandwidth on B200 for read-only, write-only, copy (1:1) and 1:2 / 1:3
-// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/micro/bw tools/micro/bw.cu
 // read:write float4 streams (grid = 148 SMs x 8 blocks, grid-stride), 1 GiB per array.
 // Used to bound the write-heavy last-level CC face kernel (~0.35 GB read, ~0.74 GB written).
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/micro/bw tools/micro/bw.cu
 #include <cstdio>
 #include <cuda_runtime.h>
 
