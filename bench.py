@@ -210,6 +210,20 @@ def gather_summaries(local, nframes, world, rank, device=None):
     return torch.cat(parts)
 
 
+def host_cpu():
+    """(model name, logical cores) of this host, for the oracle baseline's context."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
 def cpu_oracle_baseline(mesh, levels, label):
     """The oracle as it stands, single-threaded, on this host: faces/s of the final level."""
     import oracle
@@ -218,9 +232,30 @@ def cpu_oracle_baseline(mesh, levels, label):
     recs = oracle.refine(mesh, "cc", levels)
     dt = time.perf_counter() - t0
     F = recs[-1]["F"]
+    model, ncpu = host_cpu()
     return {"value": F / dt, "unit": "faces/s", "cores": 1, "kind": "oracle",
             "sample": f"{label}: CC levels 0->{levels} ({F} faces) in {dt:.2f} s, single-threaded C oracle (fp64)",
-            "seconds": dt}
+            "seconds": dt, "host_cpu": model, "host_cores": ncpu}
+
+
+def cpu_oracle_frames(mesh, levels, frames, nframes):
+    """Config 5 on the oracle: the listed frames (each a full CC evaluation of the deformed control
+    mesh), faces/s extrapolated from the per-frame time."""
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    F = 0
+    for t in frames:
+        mm = dict(mesh)
+        mm["pos"] = mg.frame_positions(mesh["pos"], t, nframes)
+        F = oracle.refine(mm, "cc", levels)[-1]["F"]
+    dt = (time.perf_counter() - t0) / len(frames)
+    model, ncpu = host_cpu()
+    return {"value": F / dt, "unit": "faces/s", "cores": 1, "kind": "oracle",
+            "sample": f"frames {list(frames)} of {nframes} (armor50k CC L{levels}, {F} faces each): "
+                      f"{dt:.2f} s per frame, single-threaded C oracle (fp64); extrapolated to "
+                      f"{nframes} frames = {dt * nframes:.0f} s", "extrapolated": True,
+            "host_cpu": model, "host_cores": ncpu}
 
 
 def run_reference(args):
@@ -249,7 +284,8 @@ def run_reference(args):
             "config": {"workload": "armor9k_cc_L6 (config 3), bounded sample", "scheme": "catmull-clark",
                        "levels_sampled": levels, "faces_out": F},
             "cpu_baseline": {"value": value, "unit": "faces/s", "cores": 1, "kind": "oracle",
-                             "sample": f"armor9k CC levels 0->{levels} ({F} faces) per step, single-threaded C oracle"},
+                             "sample": f"armor9k CC levels 0->{levels} ({F} faces) per step, single-threaded C oracle",
+                             "host_cpu": host_cpu()[0], "host_cores": host_cpu()[1]},
             "e2e": {"value": value, "unit": "faces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -561,7 +597,9 @@ def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, pea
                              "kernel": "whole static eval (position bytes only)", "peak_source": peak_src},
                 "summaries": {"frames_gathered": table_rows, "bytes_per_frame": 32, "collective": "all_gather (NCCL)"
                               if world > 1 else "none (1 rank)", "summary_ms_per_batch": summary_ms},
-                "cpu_baseline": None, "e2e": None, "gpu_launches": int((m.last_launch_count + 3) * nsteps),
+                "cpu_baseline": (cpu_oracle_frames(mesh, levels, (0,), nframes)
+                                 if (world == 1 and not args.no_cpu_baseline) else None),
+                "e2e": None, "gpu_launches": int((m.last_launch_count + 3) * nsteps),
                 "clocks": sampler.summary()}
         print(json.dumps(line), flush=True)
     m.close()
