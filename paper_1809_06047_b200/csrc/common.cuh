@@ -17,8 +17,21 @@
 
 #define ALSUB_HD __host__ __device__ __forceinline__
 #define ALSUB_D __device__ __forceinline__
-// first statement of every kernel: wait for the predecessor grid (programmatic dependent launch)
-#define ALSUB_GRID_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+// first statement of every kernel: wait for the predecessor grid (programmatic dependent launch).
+// Small grids (at most kEarlyTriggerBlocks CTAs, i.e. the latency-bound small levels) then let the
+// next kernel in the stream launch at once: its CTAs take free SM slots and wait in their own
+// griddepcontrol.wait, which hides the dependent-launch latency.  The trigger comes after the
+// wait, so at most one grid runs ahead.  Large grids do not trigger (waiting CTAs would take
+// slots from a bandwidth-bound kernel).
+#ifndef ALSUB_EARLY_TRIGGER_BLOCKS
+#define ALSUB_EARLY_TRIGGER_BLOCKS 296
+#endif
+#define ALSUB_GRID_WAIT()                                                                  \
+    do {                                                                                  \
+        asm volatile("griddepcontrol.wait;" ::: "memory");                                \
+        if (gridDim.x * gridDim.y * gridDim.z <= ALSUB_EARLY_TRIGGER_BLOCKS)              \
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");                \
+    } while (0)
 // let the next kernel in the stream begin launching (its blocks wait in ALSUB_GRID_WAIT)
 #define ALSUB_GRID_LAUNCH_NEXT() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
 
