@@ -207,6 +207,22 @@ alsub_status alsub_extract_maps(const alsub_mesh *mesh, int32_t *vtx_map, int32_
 alsub_status alsub_rcm_order(const int32_t *face_off, const int32_t *face_vtx, int32_t num_faces, int32_t num_verts,
                              int32_t *perm_vtx, int32_t *perm_face);
 
+/* Kernel probe (measurement): time ONE kernel inside every replayed refine.
+ * Arms a probe on the first launch named `kernel` ("cc_face", "cc_edge", "cc_vertex", "crease",
+ * "s3_face", ...; the names alsub_refine_profile reports) at refinement level `level` (0-based
+ * parent level, -1 = the level-0 build).  The next alsub_refine re-captures its CUDA graph with two
+ * external event-record nodes around that launch; replay i < steps records into event pair i, so
+ * the kernel is timed on its own stream inside the caller's timed region at no host sync.
+ * Re-arming with the same level/kernel only resets the pair counter (no re-capture); steps = 0
+ * disarms (and drops the graph).  Host-side; synchronises the device once.
+ * Errors: E_ARG (null mesh, steps < 0 or > 2^20, null name with steps > 0), E_CUDA. */
+alsub_status alsub_probe(alsub_mesh *mesh, int32_t level, const char *kernel, int32_t steps);
+
+/* Durations (ms, host array of `cap`) of the probed kernel in the replays since alsub_probe, in
+ * order; *count = number of replays recorded (<= steps).  Waits for the last one.
+ * Errors: E_ARG (null mesh/count, or the probe matched no launch of the captured refine), E_CUDA. */
+alsub_status alsub_probe_read(alsub_mesh *mesh, float *ms, int32_t cap, int32_t *count);
+
 /* Per-frame result summary of a batch of frames (what the sharded config-5 job
  * gathers over NCCL -- 32 B per frame instead of the frame).  frames: DEVICE fp32 [num_frames]
  * [num_verts][3] (e.g. the output of alsub_eval_frames); summary: DEVICE, num_frames records of

@@ -77,6 +77,8 @@ def lib():
     L.alsub_eval_frames_matrix.argtypes = [vp, vp, i32, vp, vp]
     L.alsub_extract_maps.argtypes = [vp, vp, vp, vp]
     L.alsub_frame_summary.argtypes = [vp, i32, i64, vp, vp]
+    L.alsub_probe.argtypes = [vp, i32, C.c_char_p, i32]
+    L.alsub_probe_read.argtypes = [vp, vp, i32, C.POINTER(i32)]
     L.alsub_last_launch_count.argtypes = [vp]
     L.alsub_last_launch_count.restype = i64
     L.alsub_mesh_destroy.argtypes = [vp]
@@ -87,7 +89,8 @@ def lib():
               "alsub_level_topology", "alsub_level_positions", "alsub_eval_frames", "alsub_eval_attributes",
               "alsub_level_positions_ptr", "alsub_reevaluate", "alsub_rcm_order", "alsub_mesh_extract",
               "alsub_extract_maps", "alsub_build_refinement_matrix", "alsub_refinement_matrix_info",
-              "alsub_refinement_matrix_csr", "alsub_eval_frames_matrix", "alsub_frame_summary"):
+              "alsub_refinement_matrix_csr", "alsub_eval_frames_matrix", "alsub_frame_summary", "alsub_probe",
+              "alsub_probe_read"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -345,6 +348,18 @@ class Mesh:
     def reevaluate(self, from_level, stream=None):
         """Recompute the positions of levels > from_level from the (edited) level from_level."""
         _check(self._lib.alsub_reevaluate(self._h, int(from_level), _stream(stream)))
+
+    def probe(self, level, kernel, steps):
+        """Arm the in-graph kernel probe (alsub_probe): replays 0 .. steps-1 of the next refines time
+        the first `kernel` launch at `level` with CUDA events on its own stream."""
+        _check(self._lib.alsub_probe(self._h, int(level), kernel.encode() if kernel else None, int(steps)))
+
+    def probe_read(self, cap=1 << 16):
+        """Per-replay durations (ms) of the probed kernel since probe() (alsub_probe_read)."""
+        buf = (C.c_float * cap)()
+        n = C.c_int32(0)
+        _check(self._lib.alsub_probe_read(self._h, buf, cap, C.byref(n)))
+        return [float(buf[i]) for i in range(min(n.value, cap))]
 
     @property
     def last_launch_count(self):

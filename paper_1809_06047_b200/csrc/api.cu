@@ -102,6 +102,15 @@ struct alsub_mesh {
     std::vector<LevelHost> lv;
     cudaGraphExec_t gexec = nullptr;
     int64_t graph_launches = 0;
+    // kernel probe (alsub_probe): per-replay event pairs retargeted into the graph's two
+    // event-record nodes, so one kernel is timed inside every replayed refine
+    std::string probe_name;
+    int probe_level = -2;
+    std::vector<cudaEvent_t> probe_start, probe_stop;
+    int32_t probe_next = 0;
+    cudaEvent_t probe_cap[2] = {nullptr, nullptr};  // the events used at capture time
+    cudaGraph_t gtemplate = nullptr;                // kept while a probe is armed (node handles)
+    cudaGraphNode_t probe_node[2] = {nullptr, nullptr};
     int64_t plan_runs = 0;  // refines run with the current plan (graph recorded from the 2nd on)
     cudaStream_t cap_stream = nullptr;
     cudaStream_t side_stream = nullptr;  // second branch for independent level kernels
@@ -358,8 +367,14 @@ extern "C" alsub_status alsub_set_positions(alsub_mesh *m, const float *pos, voi
 }
 
 // ---------------- plan ----------------
-static void free_plan(alsub_mesh *m, cudaStream_t s) {
+static void drop_graph(alsub_mesh *m) {
     if (m->gexec) { cudaGraphExecDestroy(m->gexec); m->gexec = nullptr; }
+    if (m->gtemplate) { cudaGraphDestroy(m->gtemplate); m->gtemplate = nullptr; }
+    m->probe_node[0] = m->probe_node[1] = nullptr;
+}
+
+static void free_plan(alsub_mesh *m, cudaStream_t s) {
+    drop_graph(m);
     free_list(m, m->mem_plan, s);
     free_list(m, m->mem_frames, s);
     m->scratch = m->scratch_create;
@@ -679,14 +694,48 @@ extern "C" alsub_status alsub_refine(alsub_mesh *m, alsub_scheme scheme, int32_t
             CU(cudaStreamSynchronize(m->cap_stream));
             cudaEventDestroy(ev);
             cudaGraph_t g;
+            const bool probe = !m->probe_start.empty();
+            if (probe) {
+                L.probe_name = m->probe_name.c_str();
+                L.probe_level = m->probe_level;
+                L.probe_ev[0] = m->probe_cap[0];
+                L.probe_ev[1] = m->probe_cap[1];
+            }
             CU(cudaStreamBeginCapture(m->cap_stream, cudaStreamCaptureModeThreadLocal));
             enqueue_refine(m, m->cap_stream, L);
             cudaError_t ce = cudaStreamEndCapture(m->cap_stream, &g);
             if (ce != cudaSuccess) return fail(ALSUB_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
             ce = cudaGraphInstantiate(&m->gexec, g, 0);
-            cudaGraphDestroy(g);
-            if (ce != cudaSuccess) { m->gexec = nullptr; return fail(ALSUB_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce)); }
+            if (ce != cudaSuccess) {
+                cudaGraphDestroy(g);
+                m->gexec = nullptr;
+                return fail(ALSUB_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+            }
+            if (probe && L.probe_hit) {
+                // the two event-record nodes of the probe, to retarget per replay
+                size_t nn = 0;
+                CU(cudaGraphGetNodes(g, nullptr, &nn));
+                std::vector<cudaGraphNode_t> nodes(nn);
+                CU(cudaGraphGetNodes(g, nodes.data(), &nn));
+                for (cudaGraphNode_t nd : nodes) {
+                    cudaGraphNodeType ty;
+                    CU(cudaGraphNodeGetType(nd, &ty));
+                    if (ty != cudaGraphNodeTypeEventRecord) continue;
+                    cudaEvent_t ev;
+                    CU(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+                    if (ev == m->probe_cap[0]) m->probe_node[0] = nd;
+                    if (ev == m->probe_cap[1]) m->probe_node[1] = nd;
+                }
+                m->gtemplate = g;
+            } else {
+                cudaGraphDestroy(g);
+            }
             m->graph_launches = L.n;
+        }
+        if (m->probe_node[0] && m->probe_node[1] && m->probe_next < (int32_t)m->probe_start.size()) {
+            const int32_t i = m->probe_next++;
+            CU(cudaGraphExecEventRecordNodeSetEvent(m->gexec, m->probe_node[0], m->probe_start[i]));
+            CU(cudaGraphExecEventRecordNodeSetEvent(m->gexec, m->probe_node[1], m->probe_stop[i]));
         }
         CU(cudaGraphLaunch(m->gexec, s));
         m->last_launches = m->graph_launches;
@@ -1266,14 +1315,61 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
     return ALSUB_OK;
 }
 
+static void free_probe_events(alsub_mesh *m) {
+    for (cudaEvent_t e : m->probe_start) cudaEventDestroy(e);
+    for (cudaEvent_t e : m->probe_stop) cudaEventDestroy(e);
+    m->probe_start.clear();
+    m->probe_stop.clear();
+    for (cudaEvent_t &e : m->probe_cap)
+        if (e) { cudaEventDestroy(e); e = nullptr; }
+}
+
+extern "C" alsub_status alsub_probe(alsub_mesh *m, int32_t level, const char *kernel, int32_t steps) {
+    if (!m) return fail(ALSUB_E_ARG, "null mesh");
+    if (steps < 0 || steps > 1 << 20) return fail(ALSUB_E_ARG, "steps must be in [0, 2^20]");
+    if (steps > 0 && !kernel) return fail(ALSUB_E_ARG, "null kernel name");
+    CU(cudaDeviceSynchronize());  // events of an earlier probe may still be pending
+    const bool same = steps > 0 && !m->probe_start.empty() && m->probe_level == level && m->probe_name == kernel;
+    if (!same) {
+        drop_graph(m);  // the next alsub_refine re-captures (with or without the probe nodes)
+        free_probe_events(m);
+        if (steps == 0) return ALSUB_OK;
+        m->probe_name = kernel;
+        m->probe_level = level;
+        for (cudaEvent_t &e : m->probe_cap) CU(cudaEventCreate(&e));
+    }
+    const size_t have = m->probe_start.size();
+    for (size_t i = have; i < (size_t)steps; ++i) {
+        cudaEvent_t a, b;
+        CU(cudaEventCreate(&a));
+        CU(cudaEventCreate(&b));
+        m->probe_start.push_back(a);
+        m->probe_stop.push_back(b);
+    }
+    m->probe_next = 0;
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_probe_read(alsub_mesh *m, float *ms, int32_t cap, int32_t *count) {
+    if (!m || !count) return fail(ALSUB_E_ARG, "null argument");
+    const int32_t n = m->probe_next;
+    *count = n;
+    if (!m->probe_start.empty() && m->gexec && !m->probe_node[0])
+        return fail(ALSUB_E_ARG, "the probe matched no kernel of the captured refine");
+    if (n == 0) return ALSUB_OK;
+    CU(cudaEventSynchronize(m->probe_stop[n - 1]));
+    for (int32_t i = 0; i < n && i < cap; ++i) CU(cudaEventElapsedTime(ms + i, m->probe_start[i], m->probe_stop[i]));
+    return ALSUB_OK;
+}
+
 extern "C" int64_t alsub_last_launch_count(const alsub_mesh *m) { return m ? m->last_launches : 0; }
 
 extern "C" void alsub_mesh_destroy(alsub_mesh *m) {
     if (!m) return;
     cudaStream_t s = m->cap_stream ? m->cap_stream : (cudaStream_t)0;
     cudaDeviceSynchronize();
-    if (m->gexec) cudaGraphExecDestroy(m->gexec);
-    m->gexec = nullptr;
+    drop_graph(m);
+    free_probe_events(m);
     free_list(m, m->mem_frames, s);
     free_list(m, m->mem_rm, s);
     free_list(m, m->mem_plan, s);
@@ -1290,6 +1386,9 @@ extern "C" const char *alsub_last_error(void) { return g_err.c_str(); }
 extern "C" const char *alsub_version(void) { return "alsub-b200 0.1 (sm_100a)"; }
 
 namespace alsub {
+bool Launches::probing(const char *kname) const {
+    return probe_name && !probe_hit && level == probe_level && strcmp(kname, probe_name) == 0;
+}
 bool pdl_enabled() {
     static int v = -1;
     if (v < 0) {

@@ -29,6 +29,13 @@ struct Launches {
     std::vector<cudaEvent_t> ev;
     std::vector<const char *> name;
     std::vector<int> lvl;
+    // optional probe (alsub_probe): external event records around the first launch named
+    // probe_name at level probe_level; captured into the CUDA graph as event-record nodes
+    const char *probe_name = nullptr;
+    int probe_level = -2;
+    cudaEvent_t probe_ev[2] = {nullptr, nullptr};
+    bool probe_hit = false;
+    bool probing(const char *kname) const;
     void done(const char *kname, cudaStream_t s) {
         ++n;
         if (timing) {
@@ -61,7 +68,13 @@ inline void launch(Launches &L, const char *name, void (*k)(KArgs...), dim3 grid
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    const bool probe = L.probing(name);
+    if (probe) cudaEventRecordWithFlags(L.probe_ev[0], s, cudaEventRecordExternal);
     cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+    if (probe) {
+        cudaEventRecordWithFlags(L.probe_ev[1], s, cudaEventRecordExternal);
+        L.probe_hit = true;
+    }
     L.done(name, s);
 }
 inline unsigned grid_for(int64_t n, int threads = kThreads) {

@@ -607,3 +607,30 @@ def test_frame_summary_of_eval_frames_output():
         bb, cs = split_summary(frame_summary(out))
         lo, hi, want = _summary_np(out.cpu().numpy())
         assert np.array_equal(cs, want) and np.array_equal(bb[:, :3], lo) and np.array_equal(bb[:, 3:], hi)
+
+
+def test_probe_times_kernel_inside_graph():
+    """alsub_probe: event-record nodes around one kernel of the captured refine; one duration per
+    replay, results unchanged (bitwise) by the probe; unknown kernel names are reported."""
+    from paper_1809_06047_b200 import AlsubError, Mesh
+    mesh = mg.armor(6, 5, 6, 1, 1, 2, name="armor_small")
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine("cc", 3)
+        m.refine("cc", 3)
+        ref = m.positions(3).clone()
+        m.probe(2, "cc_face", 4)
+        for _ in range(6):  # replays beyond `steps` reuse the last pair
+            m.refine("cc", 3)
+        t = m.probe_read()
+        assert len(t) == 4 and all(x > 0 for x in t)
+        assert torch.equal(m.positions(3), ref)
+        m.probe(2, "cc_face", 4)  # re-arm: counter reset, no re-capture
+        m.refine("cc", 3)
+        assert len(m.probe_read()) == 1
+        m.probe(2, "no_such_kernel", 2)
+        m.refine("cc", 3)
+        with pytest.raises(AlsubError):
+            m.probe_read()
+        m.probe(0, None, 0)  # disarm
+        m.refine("cc", 3)
+        assert m.probe_read() == [] and torch.equal(m.positions(3), ref)
