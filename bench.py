@@ -406,6 +406,8 @@ def run_alsub(args):
     roofline = {"bound": "hbm", "kernel": f"{dname} (level {dlvl}->{dlvl + 1})", "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "alg_bytes_per_launch": dbytes, "avg_launch_ms": dms, "share_of_step": dms / ms_per_step,
+                "share_of_kernel_time": dms_profile / prof_step,  # comparable with the ncu launch list
+                                                                  # (serialised kernels, no branch overlap)
                 "launches_timed": len(probe_ms),
                 "timing": "CUDA events recorded by event-record nodes around the kernel inside every "
                           "replayed refine graph of the timed region (alsub_probe), on its own stream",
