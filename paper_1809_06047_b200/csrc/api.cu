@@ -109,6 +109,8 @@ struct alsub_mesh {
     std::vector<cudaEvent_t> probe_start, probe_stop;
     int32_t probe_next = 0;
     cudaEvent_t probe_cap[2] = {nullptr, nullptr};  // the events used at capture time
+    cudaStream_t probe_stream = nullptr;
+    cudaEvent_t probe_dep[3] = {nullptr, nullptr, nullptr};
     cudaGraph_t gtemplate = nullptr;                // kept while a probe is armed (node handles)
     cudaGraphNode_t probe_node[2] = {nullptr, nullptr};
     int64_t plan_runs = 0;  // refines run with the current plan (graph recorded from the 2nd on)
@@ -700,9 +702,15 @@ extern "C" alsub_status alsub_refine(alsub_mesh *m, alsub_scheme scheme, int32_t
                 L.probe_level = m->probe_level;
                 L.probe_ev[0] = m->probe_cap[0];
                 L.probe_ev[1] = m->probe_cap[1];
+                L.probe_stream = m->probe_stream;
+                for (int k = 0; k < 3; ++k) L.probe_dep[k] = m->probe_dep[k];
             }
             CU(cudaStreamBeginCapture(m->cap_stream, cudaStreamCaptureModeThreadLocal));
             enqueue_refine(m, m->cap_stream, L);
+            if (L.probe_hit) {  // join the probe branch
+                cudaEventRecord(L.probe_dep[2], L.probe_stream);
+                cudaStreamWaitEvent(m->cap_stream, L.probe_dep[2], 0);
+            }
             cudaError_t ce = cudaStreamEndCapture(m->cap_stream, &g);
             if (ce != cudaSuccess) return fail(ALSUB_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
             ce = cudaGraphInstantiate(&m->gexec, g, 0);
@@ -1322,6 +1330,9 @@ static void free_probe_events(alsub_mesh *m) {
     m->probe_stop.clear();
     for (cudaEvent_t &e : m->probe_cap)
         if (e) { cudaEventDestroy(e); e = nullptr; }
+    for (cudaEvent_t &e : m->probe_dep)
+        if (e) { cudaEventDestroy(e); e = nullptr; }
+    if (m->probe_stream) { cudaStreamDestroy(m->probe_stream); m->probe_stream = nullptr; }
 }
 
 extern "C" alsub_status alsub_probe(alsub_mesh *m, int32_t level, const char *kernel, int32_t steps) {
@@ -1337,6 +1348,8 @@ extern "C" alsub_status alsub_probe(alsub_mesh *m, int32_t level, const char *ke
         m->probe_name = kernel;
         m->probe_level = level;
         for (cudaEvent_t &e : m->probe_cap) CU(cudaEventCreate(&e));
+        for (cudaEvent_t &e : m->probe_dep) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CU(cudaStreamCreateWithFlags(&m->probe_stream, cudaStreamNonBlocking));
     }
     const size_t have = m->probe_start.size();
     for (size_t i = have; i < (size_t)steps; ++i) {

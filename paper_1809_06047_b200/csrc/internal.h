@@ -34,6 +34,11 @@ struct Launches {
     const char *probe_name = nullptr;
     int probe_level = -2;
     cudaEvent_t probe_ev[2] = {nullptr, nullptr};
+    // the probe's event records hang off the main chain on their own stream (forked before and
+    // after the kernel, joined at the end of the refine), so the kernel keeps its programmatic
+    // launch edges to its neighbours
+    cudaStream_t probe_stream = nullptr;
+    cudaEvent_t probe_dep[3] = {nullptr, nullptr, nullptr};
     bool probe_hit = false;
     bool probing(const char *kname) const;
     void done(const char *kname, cudaStream_t s) {
@@ -69,10 +74,16 @@ inline void launch(Launches &L, const char *name, void (*k)(KArgs...), dim3 grid
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     const bool probe = L.probing(name);
-    if (probe) cudaEventRecordWithFlags(L.probe_ev[0], s, cudaEventRecordExternal);
+    if (probe) {
+        cudaEventRecord(L.probe_dep[0], s);
+        cudaStreamWaitEvent(L.probe_stream, L.probe_dep[0], 0);
+        cudaEventRecordWithFlags(L.probe_ev[0], L.probe_stream, cudaEventRecordExternal);
+    }
     cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
     if (probe) {
-        cudaEventRecordWithFlags(L.probe_ev[1], s, cudaEventRecordExternal);
+        cudaEventRecord(L.probe_dep[1], s);
+        cudaStreamWaitEvent(L.probe_stream, L.probe_dep[1], 0);
+        cudaEventRecordWithFlags(L.probe_ev[1], L.probe_stream, cudaEventRecordExternal);
         L.probe_hit = true;
     }
     L.done(name, s);
