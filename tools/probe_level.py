@@ -1,0 +1,31 @@
+"""Live (in-graph) duration of every kernel of one config-3 level via alsub_probe:
+python tools/probe_level.py [level]  (default 5, the last CC level of armor9k L6)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import meshgen as mg  # noqa: E402
+from paper_1809_06047_b200 import Mesh  # noqa: E402
+
+lvl = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+mesh = mg.armor9k()
+flush = torch.empty(64 * 1024 * 1024, device="cuda")
+m = Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"])
+for _ in range(3):
+    m.refine("cc", 6)
+for name in ("cc_face", "cc_edge", "cc_vertex", "crease"):
+    m.probe(lvl, name, 20)
+    m.refine("cc", 6)
+    m.probe(lvl, name, 20)
+    for i in range(20):
+        flush.fill_(float(i))
+        m.refine("cc", 6)
+    try:
+        t = sorted(m.probe_read())
+        print(f"level {lvl} {name:10s} median {t[len(t) // 2] * 1e3:7.1f} us  min {t[0] * 1e3:7.1f} us")
+    except Exception as e:  # no such kernel at this level
+        print(f"level {lvl} {name:10s} -- {e}")
+m.probe(0, None, 0)
+m.close()
