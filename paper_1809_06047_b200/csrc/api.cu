@@ -116,7 +116,7 @@ struct alsub_mesh {
     int64_t plan_runs = 0;  // refines run with the current plan (graph recorded from the 2nd on)
     cudaStream_t cap_stream = nullptr;
     cudaStream_t side_stream = nullptr;  // second branch for independent level kernels
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_build = nullptr;
     int64_t last_launches = 0;
     // the last refined level's special lists (crease pairs / sigma of level L and the level-L rows
     // of the special-vertex table) are only read by exports and extraction: the refine skips their
@@ -355,6 +355,7 @@ static alsub_status create_impl(const int32_t *face_off, const int32_t *face_vtx
     CU(cudaStreamCreateWithFlags(&m->side_stream, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&m->ev_build, cudaEventDisableTiming));
     m->last_launches = L.n;
     *out = m;
     g_err.clear();
@@ -604,6 +605,8 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     L.side = m->side_stream;
     L.ev_fork = m->ev_fork;
     L.ev_join = m->ev_join;
+    // CC with levels: the build's special-list branch stays open into level 0 (cc.cu joins it)
+    L.ev_build = (scheme == ALSUB_CATMULL_CLARK && levels > 0) ? m->ev_build : nullptr;
     // a1-a3: level-0 mesh matrix, M^T by counting sort, edge index, creases
     L.level = -1;
     nvtxRangePushA("alsub level-0 build");
@@ -1392,6 +1395,7 @@ extern "C" void alsub_mesh_destroy(alsub_mesh *m) {
     if (m->side_stream) cudaStreamDestroy(m->side_stream);
     if (m->ev_fork) cudaEventDestroy(m->ev_fork);
     if (m->ev_join) cudaEventDestroy(m->ev_join);
+    if (m->ev_build) cudaEventDestroy(m->ev_build);
     delete m;
 }
 

@@ -458,29 +458,34 @@ static void fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     launch(L, "b0_flags", k_b0_flags<ORDER>, dim3(grid_for(nf)), dim3(kThreads), 0, s, b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
                                                  b.face_edge, b.edge_hh, tp, b.V, E, b.bnd_word, nw, b.edge_sigma,
                                                  b.edge_cidx, b.sp_flag, b.bnd_wcnt, b.flags, b.crease_lenient);
-    // the boundary-word prefix is only read by the level kernels: a parallel branch next to the
-    // special-list chain (fork / join events become graph branches under capture)
-    const bool fork = L.can_fork() && b.zeroed;
+    // the special-list chain (special edges, special-vertex CSR) is only read by the crease rules of
+    // the level kernels: with a side stream it runs as a parallel branch beside the boundary-word
+    // prefix scan and the level-0 face kernel, and stays open (L.build_open) until the level-0
+    // vertex kernel, the first reader on the main stream, waits for L.ev_build (the edge kernel
+    // follows it on the side stream itself)
+    const bool fork = L.can_fork() && b.zeroed && L.ev_build;
+    cudaStream_t sc = s;
     if (fork) {
         cudaEventRecord(L.ev_fork, s);
         cudaStreamWaitEvent(L.side, L.ev_fork, 0);
+        sc = L.side;
     }
-    scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, region(b, 3), fork ? L.side : s, L, b.zeroed);
-    scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, region(b, 4), s, L, b.zeroed);
+    scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, region(b, 3), s, L, b.zeroed);
+    scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, region(b, 4), sc, L, b.zeroed);
     if (E > 0) {
-        launch(L, "b0_special", k_b0_special<ORDER>, dim3(grid_for(E)), dim3(kThreads), 0, s, b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp, E,
+        launch(L, "b0_special", k_b0_special<ORDER>, dim3(grid_for(E)), dim3(kThreads), 0, sc, b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp, E,
                                                       b.sp, b.sv_cnt, b.spw, b.spwpre);
     }
-    scan_exclusive(b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V, region(b, 5), s, L, b.zeroed);
+    scan_exclusive(b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V, region(b, 5), sc, L, b.zeroed);
     if (E > 0) {
-        launch(L, "b0_sv_list", k_b0_svlist, dim3(grid_for(E)), dim3(kThreads), 0, s, b.sp, b.scalars + 2, E, b.sv_off, b.sv_cur, b.sv_list);
+        launch(L, "b0_sv_list", k_b0_svlist, dim3(grid_for(E)), dim3(kThreads), 0, sc, b.sp, b.scalars + 2, E, b.sv_off, b.sv_cur, b.sv_list);
     }
     if (b.V > 0) {
-        launch(L, "b0_sv_sort", k_b0_svsort, dim3(grid_for(b.V)), dim3(kThreads), 0, s, b.V, b.sv_off, b.sv_list, b.sv_vtx, b.scalars);
+        launch(L, "b0_sv_sort", k_b0_svsort, dim3(grid_for(b.V)), dim3(kThreads), 0, sc, b.V, b.sv_off, b.sv_list, b.sv_vtx, b.scalars);
     }
     if (fork) {
-        cudaEventRecord(L.ev_join, L.side);
-        cudaStreamWaitEvent(s, L.ev_join, 0);
+        cudaEventRecord(L.ev_build, L.side);
+        L.build_open = true;
     }
 }
 

@@ -797,6 +797,10 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, b
             else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT, false>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
         }
     }
+    if (L.build_open) {  // the level-0 build's special-list branch: read by the vertex kernel
+        cudaStreamWaitEvent(s, L.ev_build, 0);
+        L.build_open = false;
+    }
     if (p.V > 0) {
         // 32-vertex warp tasks; >= 2 waves of 148 SMs for small levels, 4 tasks per warp for large
         // ones (128-vertex tasks with batched loads were measured slower)

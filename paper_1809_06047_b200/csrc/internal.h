@@ -18,6 +18,11 @@ struct Launches {
     // inside stream capture this becomes parallel graph branches)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // level-0 build: the special-list chain runs on the side stream beside the level-0 face kernel;
+    // build_open = that branch is not joined yet (ev_build marks its end); the level-0 vertex
+    // kernel (which reads the lists) waits for it
+    cudaEvent_t ev_build = nullptr;
+    bool build_open = false;
     bool can_fork() const { return side != nullptr && !timing && !no_fork(); }
     static bool no_fork() {  // ALSUB_NO_FORK=1: one branch (experiments)
         static const bool v = [] { const char *e = getenv("ALSUB_NO_FORK"); return e && e[0] == '1'; }();
