@@ -583,9 +583,12 @@ def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, pea
         for i in range(nsteps):
             batch(i, timed_last=i == nsteps - 1)
         stream.wait_stream(side)
+        eg = torch.cuda.Event(enable_timing=True)
+        eg.record(stream)
         table = gather_summaries(summ[:nsteps * nb], nsteps * nb * world, world, rank, device=dev)
         e1.record(stream)
         torch.cuda.synchronize()
+    gather_ms = eg.elapsed_time(e1)  # the NCCL all-gather of the records (reported apart)
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
     summary_ms = ev_s[0][0].elapsed_time(ev_s[0][1]) if nsteps else 0.0
@@ -611,7 +614,9 @@ def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, pea
                              "frac": gbps / peak if gbps else None, "traffic": None,
                              "kernel": "whole static eval (position bytes only)", "peak_source": peak_src},
                 "summaries": {"frames_gathered": table_rows, "bytes_per_frame": 32, "collective": "all_gather (NCCL)"
-                              if world > 1 else "none (1 rank)", "summary_ms_per_batch": summary_ms},
+                              if world > 1 else "none (1 rank)", "summary_ms_per_batch": summary_ms,
+                              "gather_ms": gather_ms},
+                "per_gpu_hbm_frac": (gbps / peak) if gbps else None,  # gbps is per rank (its frames / time)
                 "cpu_baseline": (cpu_oracle_frames(mesh, levels, (0,), nframes)
                                  if (world == 1 and not args.no_cpu_baseline) else None),
                 "e2e": None, "gpu_launches": int((m.last_launch_count + 3) * nsteps),
