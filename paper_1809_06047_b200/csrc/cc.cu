@@ -788,10 +788,14 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, b
         constexpr int IT = 2;
         const unsigned gdim = grid_for(p.E, kThreads * IT);
         // p.crease: boundary/crease rules fused into the kernels (small levels, where a separate
-        // pass costs a full dependent-kernel latency); otherwise crease.cu runs after this level
-        if (p.crease) {
-            if (one) launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 1, IT, true>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
-            else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT, true>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
+        // pass costs a full dependent-kernel latency); otherwise crease.cu runs after this level.
+        // Those small levels take one edge per thread (twice the CTAs: more latency hiding, less
+        // wave quantisation; config 3 0.689 -> 0.684 ms -- two edges per thread stay better on the
+        // large levels, 0.690 -> 0.698 ms with one)
+        if (p.crease) {  // (static frames too: the same instantiation keeps them bitwise equal)
+            const unsigned g1 = grid_for(p.E, kThreads);
+            if (one) launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 1, 1, true>, dim3(g1), dim3(kThreads), 0, se, p, c, fr, topo);
+            else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, 1, true>, dim3(g1), dim3(kThreads), 0, se, p, c, fr, topo);
         } else {
             if (one) launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 1, IT, false>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
             else launch(L, "cc_edge", k_cc_edge<ORDER, ADJ, BND, 0, IT, false>, dim3(gdim), dim3(kThreads), 0, se, p, c, fr, topo);
