@@ -1,5 +1,5 @@
 """Live (in-graph) duration of every kernel of one config-3 level via alsub_probe:
-python tools/probe_level.py [level]  (default 5, the last CC level of armor9k L6)."""
+python tools/probe_level.py [level]  (default 5, the last CC level of armor9k L6; -1 = the build)."""
 import os
 import sys
 
@@ -15,7 +15,10 @@ flush = torch.empty(64 * 1024 * 1024, device="cuda")
 m = Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"])
 for _ in range(3):
     m.refine("cc", 6)
-for name in ("cc_face", "cc_edge", "cc_vertex", "crease"):
+names = ("cc_face", "cc_edge", "cc_vertex", "crease") if lvl >= 0 else (
+    "zero", "b0_prep", "scan", "b0_scatter", "b0_edge_count", "b0_edge_fill", "b0_flags", "b0_special",
+    "b0_sv_list", "b0_sv_sort")  # level -1 = the level-0 build (first launch of each name)
+for name in names:
     m.probe(lvl, name, 20)
     m.refine("cc", 6)
     m.probe(lvl, name, 20)
