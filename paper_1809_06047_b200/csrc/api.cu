@@ -1279,7 +1279,7 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
         return ALSUB_OK;
     }
     const bool in_dev = is_device_ptr(frames_in), out_dev = is_device_ptr(frames_out);
-    const int nb_max = getenv("ALSUB_FRAME_BATCH") ? atoi(getenv("ALSUB_FRAME_BATCH")) : 8;
+    const int nb_max = getenv("ALSUB_FRAME_BATCH") ? std::max(1, std::min(64, atoi(getenv("ALSUB_FRAME_BATCH")))) : 8;
     const int nb = std::min(num_frames, nb_max);
     // per-level batch buffers of 3 V_l nb floats for l = 0 (if host input) .. levels (if host output)
     if (m->frames_nb < nb || (int)m->frame_buf.size() != m->levels + 1) {
