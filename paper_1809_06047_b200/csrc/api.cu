@@ -116,7 +116,7 @@ struct alsub_mesh {
     int64_t plan_runs = 0;  // refines run with the current plan (graph recorded from the 2nd on)
     cudaStream_t cap_stream = nullptr;
     cudaStream_t side_stream = nullptr;  // second branch for independent level kernels
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_build = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_build = nullptr, ev_aux = nullptr;
     int64_t last_launches = 0;
     // the last refined level's special lists (crease pairs / sigma of level L and the level-L rows
     // of the special-vertex table) are only read by exports and extraction: the refine skips their
@@ -356,6 +356,7 @@ static alsub_status create_impl(const int32_t *face_off, const int32_t *face_vtx
     CU(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&m->ev_build, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&m->ev_aux, cudaEventDisableTiming));
     m->last_launches = L.n;
     *out = m;
     g_err.clear();
@@ -605,6 +606,7 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
     L.side = m->side_stream;
     L.ev_fork = m->ev_fork;
     L.ev_join = m->ev_join;
+    L.ev_aux = m->ev_aux;
     // CC with levels: the build's special-list branch stays open into level 0 (cc.cu joins it)
     L.ev_build = (scheme == ALSUB_CATMULL_CLARK && levels > 0) ? m->ev_build : nullptr;
     // a1-a3: level-0 mesh matrix, M^T by counting sort, edge index, creases
@@ -658,11 +660,9 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
             }
         } else if (scheme == ALSUB_LOOP) {
             VSegs g = make_segs_loop(m, l);
-            loop_level(p, c, fr, true, adj, P.loop_stat, (adj || special) ? P.loop_base : nullptr, g, s, L);
-            if (special) {
-                if (!adj) m->lazy_lists = true;
-                crease_level(p, c, fr, (int32_t)P.V, 1, adj, s, L);
-            }
+            if (special && !adj) m->lazy_lists = true;
+            loop_level(p, c, fr, true, adj, P.loop_stat, (adj || special) ? P.loop_base : nullptr, g, s, L,
+                       special ? (adj ? 1 : 0) : -1);
         } else {
             VSegs g = make_segs_s3(m, l);
             sqrt3_level(p, c, fr, true, adj, g, s, L);
@@ -1040,8 +1040,7 @@ static void static_level(alsub_mesh *m, int l, const Frames &fr, cudaStream_t s,
         if (special && !p.crease) crease_level(p, c, fr, (int32_t)(Pl.V + Pl.F), 0, false, s, L);
     } else if (scheme == ALSUB_LOOP) {
         VSegs g = make_segs_loop(m, l);
-        loop_level(p, c, fr, false, false, nullptr, nullptr, g, s, L);
-        if (special) crease_level(p, c, fr, (int32_t)Pl.V, 1, false, s, L);
+        loop_level(p, c, fr, false, false, nullptr, nullptr, g, s, L, special ? 0 : -1);
     } else {
         VSegs g = make_segs_s3(m, l);
         sqrt3_level(p, c, fr, false, false, g, s, L);
@@ -1066,6 +1065,7 @@ extern "C" alsub_status alsub_reevaluate(alsub_mesh *m, int32_t from_level, void
     L.side = m->side_stream;
     L.ev_fork = m->ev_fork;
     L.ev_join = m->ev_join;
+    L.ev_aux = m->ev_aux;
     for (int l = from_level; l < m->levels; ++l) {
         const float *P = l == 0 ? m->pos0 : m->lv[l].pos;
         Frames fr{P, m->lv[l + 1].pos, 3 * m->lv[l].V, 3 * m->lv[l + 1].V, 1, m->hs, 0,
@@ -1298,6 +1298,7 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
     L.side = m->side_stream;
     L.ev_fork = m->ev_fork;
     L.ev_join = m->ev_join;
+    L.ev_aux = m->ev_aux;
     for (int32_t f0 = 0; f0 < num_frames; f0 += nb) {
         const int n = std::min(nb, num_frames - f0);
         const float *Pin = frames_in + 3 * V0 * (int64_t)f0;
@@ -1396,6 +1397,7 @@ extern "C" void alsub_mesh_destroy(alsub_mesh *m) {
     if (m->ev_fork) cudaEventDestroy(m->ev_fork);
     if (m->ev_join) cudaEventDestroy(m->ev_join);
     if (m->ev_build) cudaEventDestroy(m->ev_build);
+    if (m->ev_aux) cudaEventDestroy(m->ev_aux);
     delete m;
 }
 

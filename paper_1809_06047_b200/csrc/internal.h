@@ -22,6 +22,7 @@ struct Launches {
     // build_open = that branch is not joined yet (ev_build marks its end); the level-0 vertex
     // kernel (which reads the lists) waits for it
     cudaEvent_t ev_build = nullptr;
+    cudaEvent_t ev_aux = nullptr;  // Loop: end of the vertex kernel, for the crease pass on the side branch
     bool build_open = false;
     bool can_fork() const { return side != nullptr && !timing && !no_fork(); }
     static bool no_fork() {  // ALSUB_NO_FORK=1: one branch (experiments)
@@ -289,8 +290,11 @@ struct VSegs {
 // recomputes its edge ids from gp's rows and the edge kernel iterates gp's edges
 void cc_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &segs,
               const LevelDev *gp, cudaStream_t s, Launches &L);
+// crease >= 0: also run the crease module (crease_level with ep_base = V, scheme 1, inherit =
+// crease == 1) inside the level, on the side branch after the edge kernel once the vertex kernel
+// is done, i.e. beside the face kernel
 void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, int32_t *stat,
-                int32_t *base, const VSegs &g, cudaStream_t s, Launches &L);
+                int32_t *base, const VSegs &g, cudaStream_t s, Launches &L, int crease = -1);
 void sqrt3_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, const VSegs &g,
                  cudaStream_t s, Launches &L);
 // crease / boundary module (crease.cu): ONE kernel per level -- edge and vertex overrides and

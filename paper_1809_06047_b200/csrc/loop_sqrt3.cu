@@ -326,9 +326,11 @@ __global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c
 // kernel once the scan is done (torus100k Loop L4 0.551 -> 0.547 ms, ico L6 0.070 -> 0.068 ms
 // against the vertex kernel on the side branch).
 void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool topo, bool adj, int32_t *stat,
-                int32_t *base, const VSegs &g, cudaStream_t s, Launches &L) {
+                int32_t *base, const VSegs &g, cudaStream_t s, Launches &L, int crease) {
     const bool A = adj && topo;
     const bool fork = L.can_fork();
+    // (config 2b, creased tet Loop L6: 0.096 -> 0.093 ms against the crease pass after the join)
+    const bool side_crease = crease >= 0 && fork && L.ev_aux;
     cudaStream_t se = s;
     if (fork) {
         cudaEventRecord(L.ev_fork, s);
@@ -339,6 +341,7 @@ void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool top
         if (A) launch(L, "loop_vertex", k_loop_vertex<true>, dim3(grid_for(p.V)), dim3(kThreads), 0, s, p, c, fr, g);
         else launch(L, "loop_vertex", k_loop_vertex<false>, dim3(grid_for(p.V)), dim3(kThreads), 0, s, p, c, fr, g);
     }
+    if (side_crease) cudaEventRecord(L.ev_aux, s);
     if (base) {
         loop_edge_base(p, stat, base, se, L);
         if (fork) {  // the face kernel (main) waits for the bases
@@ -350,6 +353,10 @@ void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool top
         if (A) launch(L, "loop_edge", k_loop_edge<true>, dim3(grid_for(p.E, 2 * kThreads)), dim3(kThreads), 0, se, p, c, fr);
         else launch(L, "loop_edge", k_loop_edge<false>, dim3(grid_for(p.E, 2 * kThreads)), dim3(kThreads), 0, se, p, c, fr);
     }
+    if (side_crease) {  // overrides need the edge points (this branch) and the vertex points (ev_aux)
+        cudaStreamWaitEvent(se, L.ev_aux, 0);
+        crease_level(p, c, fr, p.V, 1, crease == 1, se, L);
+    }
     if (topo && p.F > 0) {
         if (A) launch(L, "loop_face", k_loop_face<true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c);
         else launch(L, "loop_face", k_loop_face<false>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c);
@@ -358,6 +365,7 @@ void loop_level(const LevelDev &p, const ChildDev &c, const Frames &fr, bool top
         cudaEventRecord(L.ev_join, L.side);
         cudaStreamWaitEvent(s, L.ev_join, 0);
     }
+    if (crease >= 0 && !side_crease) crease_level(p, c, fr, p.V, 1, crease == 1, s, L);
 }
 
 // ------------------------------------------------------------------------------------------
