@@ -10,9 +10,11 @@
  * No blocking, fusion, structured shortcuts or reordering beyond the definitions.
  *
  * Parity pins: tests/test_oracle_pins.py (counts, Euler characteristic, hand values, B-spline
- * masks, affine invariance, crease limits, brute force vs exact rationals).  The semi-sharp
- * blend (0 < sigma < 1) and the >= 3-crease average (readings R7, R8) are "parity unpinned"
- * beyond their special cases: the paper gives no numbers for them.
+ * masks, affine invariance, crease limits, brute force vs exact rationals).  The paper gives no
+ * numbers for the semi-sharp blend (0 < sigma < 1) or the >= 3-crease average (P:L411-413, L428,
+ * L440); both are pinned by hand-derived values of readings R7/R8/R21 (tests/golden/
+ * hand_values.json: cc_semisharp_vertex_L1, cc_three_creases_L1, cc_sigma_bar_exclusions_L1)
+ * and by s -> 0+ / 1- continuity against the smooth and sharp hand values.
  */
 #include "alsub_oracle.h"
 
@@ -107,6 +109,12 @@ static int find_edge(const topo *T, int32_t a, int32_t b) {
     return -1;
 }
 
+/* slot of the reverse directed edge of slot s (F(j,i) of F(i,j)), or -1 */
+static int32_t twin_slot(const topo *T, int32_t s) {
+    int32_t e = T->slot_edge[s];
+    return T->edge_fwd[e] == s ? T->edge_bwd[e] : T->edge_fwd[e];
+}
+
 static int build_topo(const om_mesh *in, topo *T, char *err, int errlen) {
     memset(T, 0, sizeof(*T));
     if (in->V < 0 || in->F < 0 || in->K < 0) { set_err(err, errlen, "negative count"); return OM_E_ARG; }
@@ -195,6 +203,34 @@ static int build_topo(const om_mesh *in, topo *T, char *err, int errlen) {
     memset(fill, 0, ((size_t)V + 1) * 4);
     for (int32_t s = 0; s < S; ++s) T->vs_slot[T->vs_off[in->face_vtx[s]] + fill[in->face_vtx[s]]++] = s;
     free(fill);
+    /* 3b. fans around each vertex (reading R18).  Rotating slot h of v to twin(prev(h)) -- the
+     * slot of v in the face across the edge entering v -- walks one fan.  A fan is open when it
+     * starts at a slot whose outgoing edge is a boundary edge (twin(h) = -1).  Open fans are
+     * allowed (a bowtie vertex; it ends up as a corner).  A closed fan together with any other
+     * fan at the same vertex is non-manifold.                                                 */
+    for (int32_t v = 0; v < V; ++v) {
+        int32_t deg = T->vs_off[v + 1] - T->vs_off[v];
+        if (deg == 0) continue;
+        int32_t starts = 0, covered = 0;
+        for (int32_t i = T->vs_off[v]; i < T->vs_off[v + 1]; ++i) {
+            int32_t h = T->vs_slot[i];
+            if (twin_slot(T, h) >= 0) continue;
+            ++starts;
+            int32_t n = 1;
+            for (int32_t g = h; twin_slot(T, T->slot_prev[g]) >= 0 && n <= deg; ++n)
+                g = twin_slot(T, T->slot_prev[g]);
+            covered += n;
+        }
+        if (starts == 0) {   /* only closed fans: the one through the first slot must hold them all */
+            int32_t h0 = T->vs_slot[T->vs_off[v]], g = h0, n = 0;
+            do { g = twin_slot(T, T->slot_prev[g]); ++n; } while (g != h0 && n <= deg);
+            covered = n;
+        }
+        if (covered != deg) {
+            set_err(err, errlen, "vertex %d: its %d faces form a closed fan plus another fan", v, deg);
+            return OM_E_NONMANIFOLD;
+        }
+    }
     /* 4. crease matrix C: sigma per edge; boundary edges are infinitely sharp (reading R6) */
     for (int32_t k = 0; k < in->K; ++k) {
         int32_t a = in->crease[2 * k], b = in->crease[2 * k + 1];

@@ -396,6 +396,125 @@ def test_semisharp_blend_lies_between_smooth_and_sharp():
     np.testing.assert_allclose(res[0.5], 0.5 * res[0.0] + 0.5 * res[1.0], atol=1e-14)
 
 
+def _bump_grid():
+    """meshgen.grid(4, 4) with z = 1 at vertex 12 = (2, 2): the hand-value fixture of the
+    semi-sharp / multi-crease pins (tests/golden/hand_values.json)."""
+    return mg.grid(4, 4, z=lambda i, j: 1.0 if (i, j) == (2, 2) else 0.0)
+
+
+def _with_creases(m, pairs, sig):
+    m = dict(m)
+    m["crease"] = np.array(pairs, np.int32)
+    m["sigma"] = np.array(sig, np.float32)
+    return m
+
+
+def _check_child_sigma(p0, p1, want, base):
+    got = {(int(a), int(b)): float(s) for (a, b), s in zip(p1["crease"], p1["sigma"])}
+    for k, val in want.items():
+        x, e = k.split("-e")
+        a, b = map(int, e.split("_"))
+        key = (int(x), base + edge_index(p0, a, b))
+        assert got[key] == (math.inf if val == "inf" else float(Q(*val))), k
+    assert len(got) == len(want)
+
+
+def test_semisharp_vertex_hand_values():
+    """k = 2, s = 3/8 < 1: the vertex point is 5/8 smooth + 3/8 sharp (a swapped blend gives
+    87/128, s = max sigma gives 84/128, s over all four edges 76.5/128)."""
+    g = HAND["cc_semisharp_vertex_L1"]
+    r = oracle.refine(_with_creases(_bump_grid(), [(11, 12), (12, 13)], [0.25, 0.5]), "cc", 1)
+    p0, p1 = r
+    base = 25 + 16
+    for v, val in g["vertex"].items():
+        np.testing.assert_allclose(p1["pos"][int(v)], q3(val), atol=1e-15, err_msg=f"vertex {v}")
+    for k, val in g["edge"].items():
+        a, b = map(int, k.split("-"))
+        np.testing.assert_allclose(p1["pos"][base + edge_index(p0, a, b)], q3(val), atol=1e-15, err_msg=k)
+    _check_child_sigma(p0, p1, g["child_sigma"], base)
+
+
+@pytest.mark.parametrize("side", ["sharp", "smooth"])
+def test_semisharp_vertex_continuity(side):
+    """s -> 1- reaches the sharp rule and s -> 0+ the smooth one (no jump at either end of the
+    blend); at s = 1 the result is the sharp rule exactly."""
+    g = HAND["cc_semisharp_vertex_L1"]["limits"]
+    eps = 2.0 ** -20
+    for sig, tol in ([(1.0 - eps, 1e-6), (1.0, 0.0)] if side == "sharp" else [(eps, 1e-6)]):
+        r = oracle.refine(_with_creases(_bump_grid(), [(11, 12), (12, 13)], [sig, sig]), "cc", 1)
+        want = q3(g["sharp_12" if side == "sharp" else "smooth_12"])
+        got = r[1]["pos"][12]
+        assert np.abs(got - want).max() <= tol, (sig, got, want)
+        if tol > 0:
+            assert np.abs(got - want).max() > 0.0  # still blended
+
+
+def test_three_creases_sigma_bar():
+    """P:L440's three adjacent parent creases: sigma_bar excludes the edge itself (an included
+    edge gives 1.0417 instead of 17/16 for the sigma = 2 edge); k = 3 makes the vertex a corner."""
+    g = HAND["cc_three_creases_L1"]
+    r = oracle.refine(_with_creases(_bump_grid(), [(11, 12), (12, 13), (12, 17)], [2.0, 3.0, 1.5]), "cc", 1)
+    p0, p1 = r
+    for v, val in g["vertex"].items():
+        np.testing.assert_allclose(p1["pos"][int(v)], q3(val), atol=1e-15)
+    _check_child_sigma(p0, p1, g["child_sigma"], 25 + 16)
+
+
+def test_sigma_bar_excludes_inf_and_boundary():
+    g = HAND["cc_sigma_bar_exclusions_L1"]
+    r = oracle.refine(_with_creases(_bump_grid(), [(11, 12), (7, 12), (5, 6)], [2.0, np.inf, 2.0]), "cc", 1)
+    _check_child_sigma(r[0], r[1], g["child_sigma"], 25 + 16)
+
+
+def _pillow2():
+    return mg._pack([(0, 1, 2, 3), (0, 3, 2, 1)], [(0, 0, 1), (1, 0, 0), (1, 1, 0), (0, 1, 0)], name="pillow2")
+
+
+def _bowtie():
+    return mg._pack([(0, 1, 2), (0, 3, 4)], [(0, 0, 1), (1, 0, 0), (1, 1, 0), (-1, 0, 0), (-1, -1, 0)], name="bowtie")
+
+
+def test_interior_valence2_pillow():
+    """Reading R17: interior vertices with n = 2 use the CC formula as written."""
+    g = HAND["cc_pillow_L1"]
+    r = oracle.refine(_pillow2(), "cc", 1)
+    for v, val in g["vertex"].items():
+        np.testing.assert_allclose(r[1]["pos"][int(v)], q3(val), atol=1e-15)
+    np.testing.assert_allclose(r[1]["pos"][4 + 2 + edge_index(r[0], 0, 1)], q3(g["edge"]["0-1"]), atol=1e-15)
+
+
+def test_bowtie_vertex_is_a_corner():
+    """Reading R18: two open fans at a vertex are allowed; the vertex (k = 4 boundary edges) stays."""
+    g = HAND["cc_bowtie_L1"]
+    r = oracle.refine(_bowtie(), "cc", 1)
+    for v, val in g["vertex"].items():
+        np.testing.assert_allclose(r[1]["pos"][int(v)], q3(val), atol=1e-15)
+
+
+def _split_edge_cube():
+    """The cube with vertex 8 inserted in edge (0,1): two pentagons, and vertex 8 is an interior
+    vertex of valence 2 (reading R17)."""
+    c = mg.cube()
+    faces = [list(c["face_vtx"][c["face_off"][i]:c["face_off"][i + 1]]) for i in range(6)]
+    out = []
+    for f in faces:
+        g = []
+        for t in range(len(f)):
+            g.append(f[t])
+            if {f[t], f[(t + 1) % len(f)]} == {0, 1}:
+                g.append(8)
+        out.append(g)
+    return mg._pack(out, np.vstack([c["pos"], [[0.5, 0.0, 0.0]]]), name="cube_split_edge")
+
+
+def _two_tets_sharing_a_vertex(open_second=False):
+    pos = [(1, 1, 1), (1, -1, -1), (-1, 1, -1), (-1, -1, 1)]
+    pos += [(3 + x, y, z) for (x, y, z) in pos[1:]]
+    A = [(0, 1, 2), (0, 3, 1), (0, 2, 3), (1, 3, 2)]
+    B = [(0, 4, 5), (0, 6, 4), (0, 5, 6), (4, 6, 5)]
+    return mg._pack(A + (B[:1] if open_second else B), pos, name="two_fans")
+
+
 # ------------------------------------------------------------------------------------------
 # independent exact-rational brute force (tests/bruteforce.py)
 # ------------------------------------------------------------------------------------------
@@ -418,6 +537,9 @@ BF_CASES = [
     ("cc", lambda: mg.grid(3, 2, tri_cells=[(1, 0)]), 2), ("cc", _pillow, 2),
     ("cc", lambda: (lambda m: m.update(crease=np.array([[1, 5], [5, 9], [0, 1], [6, 7]], np.int32),
                                        sigma=np.array([0.75, 2.5, 1.5, 0.25], np.float32)) or m)(mg.grid(3, 2)), 2),
+    ("cc", lambda: _with_creases(_bump_grid(), [(11, 12), (12, 13), (12, 17), (6, 7)], [0.25, 0.75, 2.5, 0.5]), 2),
+    ("cc", _split_edge_cube, 2), ("cc", _pillow2, 2), ("cc", _bowtie, 2),
+    ("loop", lambda: _with_creases(mg.tetrahedron(), [(0, 1), (1, 2)], [0.25, 0.75]), 1),
     ("loop", mg.tetrahedron, 1), ("loop", _octahedron, 1), ("loop", lambda: mg.tetrahedron(creased=True), 1),
     ("sqrt3", mg.tetrahedron, 1), ("sqrt3", _octahedron, 1),
     ("sqrt3", lambda: mg.torus_tris(4, 4, regular=True), 1),
@@ -482,6 +604,8 @@ def test_error_paths():
     pos = np.zeros((5, 3), np.float32)
     assert err(mg._pack([(0, 1, 2), (0, 1, 3)], pos)) == "E_NONMANIFOLD"          # flipped orientation
     assert err(mg._pack([(0, 1, 2), (1, 0, 3), (0, 1, 4)], pos)) == "E_NONMANIFOLD"  # 3 faces on an edge
+    assert err(_two_tets_sharing_a_vertex()) == "E_NONMANIFOLD"                 # two closed fans (R18)
+    assert err(_two_tets_sharing_a_vertex(open_second=True)) == "E_NONMANIFOLD"  # closed + open fan
     assert err(mg._pack([(0, 1, 7)], pos)) == "E_MESH"
     assert err(mg._pack([(0, 1)], pos)) == "E_MESH"
     assert err(mg._pack([(0, 1, 1, 2)], pos)) == "E_MESH"
