@@ -294,6 +294,9 @@ static alsub_status create_impl(const int32_t *face_off, const int32_t *face_vtx
     b.vtx_cur = A<int32_t>(m, num_verts, s, ML, ok);
     b.flags = A<int32_t>(m, 8, s, ML, ok);
     b.scalars = A<int32_t>(m, 8, s, ML, ok);
+    b.long_list = A<int32_t>(m, num_verts, s, ML, ok);
+    b.long_keys = A<uint64_t>(m, 4 * (int64_t)S0, s, ML, ok);
+    b.nlong = -1;
     m->scratch_bytes = build0_scratch_bytes(num_verts, S0);
     m->scratch = dev_alloc(m, m->scratch_bytes, s, ML);
     b.scratch = m->scratch;
@@ -349,6 +352,7 @@ static alsub_status create_impl(const int32_t *face_off, const int32_t *face_vtx
     m->B0 = sc[1];
     m->K0 = sc[2];
     m->NSV0 = sc[3];
+    b.nlong = sc[5];
     m->user_creases = (m->K0 - m->B0) > 0;
     b.no_special = m->K0 == 0 && m->B0 == 0;
     CU(cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking));

@@ -55,31 +55,10 @@ __global__ void __launch_bounds__(kThreads) k_b0_scatter(const int32_t *__restri
     vtx_slot[vtx_off[v] + atomicAdd(cur + v, 1)] = h;
 }
 
-// Candidate q of vertex j's collision list: slot vtx_slot[o0 + q/2], neighbour next (q even) or prev.
-// NC = false: the rows were written earlier in the same kernel (k_edge_count sorts them), so they
-// are read through L1 rather than the read-only path
-template <int ORDER, bool NC = true>
-struct Cand {
-    const int32_t *face_vtx, *vtx_slot;
-    Topo<ORDER> tp;
-    int32_t o0;
-    ALSUB_D int32_t slot(int32_t q) const { return NC ? __ldg(vtx_slot + o0 + (q >> 1)) : vtx_slot[o0 + (q >> 1)]; }
-    ALSUB_D int32_t vert(int32_t q) const {
-        int32_t h = slot(q);
-        return __ldg(face_vtx + ((q & 1) ? tp.prev(h) : tp.next(h)));
-    }
-    // first occurrence of value x among candidates [0, q)
-    ALSUB_D bool first(int32_t q, int32_t x) const {
-        for (int32_t p = 0; p < q; ++p)
-            if (vert(p) == x) return false;
-        return true;
-    }
-};
-
 // Warp-per-vertex collision processing: lane q < 2n holds candidate q of vertex j (slot q/2,
 // neighbour next (q even) or prev (q odd)); duplicates are found with __match_any_sync and the
 // rank of a distinct neighbour among the distinct neighbours < j with a ballot per lane.
-// Vertices with more than 16 incident faces fall back to a serial loop on lane 0.
+// Vertices with more than 16 incident faces are listed for k_long_rows (block per row).
 struct WarpCand {
     int32_t x;     // neighbour vertex (INT32_MAX = none)
     int32_t slot;  // the slot of the directed edge (j -> x for next, x -> j for prev)
@@ -110,7 +89,8 @@ ALSUB_D WarpCand warp_cand(const int32_t *face_vtx, const int32_t *vtx_slot, Top
 // the diagonal)
 template <int ORDER>
 __global__ void k_edge_count(const int32_t *__restrict__ face_vtx, const int32_t *__restrict__ vtx_off,
-                             const int32_t *vtx_slot, Topo<ORDER> tp, int32_t V, int32_t *__restrict__ cnt) {
+                             const int32_t *vtx_slot, Topo<ORDER> tp, int32_t V, int32_t *__restrict__ cnt,
+                             int32_t *__restrict__ long_list, int32_t *long_cnt) {
     ALSUB_GRID_WAIT();
     const int32_t j = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
@@ -130,20 +110,8 @@ __global__ void k_edge_count(const int32_t *__restrict__ face_vtx, const int32_t
         if (lane == 0) cnt[j] = __popc(b);
         return;
     }
-    if (lane != 0) return;
-    for (int32_t a = 1; a < n; ++a) {  // long rows: insertion sort on one lane
-        const int32_t x = row[a];
-        int32_t b = a - 1;
-        while (b >= 0 && row[b] > x) { row[b + 1] = row[b]; --b; }
-        row[b + 1] = x;
-    }
-    Cand<ORDER, false> cd{face_vtx, vtx_slot, tp, o0};
-    int32_t k = 0;
-    for (int32_t q = 0; q < 2 * n; ++q) {
-        int32_t x = cd.vert(q);
-        if (x < j && cd.first(q, x)) ++k;
-    }
-    cnt[j] = k;
+    // long rows (poles, fan caps): one block per row in k_long_rows (sorted in shared memory)
+    if (lane == 0) long_list[atomicAdd(long_cnt, 1)] = j;
 }
 
 ALSUB_D void emit_edge(int32_t e, int32_t s_ij, int32_t s_ji, int32_t i, int32_t j, int32_t *face_edge, int32_t *face_twin,
@@ -196,26 +164,198 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
         }
         return;
     }
-    if (lane != 0) return;
-    Cand<ORDER> cd{face_vtx, vtx_slot, tp, o0};
-    const int32_t nq = 2 * n;
-    for (int32_t q = 0; q < nq; ++q) {
-        int32_t i = cd.vert(q);
-        if (i >= j || !cd.first(q, i)) continue;
-        int32_t rank = 0;
-        for (int32_t p = 0; p < nq; ++p) {
-            int32_t x = cd.vert(p);
-            if (x < i && cd.first(p, x)) ++rank;
+    // long rows: k_long_rows<..., true>
+}
+
+// ------------------------------------------------------------------------------------------
+// Long rows of M^T (n > 16 incident slots: poles, fan caps).  One block per listed row: the row
+// and its 2n collision candidates (key = neighbour << 32 | candidate index) are sorted with a
+// block-wide bitonic network, so equal neighbours are adjacent, the first of each run is the
+// first occurrence, a run's length and parity give E(i,j) and the directed slots, and the rank of
+// a distinct neighbour is an exclusive count of run starts -- O(n log^2 n) work spread over the
+// block instead of the warp path's 32 candidate lanes.  Rows of up to kLongFast / 2 slots sort in
+// registers (count pass; the sorted candidates are kept in a global scratch, 4 keys per slot, for
+// the fill pass); longer rows run the same steps as a plain bitonic network in that scratch.
+// count pass (FILL = false): sort the row in place + number of distinct neighbours i < j;
+// fill pass (FILL = true): ids, twins, multiplicity checks, boundary bits (rows already sorted).
+// ------------------------------------------------------------------------------------------
+constexpr int kLongThreads = 512;
+constexpr int kLongFast = 4 * kLongThreads;  // keys sorted in registers (4 per thread)
+
+ALSUB_D int32_t pow2_at_least(int32_t n) {
+    int32_t p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+
+// ascending bitonic sort of a[0, n), n a power of two, by the whole block (rows > kLongFast / 2)
+ALSUB_D void block_bitonic(uint64_t *a, int32_t n) {
+    for (int32_t k = 2; k <= n; k <<= 1)
+        for (int32_t jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
+                const int32_t l = i ^ jj;
+                if (l > i) {
+                    const uint64_t x = a[i], y = a[l];
+                    if ((x > y) == ((i & k) == 0)) { a[i] = y; a[l] = x; }
+                }
+            }
+            __syncthreads();
         }
-        int32_t s_ji = -1, s_ij = -1, m_ji = 0, m_ij = 0;
-        for (int32_t a = 0; a < n; ++a) {
-            int32_t h = cd.slot(2 * a);
-            if (__ldg(face_vtx + tp.next(h)) == i) { s_ji = h; ++m_ji; }
-            int32_t hp = tp.prev(h);
-            if (__ldg(face_vtx + hp) == i) { s_ij = hp; ++m_ij; }
+}
+
+// ascending bitonic sort of kLongFast keys, element 4 tid + r in v[r]: partners inside the thread
+// (stride < 4) in registers, inside the warp (< 128) by shuffles, across warps through s_x --
+// 10 of the 66 stages touch shared memory
+ALSUB_D void block_sort4(uint64_t (&v)[4], uint64_t *s_x) {
+    const int tid = threadIdx.x;
+    for (int k = 2; k <= kLongFast; k <<= 1) {
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            if (jj >= 128) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) s_x[4 * tid + r] = v[r];
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int i = 4 * tid + r;
+                    const uint64_t o = s_x[i ^ jj];
+                    v[r] = (((i & jj) == 0) == ((i & k) == 0)) ? min(v[r], o) : max(v[r], o);
+                }
+                __syncthreads();
+            } else if (jj >= 4) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int i = 4 * tid + r;
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v[r], jj >> 2);
+                    v[r] = (((i & jj) == 0) == ((i & k) == 0)) ? min(v[r], o) : max(v[r], o);
+                }
+            } else {  // strides 2 and 1 inside the thread (constant register indices)
+                const bool a01 = ((4 * tid) & k) == 0, a23 = ((4 * tid + 2) & k) == 0;  // differ only for k = 2
+                auto cs = [](uint64_t &a, uint64_t &b, bool asc) {
+                    const uint64_t lo = min(a, b), hi = max(a, b);
+                    a = asc ? lo : hi;
+                    b = asc ? hi : lo;
+                };
+                if (jj == 2) { cs(v[0], v[2], a01); cs(v[1], v[3], a01); }
+                else { cs(v[0], v[1], a01); cs(v[2], v[3], a23); }
+            }
         }
-        if (m_ji > 1 || m_ij > 1) atomicOr(flags, kFlagNonManifold);
-        emit_edge(edge_off[j] + rank, s_ij, s_ji, i, j, face_edge, face_twin, edge_hh, bnd_word, vbnd, scalars);
+    }
+}
+
+// exclusive block scan of one flag per thread; returns the prefix, *total = the round's sum
+ALSUB_D int32_t block_excl_scan(bool flag, int32_t *s_w, int32_t *total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const unsigned b = __ballot_sync(0xffffffffu, flag);
+    if (lane == 0) s_w[w] = __popc(b);
+    __syncthreads();
+    int32_t before = 0, all = 0;
+    for (int k = 0; k < nw; ++k) {
+        const int32_t c = s_w[k];
+        before += k < w ? c : 0;
+        all += c;
+    }
+    __syncthreads();
+    *total = all;
+    return before + __popc(b & ((1u << lane) - 1u));
+}
+
+// candidate key q of row j: even q = next(h) (slot h carries j -> x), odd = prev(h) (x -> j)
+template <int ORDER>
+ALSUB_D uint64_t cand_key(const int32_t *face_vtx, const int32_t *row, Topo<ORDER> tp, int32_t q, int32_t nq) {
+    if (q >= nq) return ~0ull;
+    const int32_t h = row[q >> 1];
+    const int32_t x = __ldg(face_vtx + ((q & 1) ? tp.prev(h) : tp.next(h)));
+    return ((uint64_t)(uint32_t)x << 32) | (uint32_t)q;
+}
+
+template <int ORDER, bool FILL>
+__global__ void __launch_bounds__(kLongThreads) k_long_rows(const int32_t *__restrict__ face_vtx,
+                                                          const int32_t *__restrict__ vtx_off, int32_t *vtx_slot,
+                                                          Topo<ORDER> tp, const int32_t *__restrict__ long_list,
+                                                          const int32_t *long_cnt, uint64_t *__restrict__ g_keys,
+                                                          int32_t *__restrict__ cnt, const int32_t *__restrict__ edge_off,
+                                                          int32_t *__restrict__ face_edge, int32_t *__restrict__ face_twin,
+                                                          int2 *__restrict__ edge_hh, uint32_t *__restrict__ bnd_word,
+                                                          int32_t *__restrict__ vbnd, int32_t *__restrict__ scalars,
+                                                          int32_t *flags) {
+    ALSUB_GRID_WAIT();
+    __shared__ uint64_t s_key[kLongFast];
+    __shared__ int32_t s_w[kLongThreads / 32];
+    const int32_t nl = *long_cnt;
+    const int tid = threadIdx.x;
+    for (int32_t idx = blockIdx.x; idx < nl; idx += gridDim.x) {
+        const int32_t j = long_list[idx];
+        const int32_t o0 = vtx_off[j], n = vtx_off[j + 1] - o0;
+        const int32_t nq = 2 * n;
+        int32_t *row = vtx_slot + o0;
+        uint64_t *gk = g_keys + 4 * (int64_t)o0;  // 4 n keys of room (>= the padded 2 n)
+        const bool fast = nq <= kLongFast;
+        const int32_t P2 = fast ? kLongFast : pow2_at_least(nq);
+        const uint64_t *key = fast ? s_key : gk;
+        if (fast) {
+            uint64_t v[4];
+            if constexpr (!FILL) {  // sort the row by slot, then its candidates; keep them for the fill pass
+#pragma unroll
+                for (int r = 0; r < 4; ++r) v[r] = 4 * tid + r < n ? (uint64_t)row[4 * tid + r] : ~0ull;
+                block_sort4(v, s_key);
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (4 * tid + r < n) row[4 * tid + r] = (int32_t)v[r];
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < 4; ++r) v[r] = cand_key(face_vtx, row, tp, 4 * tid + r, nq);
+                block_sort4(v, s_key);
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    s_key[4 * tid + r] = v[r];
+                    if (4 * tid + r < nq) gk[4 * tid + r] = v[r];
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) s_key[4 * tid + r] = 4 * tid + r < nq ? gk[4 * tid + r] : ~0ull;
+            }
+            __syncthreads();
+        } else {  // long rows beyond the register sort: the same steps in global memory
+            if constexpr (!FILL) {
+                const int32_t P1 = pow2_at_least(n);
+                for (int32_t i = tid; i < P1; i += blockDim.x) gk[i] = i < n ? (uint64_t)row[i] : ~0ull;
+                __syncthreads();
+                block_bitonic(gk, P1);
+                for (int32_t i = tid; i < n; i += blockDim.x) row[i] = (int32_t)gk[i];
+                __syncthreads();
+            }
+            for (int32_t q = tid; q < P2; q += blockDim.x) gk[q] = cand_key(face_vtx, row, tp, q, nq);
+            __syncthreads();
+            block_bitonic(gk, P2);
+        }
+        // run starts with x < j (padding keys have x = 0xffffffff > any j); rank = exclusive count
+        int32_t base = 0;
+        for (int32_t p0 = 0; p0 < P2; p0 += blockDim.x) {
+            const int32_t p = p0 + tid;
+            const uint32_t x = p < P2 ? (uint32_t)(key[p] >> 32) : 0xffffffffu;
+            const bool start = p < P2 && x < (uint32_t)j && (p == 0 || (uint32_t)(key[p - 1] >> 32) != x);
+            int32_t total;
+            const int32_t rank = base + block_excl_scan(start, s_w, &total);
+            if constexpr (FILL) {
+                if (start) {
+                    int32_t s_ij = -1, s_ji = -1, m_ij = 0, m_ji = 0;
+                    for (int32_t r = p; r < nq && (uint32_t)(key[r] >> 32) == x; ++r) {
+                        const int32_t q = (int32_t)(uint32_t)key[r];
+                        const int32_t h = row[q >> 1];
+                        if (q & 1) { s_ij = tp.prev(h); ++m_ij; }
+                        else { s_ji = h; ++m_ji; }
+                    }
+                    if (m_ij > 1 || m_ji > 1) atomicOr(flags, kFlagNonManifold);
+                    emit_edge(edge_off[j] + rank, s_ij, s_ji, (int32_t)x, j, face_edge, face_twin, edge_hh, bnd_word,
+                              vbnd, scalars);
+                }
+            }
+            base += total;
+        }
+        if constexpr (!FILL) {
+            if (tid == 0) cnt[j] = base;
+        }
+        __syncthreads();
     }
 }
 
@@ -383,7 +523,7 @@ void build0_zero_segments(Build0 &b, ZeroSegs &z) {
     const int32_t E = b.E, nw = (int32_t)ceil_div(E > 0 ? E : 1, 32);
     z.add(b.vtx_cnt, (int64_t)b.V + 1);
     z.add(b.vtx_cur, b.V);
-    z.add(b.scalars + 1, 3);
+    z.add(b.scalars + 1, 5);  // B, K, NSV, -, long-row count
     z.add(b.bnd_word, nw);
     z.add(b.vbnd, b.V);
     z.add(b.edge_sigma, E);
@@ -403,6 +543,16 @@ void build0_validate(Build0 &b, cudaStream_t s, Launches &L) {
                b.slot_face, b.vtx_cnt, b.flags);
 }
 
+// long rows: launched when the create found some (nlong > 0) or does not know yet (nlong < 0)
+template <int ORDER, bool FILL>
+static void long_rows(Build0 &b, Topo<ORDER> tp, cudaStream_t s, Launches &L) {
+    if (b.V == 0 || b.nlong == 0) return;
+    const unsigned grid = (unsigned)(b.nlong < 0 ? 148 : std::min<int32_t>(b.nlong, 148));
+    launch(L, FILL ? "b0_long_fill" : "b0_long_count", k_long_rows<ORDER, FILL>, dim3(grid), dim3(kLongThreads), 0, s,
+           b.face_vtx, b.vtx_off, b.vtx_slot, tp, b.long_list, b.scalars + 5, b.long_keys, b.edge_cnt, b.edge_off,
+           b.face_edge, b.face_twin, b.edge_hh, b.bnd_word, b.vbnd, b.scalars, b.flags);
+}
+
 // a2 + symbolic a3: M^T (row lengths scanned into vtx_off, slots scattered into their rows, rows
 // sorted inside k_edge_count), then the per-vertex upper-triangle counts of E
 template <int ORDER>
@@ -415,7 +565,8 @@ static void count_edges(Build0 &b, cudaStream_t s, Launches &L) {
                b.vtx_cur, b.vtx_slot);
     if (b.V > 0)
         launch(L, "b0_edge_count", k_edge_count<ORDER>, dim3(grid_for(32 * (int64_t)b.V)), dim3(kThreads), 0, s, b.face_vtx,
-               b.vtx_off, b.vtx_slot, tp, b.V, b.edge_cnt);
+               b.vtx_off, b.vtx_slot, tp, b.V, b.edge_cnt, b.long_list, b.scalars + 5);
+    long_rows<ORDER, false>(b, tp, s, L);
     scan_exclusive(b.edge_cnt, b.edge_off, b.V, b.scalars + 0, region(b, 2), s, L, b.zeroed);
 }
 void build0_count_edges(Build0 &b, cudaStream_t s, Launches &L) {
@@ -440,6 +591,7 @@ static void fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
                                                                        b.edge_off, b.face_edge, b.face_twin, b.edge_hh,
                                                                        b.bnd_word, b.vbnd, b.scalars, b.flags,
                                                                        b.vtx_slot0);
+        long_rows<ORDER, true>(b, tp, s, L);
         if (check_fans) {
             launch(L, "b0_check_fans", k_check_fans<ORDER>, dim3(grid_for(b.V)), dim3(kThreads), 0, s, b.face_twin, b.vtx_off, b.vtx_slot0, tp, b.V, b.flags);
         }

@@ -653,6 +653,46 @@ ALSUB_D void cc_vertex_smooth(const VtxCtx<ORDER> &x, const Frames &fr, const VS
     }
 }
 
+// a long level-0 ring (n > kLongRing, not boundary, not special), summed by the whole warp; the
+// same two forms as cc_vertex_smooth: c0 corner sums (levels >= 1) or slot gathers (level 0)
+template <int ORDER>
+ALSUB_D bool cc_long_ring(const VSegs &g, const LevelDev &p, int32_t j, bool cr) {
+    const int32_t n = __ldg(g.vtx_off0 + j + 1) - __ldg(g.vtx_off0 + j);
+    if (n <= kLongRing || __ldg(g.vbnd0 + j)) return false;
+    return !(cr && p.sv_off[j + 1] > p.sv_off[j]);
+}
+
+template <int ORDER>
+ALSUB_D void cc_vertex_long(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs &g, int32_t j, int lane) {
+    const int shift = 2 * g.level;
+    const int32_t o = __ldg(g.vtx_off0 + j), cnt = __ldg(g.vtx_off0 + j + 1) - o;
+    const bool c0p = fr.c0 && shift >= 2;
+    const float inv = 1.0f / (float)cnt;
+    for (int f = 0; f < fr.nb; ++f) {
+        P3 acc = p3zero();
+        // 8 slots per lane in flight: the chain list -> (face_vtx ->) position is latency bound
+        for (int32_t k0 = lane; k0 < cnt; k0 += 32 * 8) {
+            int32_t b[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) b[u] = k0 + 32 * u < cnt ? __ldg(g.vtx_list0 + o + k0 + 32 * u) : -1;
+            if (c0p) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (b[u] >= 0) acc = acc + ld3c(fr.c0r(f), b[u] << (shift - 2));
+            } else {
+                int32_t nb[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) nb[u] = b[u] >= 0 ? __ldg(x.face_vtx + x.tl.next(b[u] << shift)) : -1;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (b[u] >= 0) acc = acc + ld3(fr.rd(f), nb[u]) + ld3c(fr.wr(f), x.V + x.tl.face(b[u] << shift));
+            }
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) st3(fr.wr(f), j, (1.0f - 2.0f * inv) * ld3(fr.rd(f), j) + (inv * inv) * acc);
+    }
+}
+
 template <int ORDER, int PL, bool CR>
 __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, VSegs g, int32_t *csv_list) {
     ALSUB_GRID_WAIT();
@@ -712,9 +752,11 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
             }
             continue;
         }
+        unsigned longm = 0;  // long level-0 rings of this lane, done cooperatively below
         for (int k = 0; k < PL; ++k) {
             const int32_t j = j0 + 32 * k;
             if (j >= len) continue;
+            if (g.type[s] == 0 && cc_long_ring<ORDER>(g, p, j, CR)) { longm |= 1u << k; continue; }
             if (s == g.gp_skip_seg) {
                 // done by k_cc_edge_gp when the 4 child edges of interior edge j (ids base ..
                 // base + 3) are in one of its blocks
@@ -725,6 +767,16 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
                 }
             }
             cc_vertex_one<ORDER, CR>(x, fr, g, p, csv_list, s, j);
+        }
+        if (g.type[s] == 0) {  // warp-uniform: the task lies in one segment
+            for (int k = 0; k < PL; ++k) {
+                unsigned m = __ballot_sync(0xffffffffu, (longm >> k) & 1u);
+                while (m) {
+                    const int src = __ffs(m) - 1;
+                    m &= m - 1;
+                    cc_vertex_long<ORDER>(x, fr, g, j0 - lane + src + 32 * k, lane);
+                }
+            }
         }
     }
 }

@@ -120,6 +120,21 @@ ALSUB_D P3 operator+(P3 a, P3 b) { return P3{a.x + b.x, a.y + b.y, a.z + b.z}; }
 ALSUB_D P3 operator*(float s, P3 a) { return P3{s * a.x, s * a.y, s * a.z}; }
 ALSUB_D P3 p3zero() { return P3{0.f, 0.f, 0.f}; }
 
+// Long rings (level-0 vertices with more than kLongRing incident slots, e.g. poles): the vertex
+// kernels skip them in their per-lane pass and then sum each one's ring with the whole warp --
+// lanes take slots k = lane, lane + 32, ...; warp_sum is a fixed xor butterfly, so the result is
+// deterministic (and identical between refine and eval_frames, which share the kernels).
+constexpr int32_t kLongRing = 32;
+ALSUB_D P3 warp_sum(P3 a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+        a.z += __shfl_xor_sync(0xffffffffu, a.z, o);
+    }
+    return a;
+}
+
 // Boundary-edge prefix: bprefix(e) = number of boundary edges with id < e, from a bitmask and
 // per-word exclusive prefix.
 ALSUB_D int32_t bprefix(const uint32_t *__restrict__ words, const int32_t *__restrict__ wpre, int32_t e) {

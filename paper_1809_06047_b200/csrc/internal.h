@@ -149,7 +149,10 @@ struct Build0 {
     uint32_t *spw;                // [ceil(E/32)] special-edge bitmask (level 0)
     int32_t *spwpre;              // [ceil(E/32)] its per-word prefix (= sp_off at the word start)
     int32_t *flags;               // device status flags
-    int32_t *scalars;             // device scalars: [0] E, [1] B, [2] K special, [3] NSV
+    int32_t *scalars;             // device scalars: [0] E, [1] B, [2] K special, [3] NSV, [5] long rows
+    int32_t *long_list;           // [V] vertices with > 16 incident slots (k_long_rows)
+    uint64_t *long_keys;          // [4 S] sort keys of rows longer than the shared-memory cap
+    int32_t nlong = -1;           // number of long rows (-1: not known yet, i.e. inside create)
     int32_t E;                    // host-known after the count pass (create) or plan (refine)
     void *scratch;
     bool zeroed = false;          // refine: every work array and scan region pre-initialised by k_zero

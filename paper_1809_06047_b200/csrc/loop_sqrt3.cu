@@ -266,8 +266,9 @@ __global__ void __launch_bounds__(kThreads) k_loop_edge(LevelDev p, ChildDev c, 
 template <bool ADJ>
 __global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c, Frames fr, VSegs g) {
     ALSUB_GRID_WAIT();
-    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= p.V) return;
+    const int32_t v0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = v0 < p.V;
+    const int32_t v = valid ? v0 : p.V - 1;
     int s = g.nseg - 1;
     while (s > 0 && v < g.start[s]) --s;
     const int32_t j = v - g.start[s];
@@ -300,7 +301,9 @@ __global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c
         for (int h = 0; h < hops; ++h) x = loop_c0(x);
         return x;
     };
-    for (int f = 0; f < fr.nb; ++f) {
+    // long level-0 rings: summed by the whole warp after the per-lane pass
+    const bool lng = valid && lv0 && !bnd && n > kLongRing;
+    for (int f = 0; f < fr.nb && valid && !lng; ++f) {
         const PR P = fr.rd(f);
         const PW Pn = fr.wr(f);
         const P3 pv = ld3(P, v);
@@ -316,6 +319,35 @@ __global__ void __launch_bounds__(kThreads) k_loop_vertex(LevelDev p, ChildDev c
         }
         const float beta = loop_beta(n);
         st3(Pn, v, (1.0f - (float)n * beta) * pv + beta * acc);
+    }
+    const int lane = threadIdx.x & 31;
+    unsigned m = __ballot_sync(0xffffffffu, lng);
+    while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int32_t jj = __shfl_sync(0xffffffffu, j, src), vv = __shfl_sync(0xffffffffu, v, src);
+        const int32_t oo = __ldg(g.vtx_off0 + jj), nn = __ldg(g.vtx_off0 + jj + 1) - oo;
+        const float beta = loop_beta(nn);
+        for (int f = 0; f < fr.nb; ++f) {
+            const PR P = fr.rd(f);
+            P3 acc = p3zero();
+            for (int32_t k0 = lane; k0 < nn; k0 += 32 * 8) {  // 8 independent chains per lane
+                int32_t x[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) x[u] = k0 + 32 * u < nn ? __ldg(g.vtx_list0 + oo + k0 + 32 * u) : -1;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (x[u] < 0) continue;
+                    for (int h = 0; h < g.level; ++h) x[u] = loop_c0(x[u]);  // born at level 0 (the lane's
+                    x[u] = __ldg(p.face_vtx + tri_next(x[u]));             // own segment may differ)
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (x[u] >= 0) acc = acc + ld3(P, x[u]);
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) st3(fr.wr(f), vv, (1.0f - (float)nn * beta) * ld3(P, vv) + beta * acc);
+        }
     }
 }
 
@@ -464,9 +496,40 @@ __global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, V
     for (int32_t task = warp; task < ntask; task += nwarp) {
         while (s_pre[s + 1] <= task) ++s;
         const int32_t j = ((s_lo[s] + (task - s_pre[s])) << 5) + lane;
+        const int32_t mult = g.mult[s];
+        const bool closed = g.level >= 1;
+        const int32_t vfp = g.start[g.nseg - 1];  // first face point born at this level (= V_{l-1})
+        if (g.type[s] == 0) {  // warp-uniform: long level-0 rings summed by the whole warp
+            const bool lng = j < g.len[s] && __ldg(g.vtx_off0 + j + 1) - __ldg(g.vtx_off0 + j) > kLongRing;
+            unsigned m = __ballot_sync(0xffffffffu, lng);
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const int32_t jj = j - lane + src, vv = g.start[s] + jj;
+                const int32_t oo = __ldg(g.vtx_off0 + jj), nn = __ldg(g.vtx_off0 + jj + 1) - oo;
+                const float alpha = sqrt3_alpha(nn);
+                for (int f = 0; f < nb; ++f) {
+                    const PR P = fr.rd(f);
+                    P3 acc = p3zero();
+                    for (int32_t k0 = lane; k0 < nn; k0 += 32 * 8) {  // 8 independent chains per lane
+                        int32_t q[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) q[u] = k0 + 32 * u < nn ? __ldg(g.vtx_list0 + oo + k0 + 32 * u) * mult : -1;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (q[u] >= 0) q[u] = closed ? vfp + q[u] / 9 : __ldg(p.face_vtx + tri_next(q[u]));
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (q[u] >= 0) acc = acc + ld3(P, q[u]);
+                    }
+                    acc = warp_sum(acc);
+                    if (lane == 0) st3(fr.wr(f), vv, (1.0f - alpha) * ld3(P, vv) + (alpha / (float)nn) * acc);
+                }
+            }
+            if (lng) continue;
+        }
         if (j >= g.len[s]) continue;
         const int32_t v = g.start[s] + j;
-        const int32_t mult = g.mult[s];
         if (g.type[s] == 1 && g.birth[s] == g.level) {
             // face point of parent face j: neighbours = its corners + the 3 adjacent face points
             const int m1 = g.birth[s] - 1;
@@ -505,8 +568,6 @@ __global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, V
         const float alpha = n > 0 ? sqrt3_alpha(n) : 0.0f;
         // level >= 1: every neighbour of an old vertex is a face point born at this level, the one
         // of the level-(l-1) face (slot / 9) holding the vertex's level-l slot -- no face lookup
-        const bool closed = g.level >= 1;
-        const int32_t vfp = g.start[g.nseg - 1];  // first face point born at this level (= V_{l-1})
         for (int f = 0; f < nb; ++f) {
             const PR P = fr.rd(f);
             const PW Pn = fr.wr(f);

@@ -615,3 +615,60 @@ def test_error_paths():
     assert err(dict(c, crease=np.array([[0, 1], [1, 0]], np.int32), sigma=np.array([1.0, 2.0], np.float32))) == "E_CREASE"
     assert err(c, "loop") == "E_SCHEME"
     assert err(mg.grid(2, 2, tri_cells=[(0, 0), (1, 0), (0, 1), (1, 1)]), "sqrt3") == "E_SCHEME"
+
+
+# ------------------------------------------------------------------------------------------
+# orientation (reading R13 for sqrt3, R2 for CC, a10 for Loop): a geometric pin that does not go
+# through the brute force's own vertex order -- on a convex closed control mesh centred at the
+# origin every refined face keeps an outward normal and the enclosed signed volume stays positive
+# ------------------------------------------------------------------------------------------
+
+def newell_normals(pos, face_off, face_vtx):
+    """Newell normal and centroid of every polygon (plain definition, any order)."""
+    n = np.zeros((len(face_off) - 1, 3))
+    c = np.zeros_like(n)
+    for r in range(len(face_off) - 1):
+        p = pos[face_vtx[face_off[r]:face_off[r + 1]]]
+        q = np.roll(p, -1, axis=0)
+        n[r] = [np.sum((p[:, 1] - q[:, 1]) * (p[:, 2] + q[:, 2])),
+                np.sum((p[:, 2] - q[:, 2]) * (p[:, 0] + q[:, 0])),
+                np.sum((p[:, 0] - q[:, 0]) * (p[:, 1] + q[:, 1]))]
+        c[r] = p.mean(0)
+    return n, c
+
+
+def signed_volume(pos, face_off, face_vtx):
+    """Divergence theorem over a fan triangulation of every face: > 0 for outward orientation."""
+    vol = 0.0
+    for r in range(len(face_off) - 1):
+        f = face_vtx[face_off[r]:face_off[r + 1]]
+        for t in range(1, len(f) - 1):
+            vol += np.linalg.det(np.stack([pos[f[0]], pos[f[t]], pos[f[t + 1]]])) / 6.0
+    return vol
+
+
+def check_outward(rec, what):
+    n, c = newell_normals(rec["pos"], rec["face_off"], rec["face_vtx"])
+    dots = np.einsum("ij,ij->i", n, c)
+    assert (dots > 0).all(), f"{what}: {int((dots <= 0).sum())} inward faces"
+    assert signed_volume(rec["pos"], rec["face_off"], rec["face_vtx"]) > 0, what
+
+
+@pytest.mark.parametrize("scheme,mk", [("sqrt3", _octahedron), ("sqrt3", mg.icosahedron), ("sqrt3", mg.tetrahedron),
+                                       ("loop", mg.icosahedron), ("loop", _octahedron), ("cc", mg.cube),
+                                       ("cc", mg.tetrahedron)])
+def test_orientation_outward_convex(scheme, mk):
+    mesh = mk()
+    mesh = dict(mesh, pos=mesh["pos"] - mesh["pos"].mean(0))
+    for lv, rec in enumerate(oracle.refine(mesh, scheme, 3)):
+        check_outward(rec, f"{scheme} {mesh['name']} L{lv}")
+
+
+def test_orientation_pin_detects_a_flip():
+    """The pin itself: reversing one child face's vertex order (SPEC's clockwise sqrt3 order,
+    S:L496) is caught."""
+    rec = oracle.refine(_octahedron(), "sqrt3", 1)[1]
+    fv = rec["face_vtx"].copy()
+    fv[0:3] = fv[0:3][::-1]
+    with pytest.raises(AssertionError):
+        check_outward(dict(rec, face_vtx=fv), "flipped")
