@@ -166,13 +166,23 @@ alsub_status alsub_reevaluate(alsub_mesh *mesh, int32_t from_level, void *stream
 alsub_status alsub_build_refinement_matrix(alsub_mesh *mesh, int32_t levels, void *stream);
 /* levels, rows (= V_levels) and non-zeros of the built matrix; any pointer may be NULL. */
 alsub_status alsub_refinement_matrix_info(const alsub_mesh *mesh, int32_t *levels, int64_t *rows, int64_t *nnz);
+/* The blocked form alsub_eval_frames_matrix evaluates: `chunks` = F0 + the isolated control
+ * vertices (one per owner face, then one identity row per isolated vertex); `weights` = floats of
+ * the dense per-chunk blocks W_c [|S_c|][rows_c rounded up to 64] (zeros included).  Either
+ * pointer may be NULL.  Errors: E_ARG (no matrix built). */
+alsub_status alsub_refinement_matrix_blocks(const alsub_mesh *mesh, int64_t *chunks, int64_t *weights);
 /* CSR export: row_off [rows+1], cols [nnz] (control vertex ids, ascending per row), vals [nnz];
  * host or device pointers, any may be NULL; synchronises `stream`. */
 alsub_status alsub_refinement_matrix_csr(const alsub_mesh *mesh, int32_t *row_off, int32_t *cols, float *vals,
                                          void *stream);
 /* Static evaluation by the single SpMM P_L = R P_0: frames_in [num_frames][V0][3],
- * frames_out [num_frames][V_levels][3], DEVICE pointers; batches of 32 frames.
- * Errors: E_ARG (no matrix built, host pointers). */
+ * frames_out [num_frames][V_levels][3], DEVICE pointers; batches of 32 frames.  R is applied in
+ * its blocked form: the rows owned by one control face share that face's 1-ring support S_c, so
+ * each chunk is a dense |S_c| x rows_c product (weights in registers, the batch's positions of S_c
+ * staged in shared memory).  Asynchronous (stream-ordered).
+ * Errors: E_ARG (no matrix built -- also after a refine with another scheme or level count --,
+ * host pointers).  alsub_build_refinement_matrix additionally returns E_OVERFLOW when R has more
+ * than 2^31 - 1 non-zeros (its CSR export uses int32 offsets). */
 alsub_status alsub_eval_frames_matrix(alsub_mesh *mesh, const float *frames_in, int32_t num_frames, float *frames_out,
                                       void *stream);
 

@@ -75,6 +75,7 @@ def lib():
     L.alsub_refinement_matrix_info.argtypes = [vp, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64)]
     L.alsub_refinement_matrix_csr.argtypes = [vp, vp, vp, vp, vp]
     L.alsub_eval_frames_matrix.argtypes = [vp, vp, i32, vp, vp]
+    L.alsub_refinement_matrix_blocks.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
     L.alsub_extract_maps.argtypes = [vp, vp, vp, vp]
     L.alsub_frame_summary.argtypes = [vp, i32, i64, vp, vp]
     L.alsub_probe.argtypes = [vp, i32, C.c_char_p, i32]
@@ -89,7 +90,7 @@ def lib():
               "alsub_level_topology", "alsub_level_positions", "alsub_eval_frames", "alsub_eval_attributes",
               "alsub_level_positions_ptr", "alsub_reevaluate", "alsub_rcm_order", "alsub_mesh_extract",
               "alsub_extract_maps", "alsub_build_refinement_matrix", "alsub_refinement_matrix_info",
-              "alsub_refinement_matrix_csr", "alsub_eval_frames_matrix", "alsub_frame_summary", "alsub_probe",
+              "alsub_refinement_matrix_csr", "alsub_eval_frames_matrix", "alsub_refinement_matrix_blocks", "alsub_frame_summary", "alsub_probe",
               "alsub_probe_read"):
         getattr(L, f).restype = C.c_int
     _lib = L
@@ -198,6 +199,12 @@ class Mesh:
         lv, rows, nnz = C.c_int32(), C.c_int64(), C.c_int64()
         _check(self._lib.alsub_refinement_matrix_info(self._h, C.byref(lv), C.byref(rows), C.byref(nnz)))
         return {"levels": lv.value, "rows": rows.value, "nnz": nnz.value}
+
+    def refinement_matrix_blocks(self):
+        """{chunks, weights}: size of the blocked form alsub_eval_frames_matrix evaluates."""
+        c, w = C.c_int64(), C.c_int64()
+        _check(self._lib.alsub_refinement_matrix_blocks(self._h, C.byref(c), C.byref(w)))
+        return {"chunks": c.value, "weights": w.value}
 
     def refinement_matrix_csr(self):
         """(row_off, cols, vals) numpy arrays of R."""

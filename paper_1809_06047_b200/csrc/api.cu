@@ -130,7 +130,14 @@ struct alsub_mesh {
     int64_t rm_nnz = 0;
     int32_t *rm_row_off = nullptr;
     int2 *rm_ent = nullptr;
-    float *rm_p0i = nullptr;
+    // blocked form used by alsub_eval_frames_matrix (rmatrix.cu): chunk = owner face (c < F0) or
+    // isolated control vertex (F0 + v); rows, support and dense weights per chunk
+    int32_t rb_C = 0;
+    int32_t *rb_row_off = nullptr, *rb_rows = nullptr, *rb_sup_off = nullptr, *rb_sup = nullptr;
+    int64_t *rb_w_off = nullptr;
+    float *rb_W = nullptr;
+    int64_t rb_wlen = 0;
+    float *rb_xt = nullptr;  // one batch of control positions [V0][3][32]
     // frames
     int frames_nb = 0;
     std::vector<float *> frame_buf;
@@ -383,6 +390,9 @@ static void drop_graph(alsub_mesh *m) {
 
 static void free_plan(alsub_mesh *m, cudaStream_t s) {
     drop_graph(m);
+    // the refinement matrix indexes the plan's levels: it dies with the plan
+    free_list(m, m->mem_rm, s);
+    m->rm_levels = -1;
     free_list(m, m->mem_plan, s);
     free_list(m, m->mem_frames, s);
     m->scratch = m->scratch_create;
@@ -1172,21 +1182,42 @@ extern "C" alsub_status alsub_build_refinement_matrix(alsub_mesh *m, int32_t lev
         ncol = std::max(ncol, c + 1);
     }
     const int32_t nprobe = (ncol + 2) / 3;
+    // chunks of the blocked form: the F0 owner faces, then one per isolated control vertex (its row
+    // is the identity: support {v})
+    std::vector<int32_t> iso_chunk((size_t)V0, -1);
+    int32_t C = F0;
+    for (int32_t v = 0; v < V0; ++v)
+        if (vf_off[v + 1] == vf_off[v]) {
+            iso_chunk[v] = C++;
+            sup.push_back(v);
+            sup_off.push_back((int32_t)sup.size());
+        }
     // device: probes through the static path, owners, two-pass CSR assembly
     std::vector<std::pair<void *, size_t>> tmp;
     bool ok = true;
-    int32_t *d_sup_off = A<int32_t>(m, F0 + 1, s, tmp, ok), *d_sup = A<int32_t>(m, (int64_t)sup.size(), s, tmp, ok);
+    m->rb_sup_off = A<int32_t>(m, (int64_t)C + 1, s, m->mem_rm, ok);
+    m->rb_sup = A<int32_t>(m, (int64_t)sup.size(), s, m->mem_rm, ok);
+    int32_t *d_sup_off = m->rb_sup_off, *d_sup = m->rb_sup;
     int32_t *d_col = A<int32_t>(m, V0, s, tmp, ok), *d_owner = A<int32_t>(m, VL, s, tmp, ok);
     int32_t *d_len = A<int32_t>(m, VL + 1, s, tmp, ok), *d_tot = A<int32_t>(m, 1, s, tmp, ok);
+    int64_t *d_nnz = A<int64_t>(m, 1, s, tmp, ok);
+    int32_t *d_chunk = A<int32_t>(m, VL, s, tmp, ok), *d_cnt = A<int32_t>(m, (int64_t)C + 1, s, tmp, ok);
+    int32_t *d_cur = A<int32_t>(m, C, s, tmp, ok), *d_pos = A<int32_t>(m, VL, s, tmp, ok);
+    int64_t *d_wlen = A<int64_t>(m, C, s, tmp, ok);
+    int32_t *d_iso = A<int32_t>(m, V0, s, tmp, ok);
     float *d_pin = A<float>(m, 3 * (int64_t)V0 * std::max(nprobe, 1), s, tmp, ok);
     float *d_pout = A<float>(m, 3 * VL * std::max(nprobe, 1), s, tmp, ok);
-    void *scr = dev_alloc(m, scan_scratch_bytes(VL + 1), s, tmp);
+    void *scr = dev_alloc(m, scan_scratch_bytes(std::max<int64_t>(VL, C) + 1), s, tmp);
     m->rm_row_off = A<int32_t>(m, VL + 1, s, m->mem_rm, ok);
-    m->rm_p0i = A<float>(m, 3 * (int64_t)V0 * kRmLanes, s, m->mem_rm, ok);
+    m->rb_xt = A<float>(m, 3 * (int64_t)V0 * kRmLanes + 4, s, m->mem_rm, ok);  // + the chunk counter
+    m->rb_row_off = A<int32_t>(m, (int64_t)C + 1, s, m->mem_rm, ok);
+    m->rb_rows = A<int32_t>(m, VL, s, m->mem_rm, ok);
+    m->rb_w_off = A<int64_t>(m, (int64_t)C + 1, s, m->mem_rm, ok);
     if (!ok || !scr) { free_list(m, tmp, s); free_list(m, m->mem_rm, s); return fail(ALSUB_E_NOMEM, "refinement matrix buffers"); }
     CU(cudaMemcpyAsync(d_sup_off, sup_off.data(), sizeof(int32_t) * sup_off.size(), cudaMemcpyHostToDevice, s));
     if (!sup.empty()) CU(cudaMemcpyAsync(d_sup, sup.data(), sizeof(int32_t) * sup.size(), cudaMemcpyHostToDevice, s));
     if (V0 > 0) CU(cudaMemcpyAsync(d_col, colour.data(), sizeof(int32_t) * V0, cudaMemcpyHostToDevice, s));
+    if (V0 > 0) CU(cudaMemcpyAsync(d_iso, iso_chunk.data(), sizeof(int32_t) * V0, cudaMemcpyHostToDevice, s));
     Launches L;
     rm_probes(V0, d_col, nprobe, d_pin, s, L);
     alsub_status st = nprobe > 0 ? alsub_eval_frames(m, levels, d_pin, nprobe, d_pout, stream) : ALSUB_OK;
@@ -1195,23 +1226,43 @@ extern "C" alsub_status alsub_build_refinement_matrix(alsub_mesh *m, int32_t lev
         ZeroSegs z;
         z.add(d_owner, VL, INT32_MAX);
         z.add(d_len + VL, 1, 0);
+        z.add(d_nnz, 2, 0);
+        z.add(d_cnt, (int64_t)C + 1, 0);
+        z.add(d_cur, C, 0);
         zero_segments(z, s, L);
     }
     const int shift = m->scheme == ALSUB_CATMULL_CLARK ? 2 * (levels - 1) : 2 * levels;
     rm_owner(m->lv[levels].face_vtx, (int32_t)FL, m->lv[levels].order, shift,
              m->scheme == ALSUB_CATMULL_CLARK ? m->b0.slot_face : nullptr, d_owner, s, L);
-    rm_assemble((int32_t)VL, d_owner, d_sup_off, d_sup, d_col, d_pout, 3 * VL, false, d_len, nullptr, nullptr, s, L);
+    rm_assemble((int32_t)VL, d_owner, d_sup_off, d_sup, d_col, d_pout, 3 * VL, false, d_len, nullptr, nullptr, d_nnz, s, L);
     scan_exclusive(d_len, m->rm_row_off, VL + 1, d_tot, scr, s, L);
-    int32_t nnz = 0;
-    CU(cudaMemcpyAsync(&nnz, d_tot, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    // blocked form: rows grouped by chunk (counting sort + per-chunk sort), W lengths scanned in 64 bits
+    rb_hist((int32_t)VL, d_owner, d_iso, d_chunk, d_cnt, s, L);
+    scan_exclusive(d_cnt, m->rb_row_off, (int64_t)C + 1, nullptr, scr, s, L);
+    rb_scatter((int32_t)VL, d_chunk, m->rb_row_off, d_cur, m->rb_rows, s, L);
+    rb_sort(C, m->rb_row_off, d_sup_off, m->rb_rows, d_pos, d_wlen, m->rb_w_off, s, L);
+    int64_t nnz = 0, wlen = 0;
+    CU(cudaMemcpyAsync(&nnz, d_nnz, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&wlen, m->rb_w_off + C, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    if (nnz > INT32_MAX) {  // the CSR export's int32 row offsets would wrap
+        free_list(m, tmp, s);
+        free_list(m, m->mem_rm, s);
+        return fail(ALSUB_E_OVERFLOW, "refinement matrix has more than 2^31 - 1 non-zeros");
+    }
     m->rm_ent = A<int2>(m, std::max<int64_t>(nnz, 1), s, m->mem_rm, ok);
+    m->rb_W = A<float>(m, std::max<int64_t>(wlen, 1), s, m->mem_rm, ok);
     if (!ok) { free_list(m, tmp, s); free_list(m, m->mem_rm, s); return fail(ALSUB_E_NOMEM, "refinement matrix entries"); }
-    rm_assemble((int32_t)VL, d_owner, d_sup_off, d_sup, d_col, d_pout, 3 * VL, true, nullptr, m->rm_row_off, m->rm_ent, s, L);
+    rm_assemble((int32_t)VL, d_owner, d_sup_off, d_sup, d_col, d_pout, 3 * VL, true, nullptr, m->rm_row_off, m->rm_ent, nullptr,
+                s, L);
+    if (wlen > 0) CU(cudaMemsetAsync(m->rb_W, 0, sizeof(float) * (size_t)wlen, s));
+    rb_fill((int32_t)VL, d_chunk, d_pos, m->rb_row_off, d_sup_off, d_sup, m->rb_w_off, d_col, d_pout, 3 * VL, m->rb_W, s, L);
     free_list(m, tmp, s);
     m->rm_levels = levels;
     m->rm_scheme = m->scheme;
     m->rm_nnz = nnz;
+    m->rb_C = C;
+    m->rb_wlen = wlen;
     m->last_launches = L.n;
     CU(cudaGetLastError());
     return ALSUB_OK;
@@ -1223,6 +1274,14 @@ extern "C" alsub_status alsub_refinement_matrix_info(const alsub_mesh *m, int32_
     if (levels) *levels = m->rm_levels;
     if (rows) *rows = m->lv[m->rm_levels].V;
     if (nnz) *nnz = m->rm_nnz;
+    return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_refinement_matrix_blocks(const alsub_mesh *m, int64_t *chunks, int64_t *weights) {
+    if (!m) return fail(ALSUB_E_ARG, "null mesh");
+    if (m->rm_levels < 0) return fail(ALSUB_E_ARG, "no refinement matrix: call alsub_build_refinement_matrix");
+    if (chunks) *chunks = m->rb_C;
+    if (weights) *weights = m->rb_wlen;
     return ALSUB_OK;
 }
 
@@ -1261,8 +1320,8 @@ extern "C" alsub_status alsub_eval_frames_matrix(alsub_mesh *m, const float *fra
     Launches L;
     for (int32_t f0 = 0; f0 < num_frames; f0 += kRmLanes) {
         const int32_t n = std::min(kRmLanes, num_frames - f0);
-        rm_interleave(frames_in + 3 * V0 * (int64_t)f0, (int32_t)V0, n, m->rm_p0i, s, L);
-        rm_spmm((int32_t)VL, m->rm_row_off, m->rm_ent, m->rm_p0i, n, frames_out + 3 * VL * (int64_t)f0, s, L);
+        rb_eval(m->rb_C, m->rb_row_off, m->rb_sup_off, m->rb_w_off, m->rb_rows, m->rb_sup, m->rb_W,
+                frames_in + 3 * V0 * (int64_t)f0, (int32_t)V0, n, m->rb_xt, VL, frames_out + 3 * VL * (int64_t)f0, s, L);
     }
     m->last_launches = L.n;
     CU(cudaGetLastError());

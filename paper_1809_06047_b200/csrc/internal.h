@@ -170,10 +170,20 @@ void rm_owner(const int32_t *face_vtx, int32_t FL, int order, int shift, const i
 void rm_probes(int32_t V0, const int32_t *colour, int32_t nprobe, float *out, cudaStream_t s, Launches &L);
 void rm_assemble(int32_t VL, const int32_t *owner, const int32_t *sup_off, const int32_t *sup, const int32_t *colour,
                  const float *probe, int64_t probe_stride, bool fill, int32_t *row_len, const int32_t *row_off,
-                 int2 *ent, cudaStream_t s, Launches &L);
-void rm_interleave(const float *in, int32_t V0, int32_t nb, float *out, cudaStream_t s, Launches &L);
-void rm_spmm(int32_t VL, const int32_t *row_off, const int2 *ent, const float *P0i, int32_t nb, float *out,
-             cudaStream_t s, Launches &L);
+                 int2 *ent, int64_t *nnz64, cudaStream_t s, Launches &L);
+// blocked R (chunk = owner face / isolated control vertex; rmatrix.cu)
+void rb_hist(int32_t VL, const int32_t *owner, const int32_t *iso_chunk, int32_t *chunk, int32_t *cnt, cudaStream_t s,
+             Launches &L);
+void rb_scatter(int32_t VL, const int32_t *chunk, const int32_t *row_off, int32_t *cur, int32_t *rows, cudaStream_t s,
+                Launches &L);
+void rb_sort(int32_t C, const int32_t *row_off, const int32_t *sup_off, int32_t *rows, int32_t *pos, int64_t *wlen,
+             int64_t *w_off, cudaStream_t s, Launches &L);
+void rb_fill(int32_t VL, const int32_t *chunk, const int32_t *pos, const int32_t *row_off, const int32_t *sup_off,
+             const int32_t *sup, const int64_t *w_off, const int32_t *colour, const float *probe, int64_t probe_stride,
+             float *W, cudaStream_t s, Launches &L);
+void rb_eval(int32_t C, const int32_t *row_off, const int32_t *sup_off, const int64_t *w_off, const int32_t *rows,
+             const int32_t *sup, const float *W, const float *in, int32_t V0, int32_t nb, float *XT, int64_t VL,
+             float *out, cudaStream_t s, Launches &L);
 
 // ---- selective subdivision: extraction (extract.cu) ----
 struct ExSrcHost {

@@ -15,9 +15,12 @@
 //              that colour in the support, so the probe reads exactly one weight
 // Rows are stored in CSR (exact zeros dropped) in output-vertex order.
 //
-// Evaluation: P_L = R P_0 for batches of 32 frames.  A warp owns 8 consecutive rows;
-// lane = frame, the control positions are frame-interleaved ([V0][32][3]: one 384-B row per
-// non-zero), results are staged in shared memory and written frame by frame as full sectors.
+// Evaluation: P_L = R P_0 for batches of 32 frames, in a blocked form of R (below): the
+// rows of one owner face share its support, so R restricted to them is a small dense block
+// W_c [|S_c|][rows_c] -- a warp stages the batch's control positions of S_c in shared memory once
+// and every row is a dense |S_c|-term dot product per frame with its weights in registers.
+#include <algorithm>
+
 #include "internal.h"
 
 namespace alsub {
@@ -41,25 +44,33 @@ __global__ void k_rm_assemble(int32_t VL, const int32_t *__restrict__ owner, con
                               const int32_t *__restrict__ sup, const int32_t *__restrict__ colour,
                               const float *__restrict__ probe, int64_t probe_stride, bool fill,
                               int32_t *__restrict__ row_len, const int32_t *__restrict__ row_off,
-                              int2 *__restrict__ ent) {
+                              int2 *__restrict__ ent, int64_t *nnz64) {
     ALSUB_GRID_WAIT();
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= VL) return;
-    const int32_t f = owner[i];
-    if (f == INT32_MAX) {
-        if (fill) ent[row_off[i]] = make_int2(i, __float_as_int(1.0f));
-        else row_len[i] = 1;
-        return;
+    int32_t n = 0;
+    if (i < VL) {
+        const int32_t f = owner[i];
+        if (f == INT32_MAX) {
+            if (fill) ent[row_off[i]] = make_int2(i, __float_as_int(1.0f));
+            n = 1;
+        } else {
+            const int32_t o = fill ? row_off[i] : 0;
+            for (int32_t k = __ldg(sup_off + f); k < __ldg(sup_off + f + 1); ++k) {
+                const int32_t j = __ldg(sup + k), c = __ldg(colour + j);
+                const float w = __ldg(probe + (c / 3) * probe_stride + 3 * (int64_t)i + (c % 3));
+                if (w == 0.0f) continue;
+                if (fill) ent[o + n] = make_int2(j, __float_as_int(w));
+                ++n;
+            }
+        }
+        if (!fill) row_len[i] = n;
     }
-    int32_t n = 0, o = fill ? row_off[i] : 0;
-    for (int32_t k = __ldg(sup_off + f); k < __ldg(sup_off + f + 1); ++k) {
-        const int32_t j = __ldg(sup + k), c = __ldg(colour + j);
-        const float w = __ldg(probe + (c / 3) * probe_stride + 3 * (int64_t)i + (c % 3));
-        if (w == 0.0f) continue;
-        if (fill) ent[o + n] = make_int2(j, __float_as_int(w));
-        ++n;
+    if (!fill) {  // the total in 64 bits (the int32 row offsets are only valid if it fits)
+        unsigned long long t = (unsigned long long)n;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if ((threadIdx.x & 31) == 0 && t) atomicAdd(reinterpret_cast<unsigned long long *>(nnz64), t);
     }
-    if (!fill) row_len[i] = n;
 }
 
 // probe frames: channel c of frame p = indicator of colour 3p + c
@@ -72,79 +83,284 @@ __global__ void k_rm_probes(int32_t V0, const int32_t *__restrict__ colour, int3
     out[t] = colour[v] == 3 * p + c ? 1.0f : 0.0f;
 }
 
-// [nb][V0][3] frame-major -> [V0][32][3] frame-interleaved (lanes >= nb repeat frame nb - 1)
-__global__ void k_rm_interleave(const float *__restrict__ in, int32_t V0, int32_t nb, float *__restrict__ out) {
+// ------------------------------------------------------------------------------------------
+// Blocked R.  Chunk c = owner face c (c < F0), or an isolated control vertex (identity row).
+//   row_off [C+1]   rows of chunk c = rows[row_off[c] .. row_off[c+1]), ascending row ids
+//   sup_off [C+1]   support S_c = sup[sup_off[c] ..), ascending control vertex ids
+//   w_off   [C+1]   W_c at W + w_off[c]: [|S_c|][R64_c] floats, R64_c = rows_c rounded up to 64,
+//                   W_c[k][r] = R[rows[row_off[c] + r], S_c[k]] (zero padded)
+// ------------------------------------------------------------------------------------------
+// chunk of row i: its owner face, or (unowned rows = isolated control vertices, i < V0) the chunk
+// iso_chunk[i] the host gave that vertex
+__global__ void k_rb_hist(int32_t VL, const int32_t *__restrict__ owner, const int32_t *__restrict__ iso_chunk,
+                          int32_t *__restrict__ chunk, int32_t *__restrict__ cnt) {
     ALSUB_GRID_WAIT();
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (int64_t)V0 * kRmLanes * 3) return;
-    const int64_t v = t / (kRmLanes * 3);
-    const int r = (int)(t - v * kRmLanes * 3), f = r / 3, c = r - 3 * f;
-    const int ff = f < nb ? f : nb - 1;
-    out[t] = in[((int64_t)ff * V0 + v) * 3 + c];
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= VL) return;
+    const int32_t o = owner[i];
+    const int32_t c = o == INT32_MAX ? iso_chunk[i] : o;
+    chunk[i] = c;
+    atomicAdd(cnt + c, 1);
 }
 
-// P_L = R P_0: a row of P_0 for the batch is 96 contiguous floats (32 frames x 3), so each
-// non-zero is a 96-float axpy: lanes 0..23 own one float4 of it (one 16-B load per lane, the
-// whole 384-B row in 3 cache lines), lanes 24..31 idle.  A warp owns 8 consecutive rows; results
-// are staged in shared memory and written frame by frame (8 rows x 12 B = 3 full sectors).
-constexpr int kRmWarps = 8, kRmRows = 8;
-__global__ void __launch_bounds__(32 * kRmWarps) k_rm_spmm(int32_t VL, const int32_t *__restrict__ row_off,
-                                                         const int2 *__restrict__ ent,
-                                                         const float4 *__restrict__ P0i, int32_t nb,
+__global__ void k_rb_scatter(int32_t VL, const int32_t *__restrict__ chunk, const int32_t *__restrict__ row_off,
+                             int32_t *__restrict__ cur, int32_t *__restrict__ rows) {
+    ALSUB_GRID_WAIT();
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= VL) return;
+    const int32_t c = chunk[i];
+    rows[row_off[c] + atomicAdd(cur + c, 1)] = i;
+}
+
+// rows of every chunk sorted ascending (block per chunk, shared-memory bitonic up to kRbSortCap
+// rows; longer chunks -- very high-order control faces -- by one thread), then pos[row] = its index
+// in the chunk and the chunk's W length |S_c| x R64_c
+constexpr int kRbSortCap = 4096;
+__global__ void __launch_bounds__(256) k_rb_sort(int32_t C, const int32_t *__restrict__ row_off,
+                                               const int32_t *__restrict__ sup_off, int32_t *__restrict__ rows,
+                                               int32_t *__restrict__ pos, int64_t *__restrict__ wlen) {
+    ALSUB_GRID_WAIT();
+    __shared__ int32_t sk[kRbSortCap];
+    for (int32_t c = blockIdx.x; c < C; c += gridDim.x) {
+        const int32_t r0 = row_off[c], n = row_off[c + 1] - r0;
+        if (threadIdx.x == 0)
+            wlen[c] = (int64_t)(sup_off[c + 1] - sup_off[c]) * (int64_t)((n + 63) & ~63);
+        if (n <= 1) {
+            if (n == 1 && threadIdx.x == 0) pos[rows[r0]] = 0;
+            continue;
+        }
+        if (n <= kRbSortCap) {
+            int32_t P = 1;
+            while (P < n) P <<= 1;
+            for (int32_t i = threadIdx.x; i < P; i += blockDim.x) sk[i] = i < n ? rows[r0 + i] : INT32_MAX;
+            __syncthreads();
+            for (int32_t k = 2; k <= P; k <<= 1)
+                for (int32_t jj = k >> 1; jj > 0; jj >>= 1) {
+                    for (int32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                        const int32_t l = i ^ jj;
+                        if (l > i) {
+                            const int32_t x = sk[i], y = sk[l];
+                            if ((x > y) == ((i & k) == 0)) { sk[i] = y; sk[l] = x; }
+                        }
+                    }
+                    __syncthreads();
+                }
+            for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
+                rows[r0 + i] = sk[i];
+                pos[sk[i]] = i;
+            }
+            __syncthreads();
+        } else if (threadIdx.x == 0) {
+            int32_t *r = rows + r0;
+            for (int32_t a = 1; a < n; ++a) {
+                const int32_t x = r[a];
+                int32_t b = a - 1;
+                while (b >= 0 && r[b] > x) { r[b + 1] = r[b]; --b; }
+                r[b + 1] = x;
+            }
+            for (int32_t a = 0; a < n; ++a) pos[r[a]] = a;
+        }
+    }
+}
+
+// exclusive int64 scan of wlen [C] -> w_off [C+1] by one block (build time only)
+__global__ void __launch_bounds__(1024) k_rb_scan64(int32_t C, const int64_t *__restrict__ wlen, int64_t *__restrict__ w_off) {
+    ALSUB_GRID_WAIT();
+    __shared__ int64_t s_part[1024];
+    const int32_t per = (C + blockDim.x - 1) / blockDim.x;
+    const int32_t lo = min(C, (int32_t)threadIdx.x * per), hi = min(C, lo + per);
+    int64_t acc = 0;
+    for (int32_t c = lo; c < hi; ++c) acc += wlen[c];
+    s_part[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int k = 0; k < (int)blockDim.x; ++k) {
+            const int64_t v = s_part[k];
+            s_part[k] = t;
+            t += v;
+        }
+        w_off[C] = t;
+    }
+    __syncthreads();
+    acc = s_part[threadIdx.x];
+    for (int32_t c = lo; c < hi; ++c) {
+        w_off[c] = acc;
+        acc += wlen[c];
+    }
+}
+
+// W_c[k][pos(i)] = probe value of colour(S_c[k]) at row i (the only support vertex of its colour)
+__global__ void k_rb_fill(int32_t VL, const int32_t *__restrict__ chunk, const int32_t *__restrict__ pos,
+                          const int32_t *__restrict__ row_off, const int32_t *__restrict__ sup_off,
+                          const int32_t *__restrict__ sup, const int64_t *__restrict__ w_off,
+                          const int32_t *__restrict__ colour, const float *__restrict__ probe, int64_t probe_stride,
+                          float *__restrict__ W) {
+    ALSUB_GRID_WAIT();
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= VL) return;
+    const int32_t c = chunk[i], r = pos[i];
+    const int32_t n = row_off[c + 1] - row_off[c];
+    const int64_t R64 = (n + 63) & ~63;
+    float *Wc = W + w_off[c] + r;
+    for (int32_t k = sup_off[c]; k < sup_off[c + 1]; ++k) {
+        const int32_t cl = __ldg(colour + __ldg(sup + k));
+        Wc[(k - sup_off[c]) * R64] = __ldg(probe + (cl / 3) * probe_stride + 3 * (int64_t)i + (cl % 3));
+    }
+}
+
+// one batch of nb <= 32 frames [nb][V0][3] -> XT [V0][3][32] (frames innermost, zero padded)
+__global__ void k_rb_xt(const float *__restrict__ in, int32_t V0, int32_t nb, float *__restrict__ XT,
+                        int32_t *__restrict__ next_chunk) {
+    ALSUB_GRID_WAIT();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t == 0) *next_chunk = 0;
+    if (t >= (int64_t)V0 * 3 * kRmLanes) return;
+    const int f = (int)(t % kRmLanes);
+    const int64_t vc = t / kRmLanes;  // 3 v + c
+    XT[t] = f < nb ? __ldg(in + (int64_t)f * V0 * 3 + vc) : 0.0f;
+}
+
+// P_L = R P_0 over the chunks: one CTA per chunk (taken in order from a counter), warp w on its row
+// groups w, w + 4, ... (64 rows: lane = rows r and r + 32, their |S_c| weights in registers).  The
+// batch's control positions of S_c are staged once per chunk in shared memory ([k][coord][32
+// frames]) and read as warp-wide broadcasts, 4 frames per float4: per support vertex 3 broadcast
+// loads feed 24 FMAs.  With the whole chunk in flight at once and neighbouring chunks on
+// neighbouring CTAs, the output runs that share a boundary sector are written within a few
+// microseconds of each other and merge in L2 (one warp per chunk, processed over ~100 us, left
+// those sectors to be evicted half written: DRAM read-modify-write, +40 % traffic).  Chunks with
+// |S_c| > kRbTK run the same product over kRbTK-wide support tiles (positions restaged per tile
+// and frame group in the warp's quarter of the buffer, weights from L1).
+constexpr int kRbWarps = 4, kRbTK = 24;
+constexpr int kRbXf4 = 3 * kRmLanes / 4;  // float4 per support vertex in XT / shared memory (24)
+
+// results of one row group (64 rows) for 4 frames -> the chunk's output rows.  The lanes' values
+// (row r and r + 32, 4 frames x 3 coords) go through shared memory so that each store instruction
+// writes 32 consecutive floats of one frame (float t of the group = coord t % 3 of its row t / 3):
+// contiguous row runs become full 128-B lines instead of 12-B-strided partial sectors.
+ALSUB_D void rb_store(float *so, const int32_t (&rid)[6], float *out, int64_t VL, int f0, int nb, int lane,
+                      const float (&a)[4][3], const float (&b)[4][3]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            so[u * 192 + 3 * lane + c] = a[u][c];
+            so[u * 192 + 96 + 3 * lane + c] = b[u][c];
+        }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        if (f0 + u >= nb) break;
+        float *o = out + (int64_t)(f0 + u) * VL * 3;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            const int t = lane + 32 * i;
+            if (rid[i] >= 0) o[3 * (int64_t)rid[i] + (t % 3)] = so[u * 192 + t];
+        }
+    }
+    __syncwarp();
+}
+
+ALSUB_D void rb_fma(float (&a)[4][3], float w, const float4 (&x)[3]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        a[0][c] = fmaf(w, x[c].x, a[0][c]);
+        a[1][c] = fmaf(w, x[c].y, a[1][c]);
+        a[2][c] = fmaf(w, x[c].z, a[2][c]);
+        a[3][c] = fmaf(w, x[c].w, a[3][c]);
+    }
+}
+
+__global__ void __launch_bounds__(32 * kRbWarps) k_rb_eval(int32_t C, int32_t *__restrict__ next_chunk,
+                                                         const int32_t *__restrict__ row_off,
+                                                         const int32_t *__restrict__ sup_off,
+                                                         const int64_t *__restrict__ w_off,
+                                                         const int32_t *__restrict__ rows,
+                                                         const int32_t *__restrict__ sup, const float *__restrict__ W,
+                                                         const float4 *__restrict__ XT, int32_t nb, int64_t VL,
                                                          float *__restrict__ out) {
     ALSUB_GRID_WAIT();
-    // rows padded to 25 float4 so the per-frame read-back (row stride 100 floats) is conflict-free
-    __shared__ float4 s_out[kRmWarps][kRmRows][kRmLanes * 3 / 4 + 1];
+    extern __shared__ float4 s_dyn[];  // kRbTK x 24 float4 of positions (the CTA's), then per warp 4 x 192 floats
+    __shared__ int32_t s_c;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const bool act = lane < kRmLanes * 3 / 4;
-    const int q = act ? lane : 0;
-    // each block walks one contiguous range of tiles: consecutive output vertices are spatial
-    // neighbours within a class segment, so the block's control rows stay in L1
-    const int64_t ntile = ((int64_t)VL + kRmRows - 1) / kRmRows;
-    const int64_t per = (ntile + gridDim.x - 1) / gridDim.x;
-    const int64_t t_end = min(ntile, per * (blockIdx.x + 1));
-    for (int64_t tile = per * blockIdx.x + w; tile < t_end; tile += kRmWarps) {
-        const int32_t r0 = (int32_t)(tile * kRmRows);
-        const int32_t nr = min(kRmRows, VL - r0);
-        for (int r = 0; r < nr; ++r) {
-            const int32_t a = __ldg(row_off + r0 + r), b = __ldg(row_off + r0 + r + 1);
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            int32_t k = a;
-            for (; k + 4 <= b; k += 4) {
-                int2 e[4];
+    float4 *sx = s_dyn;
+    float *so = reinterpret_cast<float *>(s_dyn + kRbTK * kRbXf4) + w * 4 * 192;
+    for (;;) {
+        if (threadIdx.x == 0) s_c = atomicAdd(next_chunk, 1);
+        __syncthreads();
+        const int32_t c = s_c;
+        if (c >= C) break;
+        const int32_t r0 = __ldg(row_off + c), nr = __ldg(row_off + c + 1) - r0;
+        const int32_t s0 = __ldg(sup_off + c), S = __ldg(sup_off + c + 1) - s0;
+        const int32_t R64 = (nr + 63) & ~63;
+        const float *Wc = W + __ldg(w_off + c);
+        if (S <= kRbTK) {
+            for (int32_t q = threadIdx.x; q < S * kRbXf4; q += blockDim.x) {
+                const int32_t k = q / kRbXf4, u = q - k * kRbXf4;
+                sx[q] = __ldg(XT + (int64_t)__ldg(sup + s0 + k) * kRbXf4 + u);
+            }
+            __syncthreads();
+            for (int32_t g = 64 * w; g < nr; g += 64 * kRbWarps) {
+                const int32_t ra = g + lane, rb = ra + 32;
+                float wa[kRbTK], wb[kRbTK];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) e[u] = __ldg(ent + k + u);
-                float4 p[4];
+                for (int k = 0; k < kRbTK; ++k) {
+                    wa[k] = k < S ? __ldg(Wc + (int64_t)k * R64 + ra) : 0.0f;
+                    wb[k] = k < S ? __ldg(Wc + (int64_t)k * R64 + rb) : 0.0f;
+                }
+                int32_t rid[6];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) p[u] = __ldg(P0i + (int64_t)e[u].x * (kRmLanes * 3 / 4) + q);
+                for (int i = 0; i < 6; ++i) {
+                    const int32_t r = g + (lane + 32 * i) / 3;
+                    rid[i] = r < nr ? __ldg(rows + r0 + r) : -1;
+                }
+                for (int f0 = 0; f0 < nb; f0 += 4) {
+                    float a[4][3] = {}, b[4][3] = {};
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float wt = __int_as_float(e[u].y);
-                    acc.x = fmaf(wt, p[u].x, acc.x);
-                    acc.y = fmaf(wt, p[u].y, acc.y);
-                    acc.z = fmaf(wt, p[u].z, acc.z);
-                    acc.w = fmaf(wt, p[u].w, acc.w);
+                    for (int k = 0; k < kRbTK; ++k) {
+                        if (k >= S) break;
+                        float4 x[3];
+#pragma unroll
+                        for (int cc = 0; cc < 3; ++cc) x[cc] = sx[k * kRbXf4 + cc * (kRmLanes / 4) + (f0 >> 2)];
+                        rb_fma(a, wa[k], x);
+                        rb_fma(b, wb[k], x);
+                    }
+                    rb_store(so, rid, out, VL, f0, nb, lane, a, b);
                 }
             }
-            for (; k < b; ++k) {
-                const int2 e = __ldg(ent + k);
-                const float4 p = __ldg(P0i + (int64_t)e.x * (kRmLanes * 3 / 4) + q);
-                const float wt = __int_as_float(e.y);
-                acc.x = fmaf(wt, p.x, acc.x);
-                acc.y = fmaf(wt, p.y, acc.y);
-                acc.z = fmaf(wt, p.z, acc.z);
-                acc.w = fmaf(wt, p.w, acc.w);
+        } else {
+            // wide support: kRbTK-wide tiles, positions of one frame group per tile, in this warp's
+            // quarter of the position buffer
+            float4 *sw = sx + w * (kRbTK * kRbXf4 / kRbWarps);
+            for (int32_t g = 64 * w; g < nr; g += 64 * kRbWarps) {
+                const int32_t ra = g + lane, rb = ra + 32;
+                int32_t rid[6];
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const int32_t r = g + (lane + 32 * i) / 3;
+                    rid[i] = r < nr ? __ldg(rows + r0 + r) : -1;
+                }
+                for (int f0 = 0; f0 < nb; f0 += 4) {
+                    float a[4][3] = {}, b[4][3] = {};
+                    for (int32_t t0 = 0; t0 < S; t0 += kRbTK) {
+                        const int32_t St = min(kRbTK, S - t0);
+                        __syncwarp();
+                        for (int32_t q = lane; q < 3 * St; q += 32) {
+                            const int32_t k = q / 3, cc = q - 3 * k;
+                            sw[q] = __ldg(XT + (int64_t)__ldg(sup + s0 + t0 + k) * kRbXf4 + cc * (kRmLanes / 4) + (f0 >> 2));
+                        }
+                        __syncwarp();
+                        for (int32_t k = 0; k < St; ++k) {
+                            const float4 x[3] = {sw[3 * k], sw[3 * k + 1], sw[3 * k + 2]};
+                            rb_fma(a, __ldg(Wc + (int64_t)(t0 + k) * R64 + ra), x);
+                            rb_fma(b, __ldg(Wc + (int64_t)(t0 + k) * R64 + rb), x);
+                        }
+                    }
+                    rb_store(so, rid, out, VL, f0, nb, lane, a, b);
+                }
             }
-            if (act) s_out[w][r][lane] = acc;
         }
-        __syncwarp();
-        // frame f: rows r0 .. r0+nr-1 are 3 nr contiguous floats of out[f]
-        if (lane < 3 * nr) {
-            const int r = lane / 3, c = lane - 3 * r;
-            const float *src = reinterpret_cast<const float *>(s_out[w][r]);
-            for (int f = 0; f < nb; ++f) out[((int64_t)f * VL + r0) * 3 + lane] = src[3 * f + c];
-        }
-        __syncwarp();
+        __syncthreads();  // the positions and s_c are reused by the next chunk
     }
 }
 
@@ -158,23 +374,49 @@ void rm_probes(int32_t V0, const int32_t *colour, int32_t nprobe, float *out, cu
 }
 void rm_assemble(int32_t VL, const int32_t *owner, const int32_t *sup_off, const int32_t *sup, const int32_t *colour,
                  const float *probe, int64_t probe_stride, bool fill, int32_t *row_len, const int32_t *row_off,
-                 int2 *ent, cudaStream_t s, Launches &L) {
+                 int2 *ent, int64_t *nnz64, cudaStream_t s, Launches &L) {
     if (VL > 0) launch(L, "rm_assemble", k_rm_assemble, dim3(grid_for(VL)), dim3(kThreads), 0, s, VL, owner, sup_off, sup, colour,
-                       probe, probe_stride, fill, row_len, row_off, ent);
+                       probe, probe_stride, fill, row_len, row_off, ent, nnz64);
 }
-void rm_interleave(const float *in, int32_t V0, int32_t nb, float *out, cudaStream_t s, Launches &L) {
-    const int64_t n = (int64_t)V0 * kRmLanes * 3;
-    if (n > 0) launch(L, "rm_interleave", k_rm_interleave, dim3(grid_for(n)), dim3(kThreads), 0, s, in, V0, nb, out);
+void rb_hist(int32_t VL, const int32_t *owner, const int32_t *iso_chunk, int32_t *chunk, int32_t *cnt, cudaStream_t s,
+             Launches &L) {
+    if (VL > 0) launch(L, "rb_hist", k_rb_hist, dim3(grid_for(VL)), dim3(kThreads), 0, s, VL, owner, iso_chunk, chunk, cnt);
 }
-void rm_spmm(int32_t VL, const int32_t *row_off, const int2 *ent, const float *P0i, int32_t nb, float *out,
-             cudaStream_t s, Launches &L) {
-    if (VL <= 0) return;
-    const int64_t ntile = ((int64_t)VL + kRmRows - 1) / kRmRows;
-    // occupancy beats L1 capacity here: a smaller shared-memory carve-out (25-50 %) was measured
-    // 1.3-1.8x slower (profiles/r01_rmatrix.json)
-    const unsigned grid = (unsigned)std::min<int64_t>((ntile + kRmWarps - 1) / kRmWarps, 148 * 8);
-    launch(L, "rm_spmm", k_rm_spmm, dim3(grid), dim3(32 * kRmWarps), 0, s, VL, row_off, ent,
-           reinterpret_cast<const float4 *>(P0i), nb, out);
+void rb_scatter(int32_t VL, const int32_t *chunk, const int32_t *row_off, int32_t *cur, int32_t *rows, cudaStream_t s,
+                Launches &L) {
+    if (VL > 0) launch(L, "rb_scatter", k_rb_scatter, dim3(grid_for(VL)), dim3(kThreads), 0, s, VL, chunk, row_off, cur, rows);
+}
+void rb_sort(int32_t C, const int32_t *row_off, const int32_t *sup_off, int32_t *rows, int32_t *pos, int64_t *wlen,
+             int64_t *w_off, cudaStream_t s, Launches &L) {
+    if (C <= 0) return;
+    launch(L, "rb_sort", k_rb_sort, dim3((unsigned)std::min<int32_t>(C, 148 * 8)), dim3(256), 0, s, C, row_off, sup_off,
+           rows, pos, wlen);
+    launch(L, "rb_scan64", k_rb_scan64, dim3(1), dim3(1024), 0, s, C, (const int64_t *)wlen, w_off);
+}
+void rb_fill(int32_t VL, const int32_t *chunk, const int32_t *pos, const int32_t *row_off, const int32_t *sup_off,
+             const int32_t *sup, const int64_t *w_off, const int32_t *colour, const float *probe, int64_t probe_stride,
+             float *W, cudaStream_t s, Launches &L) {
+    if (VL > 0) launch(L, "rb_fill", k_rb_fill, dim3(grid_for(VL)), dim3(kThreads), 0, s, VL, chunk, pos, row_off, sup_off,
+                       sup, w_off, colour, probe, probe_stride, W);
+}
+void rb_eval(int32_t C, const int32_t *row_off, const int32_t *sup_off, const int64_t *w_off, const int32_t *rows,
+             const int32_t *sup, const float *W, const float *in, int32_t V0, int32_t nb, float *XT, int64_t VL,
+             float *out, cudaStream_t s, Launches &L) {
+    if (nb <= 0) return;
+    const int64_t n = (int64_t)V0 * 3 * kRmLanes;
+    int32_t *next_chunk = reinterpret_cast<int32_t *>(XT + n);  // one int after the batch
+    launch(L, "rb_xt", k_rb_xt, dim3(grid_for(n)), dim3(kThreads), 0, s, in, V0, nb, XT, next_chunk);
+    if (C <= 0) return;
+    const size_t smem = (size_t)kRbTK * kRbXf4 * 16 + (size_t)kRbWarps * 4 * 192 * 4;
+    static bool attr = [smem] {
+        return cudaFuncSetAttribute(k_rb_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+    }();
+    (void)attr;
+    int max_blocks = 4;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks, k_rb_eval, 32 * kRbWarps, smem);
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(C, kRbWarps), 148 * std::max(max_blocks, 1));
+    launch(L, "rb_eval", k_rb_eval, dim3(grid), dim3(32 * kRbWarps), smem, s, C, next_chunk, row_off, sup_off, w_off, rows, sup, W,
+           reinterpret_cast<const float4 *>(XT), nb, VL, out);
 }
 
 }  // namespace alsub

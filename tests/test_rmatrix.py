@@ -121,3 +121,79 @@ def test_gpu_R_errors():
         with pytest.raises(AlsubError):
             m.build_refinement_matrix(3)
         assert m.build_refinement_matrix(2)["rows"] == m.counts(2)["verts"]
+
+
+# ------------------------------------------------------------------------------------------
+# the blocked evaluation (alsub_eval_frames_matrix): chunks = owner faces with dense weight blocks
+# ------------------------------------------------------------------------------------------
+
+def _iso():
+    """Armor patch + two isolated control vertices (identity chunks)."""
+    m = mg.armor(3, 3, 4, 1, 1, 1, name="armor_rm_iso")
+    pos = np.vstack([m["pos"], [[3.0, 3.0, 3.0], [-2.0, 1.0, 0.5]]]).astype(np.float32)
+    return dict(m, pos=pos)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scheme,make,L,nf", [
+    ("cc", _small, 3, 37),                        # ragged batch: 32 + 5 frames
+    ("cc", _iso, 2, 3),                           # isolated control vertices: identity chunks
+    ("loop", lambda: mg.bipyramid(30), 2, 9),     # supports of 30+ vertices: the wide-tile path
+    ("cc", lambda: mg.bipyramid(20), 2, 4),
+])
+def test_gpu_blocked_spmm_equals_oracle_R(scheme, make, L, nf):
+    """P_L = R P_0 for random frames: the GPU's blocked SpMM against the oracle's R applied in fp64
+    (the oracle's R columns are refinements of unit vectors, independent of the GPU's probing)."""
+    from paper_1809_06047_b200 import Mesh
+    mesh = make()
+    R = oracle.refinement_matrix(mesh, scheme, L)
+    rng = np.random.default_rng(7)
+    fr = (mesh["pos"][None] + rng.normal(0, 0.05, (nf,) + mesh["pos"].shape)).astype(np.float32)
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine(scheme, L)
+        m.build_refinement_matrix(L)
+        got = m.eval_frames_matrix(torch.from_numpy(fr).cuda()).cpu().numpy().astype(np.float64)
+    diag = float(np.linalg.norm(mesh["pos"].max(0) - mesh["pos"].min(0)))
+    for f in range(nf):
+        want = R @ fr[f].astype(np.float64)
+        assert np.abs(got[f] - want).max() / diag <= TOL, f
+
+
+@pytest.mark.gpu
+def test_gpu_R_invalidated_by_a_new_plan():
+    """the matrix indexes the plan's levels -- a refine with another plan drops it."""
+    from paper_1809_06047_b200 import AlsubError, Mesh
+    mesh = mg.tetrahedron(creased=True)
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine("cc", 3)
+        m.build_refinement_matrix(3)
+        m.refine("cc", 3)  # same plan (graph replay): kept
+        assert m.refinement_matrix_info()["levels"] == 3
+        m.refine("cc", 2)
+        with pytest.raises(AlsubError):
+            m.refinement_matrix_info()
+        with pytest.raises(AlsubError):
+            m.eval_frames_matrix(torch.zeros((1, 4, 3), device="cuda"))
+        m.build_refinement_matrix(2)
+        m.refine("loop", 2)
+        with pytest.raises(AlsubError):
+            m.refinement_matrix_info()
+
+
+@pytest.mark.gpu
+def test_gpu_blocked_spmm_config5_full_size():
+    """Config 5 at its stated size through the matrix path bench.py times: armor50k CC L4, frames
+    0, 2047 and 4095 of 4096 (batches of 32) against the oracle refining those frames."""
+    from paper_1809_06047_b200 import Mesh
+    mesh = mg.armor50k()
+    diag = float(np.linalg.norm(mesh["pos"].max(0) - mesh["pos"].min(0)))
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine("cc", 4)
+        m.build_refinement_matrix(4)
+        for t in (0, 2047, 4095):
+            first = (t // 32) * 32
+            fr = torch.stack([torch.from_numpy(mg.frame_positions(mesh["pos"], first + u, 4096)) for u in range(32)]).cuda()
+            out = m.eval_frames_matrix(fr)
+            want = oracle.refine(dict(mesh, pos=mg.frame_positions(mesh["pos"], t, 4096)), "cc", 4)[-1]["pos"]
+            err = float(np.abs(out[t - first].cpu().numpy().astype(np.float64) - want).max()) / diag
+            assert err <= TOL, f"frame {t}: {err:.3e}"

@@ -45,9 +45,14 @@ t_lvl = timed(lambda: m.eval_frames(frames, L, out=out))
 ref = m.eval_frames(frames[:8], L)
 got = m.eval_frames_matrix(frames[:8])
 err = float((ref - got).abs().max())
+blk = m.refinement_matrix_blocks()
+# bytes per batch of 32 frames: the weights, row ids and support lists once, the output once
+bytes_batch = 4 * blk["weights"] + 4 * VL + 12 * VL * 32
 row = {"levels": L, "frames": nf, "rows": VL, "nnz": info["nnz"], "nnz_per_row": info["nnz"] / VL,
-       "R_bytes": 8 * info["nnz"] + 4 * (VL + 1), "build_s": t_build,
+       "R_bytes": 8 * info["nnz"] + 4 * (VL + 1), "build_s": t_build, "chunks": blk["chunks"],
+       "block_weights": blk["weights"], "block_fill": info["nnz"] / blk["weights"],
        "matrix_us_per_frame": 1e3 * t_mat / nf, "levels_us_per_frame": 1e3 * t_lvl / nf,
-       "matrix_GBps": (8 * info["nnz"] * (nf / 32) + 12 * VL * nf) / (t_mat * 1e6), "max_abs_diff": err}
+       "matrix_GBps": bytes_batch * (nf / 32) / (t_mat * 1e6), "output_GBps": 12 * VL * nf / (t_mat * 1e6),
+       "fma_per_frame": 3 * blk["weights"] / 1.0, "max_abs_diff": err}
 print(json.dumps(row))
 json.dump(row, open("gpurun_out/rm_bench.json", "w"), indent=1)
