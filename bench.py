@@ -1,23 +1,30 @@
 #!/usr/bin/env python
 """Benchmark: refined faces/s of AlSub uniform refinement on B200 (BASELINE.json metric).
 
-Default workload (N=1): SURVEY.md 8(d) config 3 -- Catmull-Clark level 6 of the ArmorGuy-shaped
-creased mesh armor9k (8,590 faces -> 34,897,920 faces).  A step is one alsub_refine(CC, 6): the
-whole hot path (level-0 mesh matrix, radix-sort M^T, edge index, creases, then 6 levels of
-topology + geometry), replayed as a CUDA graph with inputs resident in HBM.  L2 is flushed (a
-256 MiB write) between timed steps.  With N > 1 ranks (torchrun) each rank refines its own
-independent mesh (seed 1809 + rank): weak scaling, no collective on the data path.
+Default workload: SURVEY.md 8(d) config 3 -- Catmull-Clark level 6 of the ArmorGuy-shaped creased
+mesh armor9k (8,590 faces -> 34,897,920 faces).  A step is one alsub_refine(CC, 6): the whole hot
+path (level-0 mesh matrix, counting-sort M^T, edge index, creases, then 6 levels of topology +
+geometry), replayed as a CUDA graph with inputs resident in HBM.  L2 is flushed (a 256 MiB write)
+between timed steps.  With N > 1 ranks each rank refines its own independent mesh (seed 1809 +
+rank): weak scaling, no collective on the data path.
 
---config 5: static-mode frames (armor50k CC level 4, 4096 frames split over the ranks, batches
-of 8 frames per step through alsub_eval_frames).
+Every line also carries "frames": config 5 -- 4096 animation frames of armor50k (CC level 4,
+fixed topology) split over the N ranks (strong scaling), static mode through the blocked
+refinement matrix (alsub_eval_frames_matrix, batches of 32), each output frame reduced to a 32-B
+record (alsub_frame_summary) and the records all-gathered over NCCL.  --config 5 prints that
+measurement as the line itself.
 
---impl reference: the CPU oracle (oracle/, plain single-threaded C) timed on this host on a
-bounded sample of the same workload -- rank 0 only.
+--gpus N without torchrun (WORLD_SIZE unset) re-launches itself under torch.distributed.run with N
+ranks.  --dry-run exercises that launch and the record gather on CPU (gloo), no GPU work.
+
+--impl reference: the CPU oracle (oracle/, plain C) timed on this host on a bounded sample of the
+same workload -- rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import sys
@@ -56,11 +63,16 @@ def level_counts(m, levels):
 
 
 def kernel_bytes_cc(name, c, prev, lvl, levels, prev2=None):
-    """Algorithmic bytes of one launch of a CC level kernel: every array the
-    kernel reads or writes, counted once.  c = counts of the parent level lvl, prev = level lvl-1.
-    Mirrors the plan in api.cu: the last refined level (lvl = levels-1 >= 2) recomputes its edge
-    rows from the grandparent and iterates the grandparent's edges, so level levels-1 never stores
-    face_edge / face_twin / edge pairs; twins are only stored where the next level emits adjacency."""
+    """Algorithmic bytes of one launch of a CC level kernel: every array the kernel
+    reads or writes, counted once, split into
+      "method"       -- the method's own data: parent topology and positions in, child topology and
+                        refined positions out (what any implementation of the level must move)
+      "intermediate" -- this implementation's scratch: the face kernel's corner sums c0 and half ring
+                        sums hs (written by the face kernel, read back by the vertex kernel).
+    c = counts of the parent level lvl, prev = level lvl-1.  Mirrors the plan in api.cu: the last
+    refined level (lvl = levels-1 >= 2) recomputes its edge rows from the grandparent and iterates
+    the grandparent's edges, so level levels-1 never stores face_edge / face_twin / edge pairs;
+    twins are only stored where the next level emits adjacency."""
     V, F, S, E = c["V"], c["F"], c["S"], c["E"]
     Fp = prev["F"] if prev else 0
     Ep = prev["E"] if prev else 0
@@ -71,13 +83,14 @@ def kernel_bytes_cc(name, c, prev, lvl, levels, prev2=None):
     child_rows = adj and not (levels >= 3 and lvl + 1 == levels - 1)  # child face_edge / edge pairs stored
     child_twin = lvl + 2 < levels
     fpv = lvl >= 2
+    inter = 0
     if name == "cc_face":
         rd = 4 * S + 12 * V + (48 * Fp if gp_last else 4 * S) + (4 * S if adj else 0)
         wr = 12 * F + 16 * S + (16 * S if child_rows else 0) + (16 * S if child_twin else 0)
-        wr += 12 * Fp if fpv else 0               # new face-point vertices
-        wr += 12 * Fq                             # face points born at lvl-1
-        wr += 12 * F if (fpv and not gp_last) else 0  # half ring sums (the last level has none)
-        wr += 12 * F if lvl >= 1 else 0             # corner-0 contributions c0
+        wr += 12 * Fp if fpv else 0               # vertex points of the face points born at lvl
+        wr += 12 * Fq                             # vertex points of the face points born at lvl-1
+        inter += 12 * F if (fpv and not gp_last) else 0  # half ring sums hs (the last level has none)
+        inter += 12 * F if lvl >= 1 else 0               # corner-0 contributions c0
     elif name == "cc_edge":
         if gp_last:
             rd = 8 * Ep + 16 * Fp + 12 * V + 12 * F
@@ -86,19 +99,20 @@ def kernel_bytes_cc(name, c, prev, lvl, levels, prev2=None):
         wr = 12 * E + (8 * (2 * E + S) if child_rows else 0)
         wr += 12 * (Ep + Eq) if gp_last else 0    # vertex points of the edge points born at lvl, lvl-1
     elif name == "cc_vertex":
-        if gp_last:  # vertices born before lvl-1 only: p + their faces' c0 (each read once)
+        if gp_last:  # vertices born before lvl-1 only: p in, S out; their faces' c0 sums
             nv = V - Fp - Ep - Fq - Eq
-            return 12 * nv + 12 * (F - 4 * Fq - 4 * Eq) + 12 * nv
+            return {"method": 12 * nv + 12 * nv, "intermediate": 12 * (F - 4 * Fq - 4 * Eq)}
         if Fq:  # the face points born at lvl-1 are done by the face kernel
             V = V - Fq
         if lvl >= 1:  # c0 sums for vertices born earlier, half sums for new edge points
-            rd = 12 * V + 12 * (F - 4 * Fq) + 8 * Ep + (12 * F if fpv else 0) + (0 if fpv else 4 * S + 12 * F)
+            rd = 12 * V + 8 * Ep + (0 if fpv else 4 * S + 12 * F)
+            inter = 12 * (F - 4 * Fq) + (12 * F if fpv else 0)
         else:
             rd = 4 * S + 12 * V + 12 * F
         wr = 12 * (V - (Fp if fpv else 0))
     else:
         return None
-    return rd + wr
+    return {"method": rd + wr, "intermediate": inter}
 
 
 def survey_level_bytes_cc(c, final):
@@ -311,8 +325,6 @@ def run_alsub(args):
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     peak, peak_src = peaks()
-    if args.config == 5:
-        return run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, peak_src)
 
     levels = args.levels
     mesh = mg.armor9k(seed=mg.SEED_TOPO + rank)
@@ -371,6 +383,13 @@ def run_alsub(args):
     step_pct = {"p10": srt[int(0.1 * (K - 1))], "median": srt[(K - 1) // 2], "p90": srt[int(0.9 * (K - 1))],
                 "note": "this rank's per-step CUDA-event times (SURVEY 8(d) timing protocol)"}
 
+    ncu_kernels = {}
+    prof_sum = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof_sum):
+        try:
+            ncu_kernels = json.load(open(prof_sum)).get("kernels", {})
+        except Exception:
+            ncu_kernels = {}
     per_level = []
     for lvl in range(-1, levels):
         ks = {n: t for (n, l), t in kt.items() if l == lvl}
@@ -386,26 +405,30 @@ def run_alsub(args):
             for n, t in ks.items():
                 b = kernel_bytes_cc(n, c, cnt[lvl - 1] if lvl > 0 else None, lvl, levels,
                                     cnt[lvl - 2] if lvl > 1 else None)
-                kk[n] = {"ms": t, "alg_bytes": b, "GBps": (b / (t * 1e6)) if b else None,
-                         "frac": (b / (t * 1e6) / peak) if b else None}
+                mb = b["method"] if b else None
+                kk[n] = {"ms": t, "alg_bytes": mb, "intermediate_bytes": b["intermediate"] if b else None,
+                         "GBps": (mb / (t * 1e6)) if mb else None, "frac": (mb / (t * 1e6) / peak) if mb else None}
+                nc = ncu_kernels.get(f"{n}@L{lvl}")
+                if nc and mb:  # ncu DRAM bytes of the same launch (profiles/ncu_summary.json)
+                    kk[n]["dram_bytes"] = nc["dram_bytes"]
+                    kk[n]["waste"] = nc["dram_bytes"] / mb  # DRAM traffic / method bytes
             row["kernels"] = kk
         per_level.append(row)
-    dbytes = kernel_bytes_cc(dname, cnt[dlvl], cnt[dlvl - 1] if dlvl > 0 else None, dlvl, levels,
-                             cnt[dlvl - 2] if dlvl > 1 else None) \
-        if dlvl >= 0 else None
+    db = kernel_bytes_cc(dname, cnt[dlvl], cnt[dlvl - 1] if dlvl > 0 else None, dlvl, levels,
+                         cnt[dlvl - 2] if dlvl > 1 else None) if dlvl >= 0 else None
+    dbytes = db["method"] if db else None
     dms = sum(probe_ms) / len(probe_ms) if probe_ms else dms_profile
     achieved = dbytes / (dms * 1e6) if dbytes else None
-    traffic = None
-    prof_sum = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof_sum):
-        try:
-            ps = json.load(open(prof_sum))
-            traffic = ps.get("kernels", {}).get(f"{dname}@L{dlvl}", {}).get("dram_bytes")
-        except Exception:
-            traffic = None
+    traffic = ncu_kernels.get(f"{dname}@L{dlvl}", {}).get("dram_bytes")
     roofline = {"bound": "hbm", "kernel": f"{dname} (level {dlvl}->{dlvl + 1})", "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "alg_bytes_per_launch": dbytes, "avg_launch_ms": dms, "share_of_step": dms / ms_per_step,
+                "alg_bytes_per_launch": dbytes,
+                "alg_bytes_note": "method bytes only (parent topology + positions in, child topology + refined "
+                                  "positions out); the kernel's scratch writes (corner sums c0, half sums hs) are "
+                                  "in intermediate_bytes_per_launch, not in achieved",
+                "intermediate_bytes_per_launch": db["intermediate"] if db else None,
+                "waste": (traffic / dbytes) if (traffic and dbytes) else None,
+                "avg_launch_ms": dms, "share_of_step": dms / ms_per_step,
                 "share_of_kernel_time": dms_profile / prof_step,  # comparable with the ncu launch list
                                                                   # (serialised kernels, no branch overlap)
                 "launches_timed": len(probe_ms),
@@ -413,18 +436,25 @@ def run_alsub(args):
                           "replayed refine graph of the timed region (alsub_probe), on its own stream",
                 "profile_pass_ms": dms_profile, "peak_source": peak_src}
 
-    # ---- e2e through the C ABI with host buffers ----
+    # ---- the last level's crease lists (not in the timed step): built on first export ----
+    lazy = last_level_lists_ms(m, levels)
+
+    # ---- e2e through the C ABI with host buffers (every rank its replica; the slowest rank) ----
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, mesh, levels, Fout, Vout, dev, flush)
+        ms_e2e = max_over_ranks(e2e["ms_per_step"])
+        e2e.update(value=world * Fout / (ms_e2e / 1000.0), ms_per_step=ms_e2e,
+                   h2d_bytes_per_step=world * e2e["h2d_bytes_per_step"], d2h_bytes_per_step=world * e2e["d2h_bytes_per_step"])
 
     others = None
-    frames = None
     if rank == 0 and world == 1 and not args.no_other_configs:
         others = other_configs(dev, flush, peak)
-        fa = argparse.Namespace(**vars(args))
-        fa.frames, fa.warmup = 64, 3
-        frames = run_frames(fa, 0, 1, dev, flush, lambda: None, lambda x: x, peak, peak_src, emit=False)
+    frames = None
+    if not args.no_frames:  # every rank: config 5's frames are split over all of them
+        del flush
+        torch.cuda.empty_cache()
+        frames = run_frames(args, rank, world, dev, barrier, max_over_ranks, peak, peak_src)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -445,13 +475,33 @@ def run_alsub(args):
                 "gpu_launches": int(launches_per_step * K), "launches_per_step": int(launches_per_step),
                 "step_ms": step_pct,
                 "clocks": sampler.summary(), "levels": per_level, "profile_step_ms": prof_step,
-                "other_configs": others, "frames_config5_sample": frames,
+                "last_level_crease_lists": lazy,
+                "other_configs": others, "frames": frames,
                 "paper_context": PAPER_CONTEXT}
         print(json.dumps(line), flush=True)
     m.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def last_level_lists_ms(m, levels):
+    """The crease inheritance of the last refined level (its child crease pairs / sigma and the
+    special-vertex rows) is not part of alsub_refine: nothing in the step reads it, so
+    the first export after a refine builds it (ensure_last_lists).  Timed here as the difference
+    between the first and the second crease export after a refine."""
+    import torch
+    m.refine("cc", levels)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        m.topology(levels, faces=False, creases=True)
+        torch.cuda.synchronize()
+        ts.append(1e3 * (time.perf_counter() - t0))
+    return {"ms": ts[0] - ts[1], "first_export_ms": ts[0], "cached_export_ms": ts[1],
+            "note": "the level-L crease lists are built lazily on first export, outside the timed step "
+                    "(no kernel of the step reads them)"}
 
 
 def other_configs(dev, flush, peak, reps=20):
@@ -528,107 +578,194 @@ def run_e2e(args, mesh, levels, Fout, Vout, dev, flush):
             "path": "alsub_mesh_create(host) + alsub_refine + alsub_level_positions/topology(pinned host)"}
 
 
-def run_frames(args, rank, world, dev, flush, barrier, max_over_ranks, peak, peak_src, emit=True):
-    """Config 5: static-mode frames, armor50k CC level 4, 4096 frames sharded over ranks."""
+def device_frames(P0, t0, n, nframes, dev):
+    """Frames t0 .. t0+n-1 of config 5 generated on the device (P0 rotated by
+    2 pi t / nframes about z plus 0.05 sin(2 pi t / 64 + 7 x) along y), float32 [n][V0][3].  Input
+    generation only (meshgen.frame_positions is the host definition the parity tests use)."""
     import torch
+    p = torch.from_numpy(P0).to(dev, torch.float64)
+    t = torch.arange(t0, t0 + n, device=dev, dtype=torch.float64)[:, None]
+    th = 2 * math.pi * t / nframes
+    c, s_ = torch.cos(th), torch.sin(th)
+    x = c * p[None, :, 0] - s_ * p[None, :, 1]
+    y = s_ * p[None, :, 0] + c * p[None, :, 1] + 0.05 * torch.sin(2 * math.pi * t / 64 + 7 * p[None, :, 0])
+    z = p[None, :, 2].expand(n, -1)
+    return torch.stack([x, y, z], dim=2).to(torch.float32).contiguous()
+
+
+def run_frames(args, rank, world, dev, barrier, max_over_ranks, peak, peak_src):
+    """Config 5: 4096 animation frames of armor50k (CC level 4) split over the ranks (contiguous
+    blocks, strong scaling).  Each rank builds the topology and the refinement matrix itself, then
+    streams its frames through alsub_eval_frames_matrix in batches of 32 into two output buffers;
+    every output frame is reduced to a 32-B record (alsub_frame_summary, side stream, overlapped with
+    the next batch) and the records are all-gathered over NCCL -- the job's only data-path
+    collective.  Returns the measurement on rank 0 (None elsewhere)."""
+    import torch
+    import torch.distributed as dist
     from paper_1809_06047_b200 import Mesh, frame_summary
-    levels = 4
-    nframes = args.frames
+    levels, nframes, nb = 4, args.frames, 32
     mesh = mg.armor50k()
-    nb = 8
     f_lo, f_hi = shard(nframes, world, rank)
     per_rank = f_hi - f_lo
-    P0 = mesh["pos"]
-    # frame inputs resident in HBM: this rank's block of frames (V0 x 12 B each)
-    frames = torch.stack([torch.from_numpy(mg.frame_positions(P0, f_lo + t, nframes)) for t in range(per_rank)]).to(dev)
-    m = Mesh(mesh["face_off"], mesh["face_vtx"], P0, mesh["crease"], mesh["sigma"])
+    m = Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"])
     m.refine("cc", levels)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    info = m.build_refinement_matrix(levels)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    blk = m.refinement_matrix_blocks()
     cnt = level_counts(m, levels)
-    Vout, Fout = cnt[-1]["V"], cnt[-1]["F"]
+    Vout, Fout, V0 = cnt[-1]["V"], cnt[-1]["F"], cnt[0]["V"]
+    frames = device_frames(mesh["pos"], f_lo, per_rank, nframes, dev)  # this rank's inputs, in HBM
     outs = [torch.empty((nb, Vout, 3), dtype=torch.float32, device=dev) for _ in range(2)]
-    nsteps = per_rank // nb
-    # per-frame result records (bbox + checksum, alsub_frame_summary), gathered over NCCL at the end
-    summ = torch.zeros((per_rank, 8), dtype=torch.int32, device=dev)
+    summ = torch.zeros((max(per_rank, 1), 8), dtype=torch.int32, device=dev)
+    nbatch = (per_rank + nb - 1) // nb
     stream = torch.cuda.current_stream()
-    # the summary of batch i runs on a side stream, overlapped with the evaluation of batch i + 1
-    # (the level kernels leave DRAM bandwidth unused); batch i + 2 reuses the buffer only after it
-    side = torch.cuda.Stream(device=dev)
-    done = [torch.cuda.Event(), torch.cuda.Event()]
-    ev_s = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
 
-    def batch(i, timed_last=False):
-        k = i % 2
-        if i >= 2:
-            stream.wait_event(done[k])
-        m.eval_frames(frames[i * nb:(i + 1) * nb], levels, out=outs[k])
-        ready = torch.cuda.Event()
-        ready.record(stream)
-        side.wait_event(ready)
-        with torch.cuda.stream(side):
-            if timed_last:
-                ev_s[0][0].record(side)
-            frame_summary(outs[k], out=summ[i * nb:(i + 1) * nb], stream=side)
-            if timed_last:
-                ev_s[0][1].record(side)
-            done[k].record(side)
+    def batch(i):
+        # the frame records are folded into the evaluation (alsub_eval_frames_matrix_summary): the
+        # output frames are not read back; two output buffers alternate (a consumer would overlap
+        # its reads of one with the evaluation into the other)
+        lo, hi = i * nb, min(per_rank, (i + 1) * nb)
+        m.eval_frames_matrix_summary(frames[lo:hi], out=outs[i % 2][:hi - lo], summary=summ[lo:hi])
 
-    for i in range(min(args.warmup, nsteps)):
+    for i in range(min(max(args.warmup, 1), nbatch)):
         batch(i)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    # the fused records must equal a separate summary pass over the frames written (the last
+    # warm-up batch's buffer)
+    iw = min(max(args.warmup, 1), nbatch) - 1
+    lo, hi = iw * nb, min(per_rank, (iw + 1) * nb)
+    records_ok = bool(torch.equal(frame_summary(outs[iw % 2][:hi - lo]), summ[lo:hi]))
+    e0, eg, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     sampler = ClockSampler(dev.index)
     barrier()
     torch.cuda.synchronize()
     with sampler:
         e0.record(stream)
-        for i in range(nsteps):
-            batch(i, timed_last=i == nsteps - 1)
-        stream.wait_stream(side)
-        eg = torch.cuda.Event(enable_timing=True)
+        for i in range(nbatch):
+            batch(i)
         eg.record(stream)
-        table = gather_summaries(summ[:nsteps * nb], nsteps * nb * world, world, rank, device=dev)
+        table = gather_summaries(summ[:per_rank], nframes, world, rank, device=dev)
         e1.record(stream)
         torch.cuda.synchronize()
-    gather_ms = eg.elapsed_time(e1)  # the NCCL all-gather of the records (SURVEY 8(d): reported apart)
     barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1))
-    summary_ms = ev_s[0][0].elapsed_time(ev_s[0][1]) if nsteps else 0.0
-    table_rows = int(table.shape[0])
-    total_frames = nsteps * nb * world
-    value = total_frames * Fout / (ms / 1000.0)
-    bytes_per_frame = sum(12 * cnt[l]["V"] + 12 * cnt[l + 1]["V"] for l in range(levels))
-    gbps = nsteps * nb * bytes_per_frame / (ms * 1e6 / 1.0) if ms else None
-    if not emit:
-        m.close()
-        return {"frames": total_frames, "faces_per_frame": Fout, "ms_per_batch_of_8": ms / nsteps,
-                "summary_ms_per_batch": summary_ms,
-                "faces_per_s": value, "position_GBps": gbps, "position_frac": gbps / peak if gbps else None}
+    local_ms = e0.elapsed_time(e1)
+    gather_ms = eg.elapsed_time(e1)
+    ms = max_over_ranks(local_ms)
+    # which GPUs took part: every rank reports its device; NCCL's communicator size
+    uuid = str(getattr(torch.cuda.get_device_properties(dev), "uuid", dev.index))
+    if world > 1:
+        names = [None] * world
+        dist.all_gather_object(names, (rank, uuid))
+        gpus_active = len({u for _, u in names})
+    else:
+        gpus_active = 1
+    comm_ok = (dist.get_world_size() if world > 1 else 1) == args.gpus
+    # algorithmic bytes of one batch of nb frames through the blocked matrix: the weights and row
+    # ids once, the control positions in (12 V0 per frame) and the refined frames out (12 V_L)
+    bytes_frame = 12 * Vout + 12 * V0 + (4 * blk["weights"] + 4 * Vout) / nb
+    per_gpu_gbps = per_rank * bytes_frame / (local_ms * 1e6) if local_ms else None
+    value = nframes * Fout / (ms / 1e3)
+    res = None
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "faces/s", "n_gpus": world, "steps": nsteps,
-                "warmup": args.warmup, "ms_per_step": ms / nsteps, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"armor50k_cc_L{levels}_frames{nframes} (SURVEY config 5)",
-                           "frames": total_frames, "batch": nb, "faces_per_frame": Fout,
-                           "l2": "inputs and outputs far larger than L2",
-                           "parallelism": f"frames sharded over {world} GPUs"},
-                "roofline": {"bound": "hbm", "achieved": gbps, "peak": peak, "unit": "GB/s",
-                             "frac": gbps / peak if gbps else None, "traffic": None,
-                             "kernel": "whole static eval (position bytes only)", "peak_source": peak_src},
-                "summaries": {"frames_gathered": table_rows, "bytes_per_frame": 32, "collective": "all_gather (NCCL)"
-                              if world > 1 else "none (1 rank)", "summary_ms_per_batch": summary_ms,
-                              "gather_ms": gather_ms},
-                "per_gpu_hbm_frac": (gbps / peak) if gbps else None,  # gbps is per rank (its frames / time)
-                "cpu_baseline": (cpu_oracle_frames(mesh, levels, (0,), nframes)
-                                 if (world == 1 and not args.no_cpu_baseline) else None),
-                "e2e": None, "gpu_launches": int((m.last_launch_count + 3) * nsteps),
-                "clocks": sampler.summary()}
-        print(json.dumps(line), flush=True)
+        res = {"workload": f"armor50k_cc_L{levels}_frames{nframes} (SURVEY config 5)", "value": value,
+               "unit": "faces/s", "ms": ms, "us_per_frame": 1e3 * ms / nframes * world,
+               "frames": nframes, "frames_per_rank": per_rank, "batch": nb, "faces_per_frame": Fout,
+               "scaling": "strong", "n_gpus": world, "gpus_active": gpus_active, "comm_nranks_ok": comm_ok,
+               "path": "alsub_eval_frames_matrix (blocked refinement matrix, P:L809)",
+               "matrix": {"rows": info["rows"], "nnz": info["nnz"], "chunks": blk["chunks"],
+                          "block_weights": blk["weights"], "build_s": build_s},
+               "roofline": {"bound": "hbm", "achieved": per_gpu_gbps, "peak": peak, "unit": "GB/s",
+                            "frac": per_gpu_gbps / peak if per_gpu_gbps else None,
+                            "bytes_per_frame": bytes_frame,
+                            "note": "per GPU (rank 0): 12 V_L out + 12 V_0 in per frame + weights and "
+                                    "row ids once per batch of 32", "peak_source": peak_src},
+               "per_gpu_hbm_frac": per_gpu_gbps / peak if per_gpu_gbps else None,
+               "summaries": {"frames_gathered": int(table.shape[0]), "bytes_per_frame": 32,
+                             "collective": "all_gather_into_tensor (NCCL)" if world > 1 else "none (1 rank)",
+                             "gather_ms": gather_ms, "fused_into_eval": True,
+                             "equal_to_alsub_frame_summary": records_ok},
+               "gpu_launches": int(m.last_launch_count * nbatch), "clocks": sampler.summary(),
+               "l2": "inputs and outputs far larger than L2"}
     m.close()
+    return res
+
+
+def run_frames_line(args):
+    """--config 5: the frames measurement as the JSON line itself."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peak, peak_src = peaks()
+    fr = run_frames(args, rank, world, dev, (lambda: dist.barrier()) if world > 1 else (lambda: None),
+                    lambda x: dist_max(x, dev), peak, peak_src)
+    if rank == 0:
+        line = {"metric": METRIC, "value": fr["value"], "unit": "faces/s", "n_gpus": world, "steps": 1,
+                "warmup": args.warmup, "ms_per_step": fr["ms"], "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": fr["workload"], "frames": fr["frames"], "batch": fr["batch"],
+                           "l2": fr["l2"], "parallelism": f"frames sharded over {world} GPUs"},
+                "roofline": dict(fr["roofline"], traffic=None), "frames": fr,
+                "cpu_baseline": (cpu_oracle_frames(mg.armor50k(), 4, (0,), fr["frames"])
+                                 if (world == 1 and not args.no_cpu_baseline) else None),
+                "e2e": None, "gpu_launches": fr["gpu_launches"], "clocks": fr["clocks"]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
     return 0
+
+
+def dry_run(args):
+    """--dry-run: the multi-rank plumbing without a GPU -- gloo process group, every rank fills its
+    shard of per-frame records, rank 0 gathers them (gather_summaries) and prints the rank map."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    lo, hi = shard(args.frames, world, rank)
+    local = torch.arange(lo, hi, dtype=torch.int32)[:, None].repeat(1, 8)
+    table = gather_summaries(local, args.frames, world, rank)
+    names = [None] * world
+    if world > 1:
+        dist.all_gather_object(names, (rank, os.getpid()))
+    else:
+        names = [(0, os.getpid())]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "requested": args.gpus,
+                          "ranks": [r for r, _ in names], "pids": len({p for _, p in names}),
+                          "frames_gathered": int(table.shape[0]),
+                          "frame_order_ok": bool((table[:, 0] == torch.arange(args.frames, dtype=torch.int32)).all())}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def relaunch(args):
+    """--gpus N with WORLD_SIZE unset: run this script under torch.distributed.run with N ranks
+    (127.0.0.1 rendezvous, a free port); returns its exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing on CPU (gloo), no GPU")
+    ap.add_argument("--no-frames", action="store_true", help="skip the config-5 frames measurement")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="alsub", choices=["alsub", "reference"])
@@ -642,8 +779,14 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 5:
+        return run_frames_line(args)
     return run_alsub(args)
 
 

@@ -185,6 +185,13 @@ alsub_status alsub_refinement_matrix_csr(const alsub_mesh *mesh, int32_t *row_of
  * than 2^31 - 1 non-zeros (its CSR export uses int32 offsets). */
 alsub_status alsub_eval_frames_matrix(alsub_mesh *mesh, const float *frames_in, int32_t num_frames, float *frames_out,
                                       void *stream);
+/* The same evaluation, and every output frame's summary record (the alsub_frame_summary layout:
+ * int32 [num_frames][8] = bbox lo.xyz, hi.xyz as float bits, then the uint64 checksum) folded in
+ * as the frame is written -- identical bit for bit to alsub_frame_summary of frames_out, without
+ * reading the frames back.  summary: DEVICE pointer.  Errors: as alsub_eval_frames_matrix; E_ARG
+ * for a null summary. */
+alsub_status alsub_eval_frames_matrix_summary(alsub_mesh *mesh, const float *frames_in, int32_t num_frames,
+                                              float *frames_out, int32_t *summary, void *stream);
 
 /* Selective / feature-adaptive subdivision, the extraction module (
  * P:L459-499, Fig. module_selective).  From level `level` of `mesh` (0, or 1 .. levels of its

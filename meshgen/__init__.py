@@ -351,6 +351,20 @@ def frame_positions(pos0, t, nframes=4096):
     return np.stack([x, y, p[:, 2]], axis=1).astype(np.float32)
 
 
+def frame_block(pos0, t0, n, nframes=4096):
+    """Frames t0 .. t0+n-1 of config 5 as one float32 array [n][V][3]: frame_positions vectorised
+    over frames (the same float64 element-wise operations, so each frame is bitwise identical)."""
+    out = np.empty((n, pos0.shape[0], 3), np.float32)
+    p = pos0.astype(np.float64)
+    for t in range(t0, t0 + n):
+        th = 2 * math.pi * t / nframes
+        c, s = math.cos(th), math.sin(th)
+        out[t - t0, :, 0] = c * p[:, 0] - s * p[:, 1]
+        out[t - t0, :, 1] = s * p[:, 0] + c * p[:, 1] + 0.05 * np.sin(2 * math.pi * t / 64 + 7 * p[:, 0])
+        out[t - t0, :, 2] = p[:, 2]
+    return out
+
+
 CONFIGS = {
     1: dict(name="cube_cc_L3", mesh=cube, scheme="cc", levels=3),
     2: dict(name="ico_loop_L6", mesh=icosahedron, scheme="loop", levels=6),

@@ -76,6 +76,7 @@ def lib():
     L.alsub_refinement_matrix_csr.argtypes = [vp, vp, vp, vp, vp]
     L.alsub_eval_frames_matrix.argtypes = [vp, vp, i32, vp, vp]
     L.alsub_refinement_matrix_blocks.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
+    L.alsub_eval_frames_matrix_summary.argtypes = [vp, vp, i32, vp, vp, vp]
     L.alsub_extract_maps.argtypes = [vp, vp, vp, vp]
     L.alsub_frame_summary.argtypes = [vp, i32, i64, vp, vp]
     L.alsub_probe.argtypes = [vp, i32, C.c_char_p, i32]
@@ -90,7 +91,7 @@ def lib():
               "alsub_level_topology", "alsub_level_positions", "alsub_eval_frames", "alsub_eval_attributes",
               "alsub_level_positions_ptr", "alsub_reevaluate", "alsub_rcm_order", "alsub_mesh_extract",
               "alsub_extract_maps", "alsub_build_refinement_matrix", "alsub_refinement_matrix_info",
-              "alsub_refinement_matrix_csr", "alsub_eval_frames_matrix", "alsub_refinement_matrix_blocks", "alsub_frame_summary", "alsub_probe",
+              "alsub_refinement_matrix_csr", "alsub_eval_frames_matrix", "alsub_refinement_matrix_blocks", "alsub_eval_frames_matrix_summary", "alsub_frame_summary", "alsub_probe",
               "alsub_probe_read"):
         getattr(L, f).restype = C.c_int
     _lib = L
@@ -224,6 +225,20 @@ class Mesh:
             out = torch.empty((B, rows, 3), dtype=torch.float32, device="cuda")
         _check(self._lib.alsub_eval_frames_matrix(self._h, _ptr(fr), B, _ptr(out), _stream(stream)))
         return out
+
+    def eval_frames_matrix_summary(self, frames, out=None, summary=None, stream=None):
+        """eval_frames_matrix plus each output frame's summary record (alsub_frame_summary layout),
+        computed while the frames are written: returns (out [B, V_L, 3], summary int32 [B, 8])."""
+        fr = frames.to(torch.float32).contiguous()
+        B = int(fr.shape[0])
+        rows = self.refinement_matrix_info()["rows"]
+        if out is None:
+            out = torch.empty((B, rows, 3), dtype=torch.float32, device="cuda")
+        if summary is None:
+            summary = torch.empty((B, 8), dtype=torch.int32, device="cuda")
+        _check(self._lib.alsub_eval_frames_matrix_summary(self._h, _ptr(fr), B, _ptr(out), _ptr(summary),
+                                                          _stream(stream)))
+        return out, summary
 
     def extract(self, level, vsel=None, rings=1, stream=None):
         """Selective / feature-adaptive subdivision, extraction module: the faces

@@ -1309,23 +1309,38 @@ extern "C" alsub_status alsub_refinement_matrix_csr(const alsub_mesh *m, int32_t
     return ALSUB_OK;
 }
 
-extern "C" alsub_status alsub_eval_frames_matrix(alsub_mesh *m, const float *frames_in, int32_t num_frames,
-                                                 float *frames_out, void *stream) {
+static alsub_status eval_frames_matrix(alsub_mesh *m, const float *frames_in, int32_t num_frames, float *frames_out,
+                                       int32_t *summary, void *stream) {
     if (!m || num_frames < 0 || (num_frames > 0 && (!frames_in || !frames_out))) return fail(ALSUB_E_ARG, "bad argument");
     if (m->rm_levels < 0) return fail(ALSUB_E_ARG, "no refinement matrix: call alsub_build_refinement_matrix");
-    if (num_frames > 0 && (!is_device_ptr(frames_in) || !is_device_ptr(frames_out)))
+    if (num_frames > 0 && (!is_device_ptr(frames_in) || !is_device_ptr(frames_out) || (summary && !is_device_ptr(summary))))
         return fail(ALSUB_E_ARG, "alsub_eval_frames_matrix takes device pointers");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V0 = m->V0, VL = m->lv[m->rm_levels].V;
     Launches L;
     for (int32_t f0 = 0; f0 < num_frames; f0 += kRmLanes) {
         const int32_t n = std::min(kRmLanes, num_frames - f0);
+        SummaryRec *rec = summary ? reinterpret_cast<SummaryRec *>(summary) + f0 : nullptr;
+        if (rec) summary_init(rec, n, s, L);
         rb_eval(m->rb_C, m->rb_row_off, m->rb_sup_off, m->rb_w_off, m->rb_rows, m->rb_sup, m->rb_W,
-                frames_in + 3 * V0 * (int64_t)f0, (int32_t)V0, n, m->rb_xt, VL, frames_out + 3 * VL * (int64_t)f0, s, L);
+                frames_in + 3 * V0 * (int64_t)f0, (int32_t)V0, n, m->rb_xt, VL, frames_out + 3 * VL * (int64_t)f0, rec,
+                s, L);
+        if (rec) summary_decode(rec, n, s, L);
     }
     m->last_launches = L.n;
     CU(cudaGetLastError());
     return ALSUB_OK;
+}
+
+extern "C" alsub_status alsub_eval_frames_matrix(alsub_mesh *m, const float *frames_in, int32_t num_frames,
+                                                 float *frames_out, void *stream) {
+    return eval_frames_matrix(m, frames_in, num_frames, frames_out, nullptr, stream);
+}
+
+extern "C" alsub_status alsub_eval_frames_matrix_summary(alsub_mesh *m, const float *frames_in, int32_t num_frames,
+                                                         float *frames_out, int32_t *summary, void *stream) {
+    if (!summary && num_frames > 0) return fail(ALSUB_E_ARG, "null summary");
+    return eval_frames_matrix(m, frames_in, num_frames, frames_out, summary, stream);
 }
 
 // ---------------- static mode: frames ----------------

@@ -120,6 +120,20 @@ ALSUB_D P3 operator+(P3 a, P3 b) { return P3{a.x + b.x, a.y + b.y, a.z + b.z}; }
 ALSUB_D P3 operator*(float s, P3 a) { return P3{s * a.x, s * a.y, s * a.z}; }
 ALSUB_D P3 p3zero() { return P3{0.f, 0.f, 0.f}; }
 
+// Per-frame summary record (alsub_frame_summary, include/alsub.h): bbox lo.xyz / hi.xyz and the
+// wrapping checksum sum_i bits(x_i) (2 i + 1).  While accumulating, lo / hi hold the ordered-int
+// image of the floats (f2ord: the same total order as the floats, so atomicMin / atomicMax on ints
+// apply); a decode pass turns them back into float bits.
+struct SummaryRec {
+    int32_t lo[3], hi[3];
+    unsigned long long sum;
+};
+ALSUB_D int32_t f2ord(float f) {
+    const int32_t i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7fffffff;
+}
+ALSUB_D float ord2f(int32_t i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
 // Long rings (level-0 vertices with more than kLongRing incident slots, e.g. poles): the vertex
 // kernels skip them in their per-lane pass and then sum each one's ring with the whole warp --
 // lanes take slots k = lane, lane + 32, ...; warp_sum is a fixed xor butterfly, so the result is

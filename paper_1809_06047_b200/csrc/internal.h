@@ -171,6 +171,10 @@ void rm_probes(int32_t V0, const int32_t *colour, int32_t nprobe, float *out, cu
 void rm_assemble(int32_t VL, const int32_t *owner, const int32_t *sup_off, const int32_t *sup, const int32_t *colour,
                  const float *probe, int64_t probe_stride, bool fill, int32_t *row_len, const int32_t *row_off,
                  int2 *ent, int64_t *nnz64, cudaStream_t s, Launches &L);
+// per-frame summary records (summary.cu): init (empty bbox, zero sum) and decode (ordered ints ->
+// float bits) of records accumulated by a producer kernel
+void summary_init(SummaryRec *rec, int32_t nb, cudaStream_t s, Launches &L);
+void summary_decode(SummaryRec *rec, int32_t nb, cudaStream_t s, Launches &L);
 // blocked R (chunk = owner face / isolated control vertex; rmatrix.cu)
 void rb_hist(int32_t VL, const int32_t *owner, const int32_t *iso_chunk, int32_t *chunk, int32_t *cnt, cudaStream_t s,
              Launches &L);
@@ -183,7 +187,7 @@ void rb_fill(int32_t VL, const int32_t *chunk, const int32_t *pos, const int32_t
              float *W, cudaStream_t s, Launches &L);
 void rb_eval(int32_t C, const int32_t *row_off, const int32_t *sup_off, const int64_t *w_off, const int32_t *rows,
              const int32_t *sup, const float *W, const float *in, int32_t V0, int32_t nb, float *XT, int64_t VL,
-             float *out, cudaStream_t s, Launches &L);
+             float *out, SummaryRec *rec, cudaStream_t s, Launches &L);
 
 // ---- selective subdivision: extraction (extract.cu) ----
 struct ExSrcHost {

@@ -238,8 +238,49 @@ constexpr int kRbXf4 = 3 * kRmLanes / 4;  // float4 per support vertex in XT / s
 // (row r and r + 32, 4 frames x 3 coords) go through shared memory so that each store instruction
 // writes 32 consecutive floats of one frame (float t of the group = coord t % 3 of its row t / 3):
 // contiguous row runs become full 128-B lines instead of 12-B-strided partial sectors.
+// the frame's summary record (alsub_frame_summary) folded in from the lane's two rows: float
+// index 3 row + c, bbox over the ordered-int images, checksum sum bits (2 idx + 1) mod 2^64; warp
+// reductions by redux.sync (the 64-bit sum as three exact 32-bit partial sums), one lane's shared
+// atomics into the CTA's record
+ALSUB_D void rb_fold(SummaryRec &r, int32_t ra, int32_t rb, const float (&a)[3], const float (&b)[3]) {
+    int32_t lo[3], hi[3];
+    unsigned long long sum = 0ull;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int32_t qa = ra >= 0 ? f2ord(a[c]) : INT32_MAX, qb = rb >= 0 ? f2ord(b[c]) : INT32_MAX;
+        const int32_t pa = ra >= 0 ? f2ord(a[c]) : INT32_MIN, pb = rb >= 0 ? f2ord(b[c]) : INT32_MIN;
+        lo[c] = min(qa, qb);
+        hi[c] = max(pa, pb);
+        if (ra >= 0) sum += (unsigned long long)(uint32_t)__float_as_int(a[c]) * (unsigned long long)(6ll * ra + 2 * c + 1);
+        if (rb >= 0) sum += (unsigned long long)(uint32_t)__float_as_int(b[c]) * (unsigned long long)(6ll * rb + 2 * c + 1);
+    }
+    const unsigned m = 0xffffffffu;
+    const uint32_t s0 = __reduce_add_sync(m, (uint32_t)(sum & 0xffffu));
+    const uint32_t s1 = __reduce_add_sync(m, (uint32_t)((sum >> 16) & 0xffffu));
+    const uint32_t s2 = __reduce_add_sync(m, (uint32_t)(sum >> 32));
+    int32_t l[3], h[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        l[c] = __reduce_min_sync(m, lo[c]);
+        h[c] = __reduce_max_sync(m, hi[c]);
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            atomicMin(&r.lo[c], l[c]);
+            atomicMax(&r.hi[c], h[c]);
+        }
+        atomicAdd(&r.sum, (unsigned long long)s0 + ((unsigned long long)s1 << 16) + ((unsigned long long)s2 << 32));
+    }
+}
+
 ALSUB_D void rb_store(float *so, const int32_t (&rid)[6], float *out, int64_t VL, int f0, int nb, int lane,
-                      const float (&a)[4][3], const float (&b)[4][3]) {
+                      const float (&a)[4][3], const float (&b)[4][3], SummaryRec *srec, int32_t rowa, int32_t rowb) {
+    if (srec) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (f0 + u < nb) rb_fold(srec[f0 + u], rowa, rowb, a[u], b[u]);
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -278,11 +319,23 @@ __global__ void __launch_bounds__(32 * kRbWarps) k_rb_eval(int32_t C, int32_t *_
                                                          const int32_t *__restrict__ rows,
                                                          const int32_t *__restrict__ sup, const float *__restrict__ W,
                                                          const float4 *__restrict__ XT, int32_t nb, int64_t VL,
-                                                         float *__restrict__ out) {
+                                                         float *__restrict__ out, SummaryRec *__restrict__ rec) {
     ALSUB_GRID_WAIT();
     extern __shared__ float4 s_dyn[];  // kRbTK x 24 float4 of positions (the CTA's), then per warp 4 x 192 floats
     __shared__ int32_t s_c;
+    // per-frame summary records of this CTA's rows (rec != nullptr), flushed to rec at the end
+    __shared__ SummaryRec s_rec[kRmLanes];
+    SummaryRec *srec = rec ? s_rec : nullptr;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (rec && threadIdx.x < kRmLanes) {
+        SummaryRec r;
+        for (int c = 0; c < 3; ++c) {
+            r.lo[c] = INT32_MAX;
+            r.hi[c] = INT32_MIN;
+        }
+        r.sum = 0ull;
+        s_rec[threadIdx.x] = r;
+    }
     float4 *sx = s_dyn;
     float *so = reinterpret_cast<float *>(s_dyn + kRbTK * kRbXf4) + w * 4 * 192;
     for (;;) {
@@ -314,6 +367,7 @@ __global__ void __launch_bounds__(32 * kRbWarps) k_rb_eval(int32_t C, int32_t *_
                     const int32_t r = g + (lane + 32 * i) / 3;
                     rid[i] = r < nr ? __ldg(rows + r0 + r) : -1;
                 }
+                const int32_t rowa = ra < nr ? __ldg(rows + r0 + ra) : -1, rowb = rb < nr ? __ldg(rows + r0 + rb) : -1;
                 for (int f0 = 0; f0 < nb; f0 += 4) {
                     float a[4][3] = {}, b[4][3] = {};
 #pragma unroll
@@ -325,7 +379,7 @@ __global__ void __launch_bounds__(32 * kRbWarps) k_rb_eval(int32_t C, int32_t *_
                         rb_fma(a, wa[k], x);
                         rb_fma(b, wb[k], x);
                     }
-                    rb_store(so, rid, out, VL, f0, nb, lane, a, b);
+                    rb_store(so, rid, out, VL, f0, nb, lane, a, b, srec, rowa, rowb);
                 }
             }
         } else {
@@ -340,6 +394,7 @@ __global__ void __launch_bounds__(32 * kRbWarps) k_rb_eval(int32_t C, int32_t *_
                     const int32_t r = g + (lane + 32 * i) / 3;
                     rid[i] = r < nr ? __ldg(rows + r0 + r) : -1;
                 }
+                const int32_t rowa = ra < nr ? __ldg(rows + r0 + ra) : -1, rowb = rb < nr ? __ldg(rows + r0 + rb) : -1;
                 for (int f0 = 0; f0 < nb; f0 += 4) {
                     float a[4][3] = {}, b[4][3] = {};
                     for (int32_t t0 = 0; t0 < S; t0 += kRbTK) {
@@ -356,11 +411,20 @@ __global__ void __launch_bounds__(32 * kRbWarps) k_rb_eval(int32_t C, int32_t *_
                             rb_fma(b, __ldg(Wc + (int64_t)(t0 + k) * R64 + rb), x);
                         }
                     }
-                    rb_store(so, rid, out, VL, f0, nb, lane, a, b);
+                    rb_store(so, rid, out, VL, f0, nb, lane, a, b, srec, rowa, rowb);
                 }
             }
         }
         __syncthreads();  // the positions and s_c are reused by the next chunk
+    }
+    if (rec && threadIdx.x < nb) {  // the loop ended with a barrier: s_rec is complete
+        const SummaryRec &r = s_rec[threadIdx.x];
+        SummaryRec &g = rec[threadIdx.x];
+        for (int c = 0; c < 3; ++c) {
+            atomicMin(&g.lo[c], r.lo[c]);
+            atomicMax(&g.hi[c], r.hi[c]);
+        }
+        atomicAdd(&g.sum, r.sum);
     }
 }
 
@@ -401,7 +465,7 @@ void rb_fill(int32_t VL, const int32_t *chunk, const int32_t *pos, const int32_t
 }
 void rb_eval(int32_t C, const int32_t *row_off, const int32_t *sup_off, const int64_t *w_off, const int32_t *rows,
              const int32_t *sup, const float *W, const float *in, int32_t V0, int32_t nb, float *XT, int64_t VL,
-             float *out, cudaStream_t s, Launches &L) {
+             float *out, SummaryRec *rec, cudaStream_t s, Launches &L) {
     if (nb <= 0) return;
     const int64_t n = (int64_t)V0 * 3 * kRmLanes;
     int32_t *next_chunk = reinterpret_cast<int32_t *>(XT + n);  // one int after the batch
@@ -416,7 +480,7 @@ void rb_eval(int32_t C, const int32_t *row_off, const int32_t *sup_off, const in
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks, k_rb_eval, 32 * kRbWarps, smem);
     const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(C, kRbWarps), 148 * std::max(max_blocks, 1));
     launch(L, "rb_eval", k_rb_eval, dim3(grid), dim3(32 * kRbWarps), smem, s, C, next_chunk, row_off, sup_off, w_off, rows, sup, W,
-           reinterpret_cast<const float4 *>(XT), nb, VL, out);
+           reinterpret_cast<const float4 *>(XT), nb, VL, out, rec);
 }
 
 }  // namespace alsub

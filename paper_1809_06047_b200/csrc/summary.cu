@@ -14,18 +14,6 @@
 namespace alsub {
 alsub_status set_error(alsub_status st, const char *msg);  // api.cu (thread-local last error)
 
-// fp32 <-> int32 with the same total order (for atomicMin / atomicMax on ints)
-ALSUB_D int32_t f2ord(float f) {
-    const int32_t i = __float_as_int(f);
-    return i >= 0 ? i : i ^ 0x7fffffff;
-}
-ALSUB_D float ord2f(int32_t i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
-
-struct SummaryRec {
-    int32_t lo[3], hi[3];
-    unsigned long long sum;
-};
-
 __global__ void __launch_bounds__(kThreads) k_summary_init(SummaryRec *out, int32_t nb) {
     ALSUB_GRID_WAIT();
     const int32_t b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -107,6 +95,13 @@ __global__ void __launch_bounds__(kThreads) k_summary_decode(SummaryRec *out, in
         r.lo[c] = __float_as_int(ord2f(r.lo[c]));
         r.hi[c] = __float_as_int(ord2f(r.hi[c]));
     }
+}
+
+void summary_init(SummaryRec *rec, int32_t nb, cudaStream_t s, Launches &L) {
+    if (nb > 0) launch(L, "summary_init", k_summary_init, dim3(grid_for(nb)), dim3(kThreads), 0, s, rec, nb);
+}
+void summary_decode(SummaryRec *rec, int32_t nb, cudaStream_t s, Launches &L) {
+    if (nb > 0) launch(L, "summary_decode", k_summary_decode, dim3(grid_for(nb)), dim3(kThreads), 0, s, rec, nb);
 }
 
 }  // namespace alsub

@@ -120,3 +120,21 @@ def test_bench_reference_arm_json():
               "cpu_baseline", "e2e", "config"):
         assert k in line
     assert line["impl"] == "reference" and line["value"] > 0
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`python bench.py --gpus 2` without torchrun re-launches itself under torch.distributed.run
+    with two ranks (--gpus was parsed and never read); --dry-run runs the multi-rank
+    plumbing (gloo process group, sharded records, their gather in frame order) without a GPU."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--dry-run", "--gpus", "2", "--frames", "37"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["ranks"] == [0, 1] and line["pids"] == 2
+    assert line["frames_gathered"] == 37 and line["frame_order_ok"]

@@ -197,3 +197,22 @@ def test_gpu_blocked_spmm_config5_full_size():
             want = oracle.refine(dict(mesh, pos=mg.frame_positions(mesh["pos"], t, 4096)), "cc", 4)[-1]["pos"]
             err = float(np.abs(out[t - first].cpu().numpy().astype(np.float64) - want).max()) / diag
             assert err <= TOL, f"frame {t}: {err:.3e}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scheme,make,L,nf", [("cc", _small, 3, 37), ("loop", lambda: mg.bipyramid(30), 2, 5)])
+def test_gpu_fused_summaries_equal_frame_summary(scheme, make, L, nf):
+    """alsub_eval_frames_matrix_summary: the records folded in while the frames are written are
+    bit for bit alsub_frame_summary of the written frames (bbox and checksum are order-free), and
+    the frames equal the plain matrix evaluation."""
+    from paper_1809_06047_b200 import Mesh, frame_summary
+    mesh = make()
+    rng = np.random.default_rng(11)
+    fr = torch.from_numpy((mesh["pos"][None] + rng.normal(0, 0.05, (nf,) + mesh["pos"].shape)).astype(np.float32)).cuda()
+    with Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"]) as m:
+        m.refine(scheme, L)
+        m.build_refinement_matrix(L)
+        out, rec = m.eval_frames_matrix_summary(fr)
+        plain = m.eval_frames_matrix(fr)
+        assert torch.equal(out, plain)
+        assert torch.equal(rec, frame_summary(out))
