@@ -76,8 +76,10 @@ typedef struct {
  *   crease_pairs [num_creases][2] int32 vertex pairs (nullable if num_creases == 0)
  *   crease_sigma [num_creases] fp32, >= 0, +inf allowed; 0 entries are ignored
  *   alloc        nullable
- * Copies every input (they may be freed on return), runs the level-0 build once on `stream`
- * to validate the mesh and count its edges, and synchronises `stream` once.
+ * Copies every input (they may be freed on return), runs the whole level-0 build on `stream`
+ * and synchronises `stream` once, after it, to read E_0, the validation flags and the special-
+ * list sizes together (edge arrays are sized by the bound E_0 <= S_0 until then).  Device-
+ * resident face_off adds one earlier read of the offsets (S_0, face orders) on `stream`.
  * Errors: E_ARG, E_MESH, E_NONMANIFOLD, E_CREASE, E_OVERFLOW, E_NOMEM, E_CUDA (no handle). */
 alsub_status alsub_mesh_create(const int32_t *face_off, const int32_t *face_vtx, int32_t num_faces,
                                const float *pos, int32_t num_verts,

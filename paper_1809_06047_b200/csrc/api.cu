@@ -245,7 +245,12 @@ static alsub_status create_impl(const int32_t *face_off, const int32_t *face_vtx
     cudaStream_t s = (cudaStream_t)stream;
     // face offsets on the host: S0, monotonicity, uniform order
     std::vector<int32_t> off((size_t)num_faces + 1);
-    CU(cudaMemcpy(off.data(), face_off, sizeof(int32_t) * off.size(), cudaMemcpyDefault));
+    if (is_device_ptr(face_off)) {  // device-resident offsets: one read on the stream before the build
+        CU(cudaMemcpyAsync(off.data(), face_off, sizeof(int32_t) * off.size(), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+    } else {
+        std::memcpy(off.data(), face_off, sizeof(int32_t) * off.size());
+    }
     if (off[0] != 0) return fail(ALSUB_E_MESH, "face_off[0] != 0");
     int order = -1;
     for (int32_t r = 0; r < num_faces; ++r) {
@@ -314,48 +319,44 @@ static alsub_status create_impl(const int32_t *face_off, const int32_t *face_vtx
     cudaMemsetAsync(b.scalars, 0, 8 * sizeof(int32_t), s);
     init_scheme_tables(s);
     Launches L;
-    // stage 1: face validation (+ the sort input and histograms)
-    build0_validate(b, s, L);
-    int32_t flags = 0;
-    if (cudaMemcpyAsync(&flags, b.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
-        return bail(fail(ALSUB_E_CUDA, std::string("level-0 validation: ") + cudaGetErrorString(cudaGetLastError())));
-    if (flags) return bail(map_flags(flags));
-    // stage 2: M^T + symbolic edge count -> E_0
-    build0_count_edges(b, s, L);
-    int32_t E0 = 0;
-    cudaMemcpyAsync(&E0, b.scalars + 0, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess)
-        return bail(fail(ALSUB_E_CUDA, std::string("level-0 edge count: ") + cudaGetErrorString(cudaGetLastError())));
-    m->E0 = E0;
-    b.E = E0;
-    const int64_t nw = ceil_div(E0 > 0 ? E0 : 1, 32);
-    b.edge_hh = A<int2>(m, E0, s, ML, ok);
+    // The whole level-0 build runs before the one host read: the edge arrays are sized by the
+    // upper bound E_0 <= S_0 (every edge has a slot), the kernels that need E_0 read it from the
+    // device, and the validation flags, E_0 and the special-list sizes come back together.  The
+    // kernels are memory-safe on invalid input (out-of-range ids never become edges); the flags
+    // then turn the whole create into an error.
+    const int32_t Emax = std::max<int32_t>(S0, 1);
+    const int64_t nw = ceil_div(Emax, 32);
+    b.edge_hh = A<int2>(m, Emax, s, ML, ok);
     b.bnd_word = A<uint32_t>(m, nw, s, ML, ok);
     b.bnd_wcnt = A<int32_t>(m, nw, s, ML, ok);
     b.bnd_wpre = A<int32_t>(m, nw, s, ML, ok);
-    b.edge_sigma = A<float>(m, E0, s, ML, ok);
-    b.edge_cidx = A<int32_t>(m, E0, s, ML, ok);
-    b.sp_flag = A<int32_t>(m, E0, s, ML, ok);
-    b.sp_off = A<int32_t>(m, E0, s, ML, ok);
-    b.sp = A<SpEdge>(m, E0, s, ML, ok);
+    b.edge_sigma = A<float>(m, Emax, s, ML, ok);
+    b.edge_cidx = A<int32_t>(m, Emax, s, ML, ok);
+    b.sp_flag = A<int32_t>(m, Emax, s, ML, ok);
+    b.sp_off = A<int32_t>(m, Emax, s, ML, ok);
+    b.sp = A<SpEdge>(m, Emax, s, ML, ok);
     b.sv_vtx = A<int32_t>(m, num_verts, s, ML, ok);
     b.sv_off = A<int32_t>(m, (int64_t)num_verts + 1, s, ML, ok);
     b.sv_cnt = A<int32_t>(m, num_verts, s, ML, ok);
     b.sv_cur = A<int32_t>(m, num_verts, s, ML, ok);
-    b.sv_list = A<int32_t>(m, 2 * (int64_t)E0, s, ML, ok);
+    b.sv_list = A<int32_t>(m, 2 * (int64_t)Emax, s, ML, ok);
     b.spw = A<uint32_t>(m, nw, s, ML, ok);
     b.spwpre = A<int32_t>(m, nw, s, ML, ok);
     m->sv_vtx = m->sv_vtx_create = b.sv_vtx;
     m->sv_off = m->sv_off_create = b.sv_off;
     if (!ok) return bail(fail(ALSUB_E_NOMEM, "device allocation failed"));
-    build0_fill(b, true, s, L);
-    int32_t sc[8];
+    build0_validate(b, s, L);     // a1: validation + M^T row lengths
+    build0_count_edges(b, s, L);  // a2 + symbolic a3 -> E_0 on the device
+    b.E = Emax;
+    build0_fill(b, true, s, L);   // numeric a3, crease matrix, special lists
+    int32_t flags = 0, sc[8];
     cudaMemcpyAsync(&flags, b.flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(sc, b.scalars, sizeof(sc), cudaMemcpyDeviceToHost, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess)
+    if (cudaStreamSynchronize(s) != cudaSuccess)  // the create's one host synchronisation
         return bail(fail(ALSUB_E_CUDA, std::string("level-0 build: ") + cudaGetErrorString(cudaGetLastError())));
     if (flags) return bail(map_flags(flags));
+    m->E0 = sc[0];
+    b.E = sc[0];
     m->B0 = sc[1];
     m->K0 = sc[2];
     m->NSV0 = sc[3];
@@ -886,9 +887,18 @@ extern "C" alsub_status alsub_level_topology(const alsub_mesh *mc, int32_t level
         if (!have) { free_list(m, tmp, s); return fail(ALSUB_E_ARG, "edge tables are not kept for this level"); }
         LevelHost Lx = *L;
         if (rebuild) {
-            // re-emit the edge pairs of this (last refined) level with the parent's topology kernels
+            // re-emit the edge pairs of this (last refined) level with the parent's topology kernels,
+            // into scratch copies of everything those kernels write (face rows, boundary words and
+            // prefixes), so the live tables of the handle are only read (a const export
+            // must not race a replay on another stream)
+            const int64_t nwx = ceil_div(L->E > 0 ? L->E : 1, 32);
             Lx.edge_hh = A<int2>(m, L->E, s, tmp, ok);
-            if (!ok) return fail(ALSUB_E_NOMEM, "export buffer");
+            Lx.face_vtx = A<int32_t>(m, L->S, s, tmp, ok);
+            if (L->bnd_word) {
+                Lx.bnd_word = A<uint32_t>(m, nwx, s, tmp, ok);
+                Lx.bnd_wpre = A<int32_t>(m, nwx, s, tmp, ok);
+            }
+            if (!ok) { free_list(m, tmp, s); return fail(ALSUB_E_NOMEM, "export buffer"); }
             const LevelHost &Pp = m->lv[level - 1];
             LevelDev pd = dev_of(Pp);
             ChildDev cd = child_of(Lx);

@@ -106,7 +106,8 @@ __global__ void k_edge_count(const int32_t *__restrict__ face_vtx, const int32_t
         if (lane < n) row[rank] = sq;
         __syncwarp();
         const WarpCand c = warp_cand<ORDER, false>(face_vtx, vtx_slot, tp, o0, n, lane);
-        const unsigned b = __ballot_sync(0xffffffffu, c.first && c.x < j);
+        // unsigned: an out-of-range (negative) id of an invalid mesh is never an edge
+        const unsigned b = __ballot_sync(0xffffffffu, c.first && (uint32_t)c.x < (uint32_t)j);
         if (lane == 0) cnt[j] = __popc(b);
         return;
     }
@@ -145,11 +146,11 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
     if (lane == 0) slot0[j] = n > 0 ? vtx_slot[o0] : -1;
     if (n <= 16) {
         const WarpCand c = warp_cand(face_vtx, vtx_slot, tp, o0, n, lane);
-        const bool mine = c.first && c.x < j;
+        const bool mine = c.first && (uint32_t)c.x < (uint32_t)j;
         int32_t rank = 0;
         for (int k = 0; k < 2 * n; ++k) {  // candidates live in lanes < 2n (n is warp-uniform)
             const int32_t xk = __shfl_sync(0xffffffffu, c.x, k);
-            const unsigned b = __ballot_sync(0xffffffffu, c.first && c.x < xk);
+            const unsigned b = __ballot_sync(0xffffffffu, c.first && (uint32_t)c.x < (uint32_t)xk);
             if (lane == k) rank = __popc(b);
         }
         // the directed slots of the edge among the candidate lanes: even lanes carry j -> x,
@@ -401,9 +402,12 @@ __global__ void __launch_bounds__(kThreads) k_b0_flags(const int32_t *__restrict
                                                      Topo<ORDER> tp, int32_t V, int32_t E, const uint32_t *__restrict__ bnd_word,
                                                      int32_t nw, float *__restrict__ edge_sigma,
                                                      int32_t *__restrict__ edge_cidx, int32_t *__restrict__ flag,
-                                                     int32_t *__restrict__ wcnt, int32_t *flags, int32_t lenient) {
+                                                     int32_t *__restrict__ wcnt, int32_t *flags, int32_t lenient,
+                                                     const int32_t *__restrict__ Edev) {
     ALSUB_GRID_WAIT();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // inside alsub_mesh_create the arrays are sized by an upper bound and E is only on the device
+    if (Edev) E = min(E, *Edev);
     if (t < E && edge_hh[t].y < 0) atomicOr(flag + t, 1);
     if (t < nw) wcnt[t] = __popc(bnd_word[t]);
     // one warp per crease pair: the lanes test the incident slots of max(a, b) in parallel
@@ -609,7 +613,8 @@ static void fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     const int64_t nf = std::max<int64_t>(std::max<int64_t>(E, 32 * (int64_t)b.K_in), nw);
     launch(L, "b0_flags", k_b0_flags<ORDER>, dim3(grid_for(nf)), dim3(kThreads), 0, s, b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
                                                  b.face_edge, b.edge_hh, tp, b.V, E, b.bnd_word, nw, b.edge_sigma,
-                                                 b.edge_cidx, b.sp_flag, b.bnd_wcnt, b.flags, b.crease_lenient);
+                                                 b.edge_cidx, b.sp_flag, b.bnd_wcnt, b.flags, b.crease_lenient,
+                                                 b.zeroed ? nullptr : b.scalars + 0);
     // the special-list chain (special edges, special-vertex CSR) is only read by the crease rules of
     // the level kernels: with a side stream it runs as a parallel branch beside the boundary-word
     // prefix scan and the level-0 face kernel, and stays open (L.build_open) until the level-0
