@@ -239,17 +239,34 @@ def host_cpu():
 
 
 def cpu_oracle_baseline(mesh, levels, label):
-    """The oracle as it stands, single-threaded, on this host: faces/s of the final level."""
+    """The oracle as it stands on this host: the full workload level by level,
+    once single-threaded (liboracle.so) and once on every host core (the same source built with
+    OpenMP over its single-writer per-element loops; the edge sort stays serial).  value = the
+    faster run's final-level faces/s (cores = its thread count); both runs' per-level times are
+    reported."""
     import oracle
     oracle.build()
-    t0 = time.perf_counter()
-    recs = oracle.refine(mesh, "cc", levels)
-    dt = time.perf_counter() - t0
-    F = recs[-1]["F"]
     model, ncpu = host_cpu()
-    return {"value": F / dt, "unit": "faces/s", "cores": 1, "kind": "oracle",
-            "sample": f"{label}: CC levels 0->{levels} ({F} faces) in {dt:.2f} s, single-threaded C oracle (fp64)",
-            "seconds": dt, "host_cpu": model, "host_cores": ncpu}
+    runs = {}
+    for threads in (1, ncpu):
+        t = []
+        t0 = time.perf_counter()
+        if threads == 1:
+            recs = oracle.refine(mesh, "cc", levels, times=t)
+            used = 1
+        else:
+            used = oracle.lib_threads(threads)[1]
+            recs = oracle.refine(mesh, "cc", levels, threads=threads, times=t)
+        dt = time.perf_counter() - t0
+        F = recs[-1]["F"]
+        del recs
+        runs[used] = {"seconds": dt, "level_seconds": t, "faces_per_s": F / dt}
+    best = max(runs, key=lambda k: runs[k]["faces_per_s"])  # the faster of the two runs
+    ncpu_used = max(runs)
+    return {"value": runs[best]["faces_per_s"], "unit": "faces/s", "cores": best, "kind": "oracle",
+            "sample": f"{label}: CC levels 0->{levels} ({F} faces), C oracle (fp64), "
+                      f"{runs[1]['seconds']:.2f} s on 1 thread, {runs[ncpu_used]['seconds']:.2f} s on {ncpu_used}",
+            "runs": {str(k): v for k, v in runs.items()}, "host_cpu": model, "host_cores": ncpu}
 
 
 def cpu_oracle_frames(mesh, levels, frames, nframes):
@@ -459,7 +476,6 @@ def run_alsub(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_baseline(mg.armor9k(), levels, "armor9k (config 3), the full workload")
-        cpu.pop("seconds", None)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "faces/s", "n_gpus": world, "steps": K,

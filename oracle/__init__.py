@@ -46,31 +46,62 @@ class _Edges(C.Structure):
                 ("edge_vtx", C.POINTER(C.c_int32)), ("edge_face", C.POINTER(C.c_int32))]
 
 
-def build(force: bool = False) -> str:
-    """Compile the oracle with plain gcc (no fast-math)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+_HDR = os.path.join(_HERE, "alsub_oracle.h")
+
+
+def _compile(out, extra):
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
+    if not os.path.exists(out) or os.path.getmtime(out) < newest:
+        tmp = out + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c99", "-D_DEFAULT_SOURCE", "-fPIC", "-shared",
-                               "-Wall", "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+                               "-Wall"] + extra + ["-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, out)
+    return out
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with plain gcc (no fast-math): the serial library the tests use, and the
+    same source with -fopenmp for the all-cores host baseline (bench.py)."""
+    if force:
+        for p in (_LIB, _LIB_OMP):
+            if os.path.exists(p):
+                os.remove(p)
+    _compile(_LIB_OMP, ["-fopenmp"])
+    return _compile(_LIB, [])
 
 
 _lib = None
+_lib_omp = None
+
+
+def _setup(L):
+    L.om_level.argtypes = [C.c_int, C.POINTER(_Mesh), C.POINTER(_Mesh), C.POINTER(_Edges), C.c_char_p, C.c_int]
+    L.om_edges_of.argtypes = [C.POINTER(_Mesh), C.POINTER(_Edges), C.c_char_p, C.c_int]
+    L.om_mesh_free.argtypes = [C.POINTER(_Mesh)]
+    L.om_edges_free.argtypes = [C.POINTER(_Edges)]
+    L.om_loop_beta.restype = C.c_double
+    L.om_loop_beta.argtypes = [C.c_int]
+    L.om_sqrt3_alpha.restype = C.c_double
+    L.om_sqrt3_alpha.argtypes = [C.c_int]
+    L.om_set_threads.restype = C.c_int
+    L.om_set_threads.argtypes = [C.c_int]
+    return L
+
+
+def lib_threads(n):
+    """The OpenMP build with n threads (bench.py's all-cores oracle timing); returns (lib, threads)."""
+    global _lib_omp
+    if _lib_omp is None:
+        build()
+        _lib_omp = _setup(C.CDLL(_LIB_OMP))
+    return _lib_omp, _lib_omp.om_set_threads(int(n))
 
 
 def lib():
     global _lib
     if _lib is None:
-        _lib = C.CDLL(build())
-        _lib.om_level.argtypes = [C.c_int, C.POINTER(_Mesh), C.POINTER(_Mesh), C.POINTER(_Edges), C.c_char_p, C.c_int]
-        _lib.om_edges_of.argtypes = [C.POINTER(_Mesh), C.POINTER(_Edges), C.c_char_p, C.c_int]
-        _lib.om_mesh_free.argtypes = [C.POINTER(_Mesh)]
-        _lib.om_edges_free.argtypes = [C.POINTER(_Edges)]
-        _lib.om_loop_beta.restype = C.c_double
-        _lib.om_loop_beta.argtypes = [C.c_int]
-        _lib.om_sqrt3_alpha.restype = C.c_double
-        _lib.om_sqrt3_alpha.argtypes = [C.c_int]
+        _lib = _setup(C.CDLL(build()))
     return _lib
 
 
@@ -145,25 +176,34 @@ def edges_of(rec):
     return out
 
 
-def level(rec, scheme):
-    """One refinement level: returns (child record, parent edge tables)."""
+def level(rec, scheme, L=None):
+    """One refinement level: returns (child record, parent edge tables).  L: the library (default
+    the serial build)."""
+    L = L or lib()
     keep = []
     m = _to_c(rec, keep)
     out, e = _Mesh(), _Edges()
     err = C.create_string_buffer(512)
-    st = lib().om_level(SCHEMES[scheme], C.byref(m), C.byref(out), C.byref(e), err, 512)
+    st = L.om_level(SCHEMES[scheme], C.byref(m), C.byref(out), C.byref(e), err, 512)
     if st != 0:
         raise OracleError(st, err.value.decode())
     child, edges = _from_c(out), _edges_from_c(e)
-    lib().om_mesh_free(C.byref(out))
-    lib().om_edges_free(C.byref(e))
+    L.om_mesh_free(C.byref(out))
+    L.om_edges_free(C.byref(e))
     return child, edges
 
 
-def refine(mesh, scheme, levels, edges_last=False):
+def refine(mesh, scheme, levels, edges_last=False, threads=None, times=None):
+    """Levels 0..levels of `mesh`.  threads: run the OpenMP build with that many threads (same
+    results); times: a list that receives the wall time of each level (seconds)."""
+    import time
+    L = lib_threads(threads)[0] if threads else lib()
     recs = [level0(mesh)]
     for _ in range(levels):
-        child, edges = level(recs[-1], scheme)
+        t0 = time.perf_counter()
+        child, edges = level(recs[-1], scheme, L)
+        if times is not None:
+            times.append(time.perf_counter() - t0)
         recs[-1].update(edges)
         recs.append(child)
     if edges_last:

@@ -24,6 +24,27 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* OpenMP appears only in the separately compiled liboracle_omp.so that times the oracle on all
+ * host cores.  It marks the per-face / per-edge / per-vertex loops of a level,
+ * each iteration the single writer of its outputs with no reductions, so the results are
+ * identical to the serial build that the tests use.  The edge sort (qsort) stays serial. */
+#ifdef _OPENMP
+#include <omp.h>
+#define OM_PARALLEL_FOR _Pragma("omp parallel for schedule(static)")
+#else
+#define OM_PARALLEL_FOR
+#endif
+
+int om_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
+}
+
 /* ------------------------------------------------------------------------------------------ */
 static void set_err(char *err, int len, const char *fmt, ...) {
     if (!err || len <= 0) return;
@@ -379,6 +400,7 @@ static int level_cc(const om_mesh *in, const topo *T, om_mesh *out, char *err, i
     double *fp = out->pos + 3 * (size_t)V;                 /* face points  at V + r      */
     double *epnt = out->pos + 3 * ((size_t)V + F);         /* edge points  at V + F + e  */
     /* face points f_r = (1/c_r) sum of the face's vertices (Eq. spla_fp) */
+    OM_PARALLEL_FOR
     for (int32_t r = 0; r < F; ++r) {
         int32_t o = in->face_off[r], c = in->face_off[r + 1] - o;
         double acc[3] = {0, 0, 0};
@@ -387,6 +409,7 @@ static int level_cc(const om_mesh *in, const topo *T, om_mesh *out, char *err, i
         for (int d = 0; d < 3; ++d) fp[3 * r + d] = acc[d] / (double)c;
     }
     /* edge points e = 1/4 (p_k + p_l + f_r + f_s); boundary/crease rule */
+    OM_PARALLEL_FOR
     for (int32_t e = 0; e < E; ++e) {
         int32_t a = T->edge_lo[e], b = T->edge_hi[e];
         double smooth[3];
@@ -401,6 +424,7 @@ static int level_cc(const om_mesh *in, const topo *T, om_mesh *out, char *err, i
     }
     /* vertex points S(p) = (1 - 2/n) p + 1/n^2 sum p_j + 1/n^2 sum f_j (Eq. pos_update, P:L202-209,
      * split P:L332-357); n = number of incident faces (Eq. vo; reading R4).       */
+    OM_PARALLEL_FOR
     for (int32_t v = 0; v < V; ++v) {
         int32_t n = T->vs_off[v + 1] - T->vs_off[v];
         double smooth[3];
@@ -426,6 +450,7 @@ static int level_cc(const om_mesh *in, const topo *T, om_mesh *out, char *err, i
     /* topology: column r -> c_r quads (v_t, ep(v_t,v_t+1), fp_r, ep(v_t-1,v_t)) (R2) */
     out->face_off = xcalloc((size_t)Fn + 1, 4);
     out->face_vtx = xcalloc((size_t)4 * Fn, 4);
+    OM_PARALLEL_FOR
     for (int32_t r = 0; r < F; ++r) {
         int32_t o = in->face_off[r], c = in->face_off[r + 1] - o;
         for (int32_t t = 0; t < c; ++t) {
@@ -455,6 +480,7 @@ static int level_loop(const om_mesh *in, const topo *T, om_mesh *out, char *err,
     double *epnt = out->pos + 3 * (size_t)V;
     /* edge points: 3/8 (p_a + p_b) + 1/8 (p_G(a,b) + p_G(b,a)); G = vertex opposite the directed
      * edge (Eq. G); weights from Fig. loop_scheme (reading R11).  */
+    OM_PARALLEL_FOR
     for (int32_t e = 0; e < E; ++e) {
         int32_t a = T->edge_lo[e], b = T->edge_hi[e];
         double smooth[3];
@@ -469,6 +495,7 @@ static int level_loop(const om_mesh *in, const topo *T, om_mesh *out, char *err,
         edge_rule(T, P, e, smooth, epnt + 3 * (size_t)e);
     }
     /* vertex update S(p) = (1 - n beta) p + beta sum p_j (Eq. loop_smooth) */
+    OM_PARALLEL_FOR
     for (int32_t v = 0; v < V; ++v) {
         int32_t n = T->ve_off[v + 1] - T->ve_off[v];
         double smooth[3];
@@ -488,6 +515,7 @@ static int level_loop(const om_mesh *in, const topo *T, om_mesh *out, char *err,
     /* topology: (k, e_kl, e_mk), (l, e_lm, e_kl), (m, e_mk, e_lm), (e_kl, e_lm, e_mk) */
     out->face_off = xcalloc((size_t)Fn + 1, 4);
     out->face_vtx = xcalloc((size_t)3 * Fn, 4);
+    OM_PARALLEL_FOR
     for (int32_t r = 0; r < F; ++r) {
         int32_t o = in->face_off[r];
         int32_t ep[3];
@@ -520,6 +548,7 @@ static int level_sqrt3(const om_mesh *in, const topo *T, om_mesh *out, char *err
     out->V = (int32_t)Vn; out->F = (int32_t)Fn;
     out->pos = xcalloc((size_t)3 * Vn, sizeof(double));
     /* new vertex points: barycenters f = M^T P with (1,2,3) -> 1/3 */
+    OM_PARALLEL_FOR
     for (int32_t r = 0; r < F; ++r) {
         int32_t o = in->face_off[r];
         for (int d = 0; d < 3; ++d)
@@ -527,6 +556,7 @@ static int level_sqrt3(const om_mesh *in, const topo *T, om_mesh *out, char *err
                 (P[3 * in->face_vtx[o] + d] + P[3 * in->face_vtx[o + 1] + d] + P[3 * in->face_vtx[o + 2] + d]) / 3.0;
     }
     /* S(p) = (1 - alpha) p + alpha/n sum p_j (Eqs. sqrt2, alpha) */
+    OM_PARALLEL_FOR
     for (int32_t v = 0; v < V; ++v) {
         int32_t n = T->ve_off[v + 1] - T->ve_off[v];
         if (n == 0) { for (int d = 0; d < 3; ++d) out->pos[3 * (size_t)v + d] = P[3 * v + d]; continue; }
@@ -542,6 +572,7 @@ static int level_sqrt3(const om_mesh *in, const topo *T, om_mesh *out, char *err
      * (CCW order, reading R13)                                                  */
     out->face_off = xcalloc((size_t)Fn + 1, 4);
     out->face_vtx = xcalloc((size_t)3 * Fn, 4);
+    OM_PARALLEL_FOR
     for (int32_t r = 0; r < F; ++r) {
         int32_t o = in->face_off[r];
         for (int t = 0; t < 3; ++t) {

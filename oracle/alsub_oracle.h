@@ -54,6 +54,9 @@ void om_edges_free(om_edges *e);
 double om_loop_beta(int n);
 double om_sqrt3_alpha(int n);
 
+/* Threads of the OpenMP build (liboracle_omp.so); returns the count in use (1 in the serial build). */
+int om_set_threads(int n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,6 +8,8 @@ import sys
 
 import pytest
 
+import meshgen as mg
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -138,3 +140,21 @@ def test_bench_gpus_flag_spawns_ranks():
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["ranks"] == [0, 1] and line["pids"] == 2
     assert line["frames_gathered"] == 37 and line["frame_order_ok"]
+
+
+@pytest.mark.parametrize("scheme,mk", [("cc", lambda: mg.armor(4, 5, 6, 1, 1, 2, name="a")),
+                                       ("loop", lambda: mg.tetrahedron(creased=True)),
+                                       ("sqrt3", lambda: mg.torus_tris(8, 6))])
+def test_oracle_openmp_build_is_identical(scheme, mk):
+    """The all-cores oracle (liboracle_omp.so, bench.py's host baseline) marks only single-writer
+    per-element loops: its levels equal the serial oracle's bit for bit."""
+    import numpy as np
+    import oracle
+    mesh = mk()
+    t1, t2 = [], []
+    a = oracle.refine(mesh, scheme, 3, times=t1)
+    b = oracle.refine(mesh, scheme, 3, threads=4, times=t2)
+    assert len(t1) == len(t2) == 3
+    for x, y in zip(a, b):
+        for k in ("pos", "face_vtx", "face_off", "crease", "sigma"):
+            assert np.array_equal(x[k], y[k]), k
