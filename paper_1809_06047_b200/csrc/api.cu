@@ -535,6 +535,7 @@ static VSegs make_segs_s3(alsub_mesh *m, int l) {
     }
     g.nseg = n;
     g.vtx_off0 = m->b0.vtx_off; g.vtx_list0 = m->b0.vtx_slot; g.face_off0 = m->in_face_off;
+    g.long_list = m->b0.long_list; g.nlong = std::max(m->b0.nlong, 0);
     g.slot_face0 = m->b0.slot_face; g.vbnd0 = m->b0.vbnd;
     return g;
 }
@@ -555,6 +556,7 @@ static VSegs make_segs_loop(alsub_mesh *m, int l) {
     }
     g.nseg = n;
     g.vtx_off0 = m->b0.vtx_off; g.vtx_list0 = m->b0.vtx_slot; g.face_off0 = m->in_face_off;
+    g.long_list = m->b0.long_list; g.nlong = std::max(m->b0.nlong, 0);
     g.slot_face0 = m->b0.slot_face; g.vbnd0 = m->b0.vbnd;
     return g;
 }
@@ -581,6 +583,7 @@ static VSegs make_segs(alsub_mesh *m, int l) {
     g.nseg = n;
     g.hs_seg = l >= 2 ? n - 1 : -1;  // the last segment = edge points born at level l
     g.vtx_off0 = m->b0.vtx_off; g.vtx_list0 = m->b0.vtx_slot; g.face_off0 = m->in_face_off;
+    g.long_list = m->b0.long_list; g.nlong = std::max(m->b0.nlong, 0);
     g.slot_face0 = m->b0.slot_face; g.vbnd0 = m->b0.vbnd;
     return g;
 }

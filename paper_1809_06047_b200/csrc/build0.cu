@@ -97,7 +97,7 @@ __global__ void k_edge_count(const int32_t *__restrict__ face_vtx, const int32_t
     if (j >= V) return;
     const int32_t o0 = vtx_off[j], n = vtx_off[j + 1] - o0;
     int32_t *row = const_cast<int32_t *>(vtx_slot) + o0;
-    if (n <= 16) {
+    if (n <= kLongRow) {
         // sort the row by slot: lane q moves its slot to its rank (slots are distinct)
         const int32_t sq = lane < n ? row[lane] : INT32_MAX;
         int32_t rank = 0;
@@ -144,7 +144,7 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
     if (j >= V) return;
     const int32_t o0 = vtx_off[j], n = vtx_off[j + 1] - o0;
     if (lane == 0) slot0[j] = n > 0 ? vtx_slot[o0] : -1;
-    if (n <= 16) {
+    if (n <= kLongRow) {
         const WarpCand c = warp_cand(face_vtx, vtx_slot, tp, o0, n, lane);
         const bool mine = c.first && (uint32_t)c.x < (uint32_t)j;
         int32_t rank = 0;

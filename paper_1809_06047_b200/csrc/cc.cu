@@ -655,15 +655,27 @@ ALSUB_D void cc_vertex_smooth(const VtxCtx<ORDER> &x, const Frames &fr, const VS
 
 // a long level-0 ring (n > kLongRing, not boundary, not special), summed by the whole warp; the
 // same two forms as cc_vertex_smooth: c0 corner sums (levels >= 1) or slot gathers (level 0)
-template <int ORDER>
+// level-0 vertex j is summed by k_cc_vertex_long: a long M^T row (the build's list, n > 16), not on
+// a boundary, not special (those keep the per-lane path)
 ALSUB_D bool cc_long_ring(const VSegs &g, const LevelDev &p, int32_t j, bool cr) {
     const int32_t n = __ldg(g.vtx_off0 + j + 1) - __ldg(g.vtx_off0 + j);
-    if (n <= kLongRing || __ldg(g.vbnd0 + j)) return false;
+    if (n <= kLongRow || __ldg(g.vbnd0 + j)) return false;
     return !(cr && p.sv_off[j + 1] > p.sv_off[j]);
 }
 
-template <int ORDER>
-ALSUB_D void cc_vertex_long(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs &g, int32_t j, int lane) {
+// The long rings, a warp per listed vertex (only launched when the mesh has long rows): kept out
+// of k_cc_vertex, whose registers an inlined (or called) 8-wide gather loop raised from 40 to 64
+// (config 3 0.685 -> 0.704 ms).  Same two forms as cc_vertex_smooth: c0 corner sums (levels >= 1)
+// or slot gathers (level 0); lanes take slots k = lane, lane + 32, ..., warp_sum reduces.
+template <int ORDER, bool CR>
+__global__ void __launch_bounds__(kThreads) k_cc_vertex_long(LevelDev p, Frames fr, VSegs g) {
+    ALSUB_GRID_WAIT();
+    const int32_t w = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (w >= g.nlong) return;
+    const int32_t j = __ldg(g.long_list + w);
+    if (!cc_long_ring(g, p, j, CR)) return;
+    const Topo<ORDER> tl{p.face_off, p.slot_face};
     const int shift = 2 * g.level;
     const int32_t o = __ldg(g.vtx_off0 + j), cnt = __ldg(g.vtx_off0 + j + 1) - o;
     const bool c0p = fr.c0 && shift >= 2;
@@ -680,12 +692,12 @@ ALSUB_D void cc_vertex_long(const VtxCtx<ORDER> &x, const Frames &fr, const VSeg
                 for (int u = 0; u < 8; ++u)
                     if (b[u] >= 0) acc = acc + ld3c(fr.c0r(f), b[u] << (shift - 2));
             } else {
-                int32_t nb[8];
+                int32_t nbr[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) nb[u] = b[u] >= 0 ? __ldg(x.face_vtx + x.tl.next(b[u] << shift)) : -1;
+                for (int u = 0; u < 8; ++u) nbr[u] = b[u] >= 0 ? __ldg(p.face_vtx + tl.next(b[u] << shift)) : -1;
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
-                    if (b[u] >= 0) acc = acc + ld3(fr.rd(f), nb[u]) + ld3c(fr.wr(f), x.V + x.tl.face(b[u] << shift));
+                    if (b[u] >= 0) acc = acc + ld3(fr.rd(f), nbr[u]) + ld3c(fr.wr(f), p.V + tl.face(b[u] << shift));
             }
         }
         acc = warp_sum(acc);
@@ -752,11 +764,10 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
             }
             continue;
         }
-        unsigned longm = 0;  // long level-0 rings of this lane, done cooperatively below
         for (int k = 0; k < PL; ++k) {
             const int32_t j = j0 + 32 * k;
             if (j >= len) continue;
-            if (g.type[s] == 0 && cc_long_ring<ORDER>(g, p, j, CR)) { longm |= 1u << k; continue; }
+            if (g.nlong > 0 && g.type[s] == 0 && cc_long_ring(g, p, j, CR)) continue;  // k_cc_vertex_long
             if (s == g.gp_skip_seg) {
                 // done by k_cc_edge_gp when the 4 child edges of interior edge j (ids base ..
                 // base + 3) are in one of its blocks
@@ -767,16 +778,6 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
                 }
             }
             cc_vertex_one<ORDER, CR>(x, fr, g, p, csv_list, s, j);
-        }
-        if (g.type[s] == 0) {  // warp-uniform: the task lies in one segment
-            for (int k = 0; k < PL; ++k) {
-                unsigned m = __ballot_sync(0xffffffffu, (longm >> k) & 1u);
-                while (m) {
-                    const int src = __ffs(m) - 1;
-                    m &= m - 1;
-                    cc_vertex_long<ORDER>(x, fr, g, j0 - lane + src + 32 * k, lane);
-                }
-            }
         }
     }
 }
@@ -860,12 +861,14 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, b
     if (p.V > 0) {
         // 32-vertex warp tasks; >= 2 waves of 148 SMs for small levels, 4 tasks per warp for large
         // ones (128-vertex tasks with batched loads were measured slower)
-        if (false) {
-        } else {
-            const unsigned nblk = (unsigned)std::max<int64_t>(grid_for(p.V, 4 * kThreads),
-                                                              std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
-            if (p.crease) launch(L, "cc_vertex", k_cc_vertex<ORDER == 4 ? 4 : 0, 1, true>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g, c.sv_list);
-            else launch(L, "cc_vertex", k_cc_vertex<ORDER == 4 ? 4 : 0, 1, false>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g, c.sv_list);
+        const unsigned nblk = (unsigned)std::max<int64_t>(grid_for(p.V, 4 * kThreads),
+                                                          std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
+        if (p.crease) launch(L, "cc_vertex", k_cc_vertex<ORDER == 4 ? 4 : 0, 1, true>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g, c.sv_list);
+        else launch(L, "cc_vertex", k_cc_vertex<ORDER == 4 ? 4 : 0, 1, false>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g, c.sv_list);
+        if (g.nlong > 0) {  // the poles' rings (reads what the vertex kernel reads, writes disjoint ids)
+            const unsigned gl = grid_for(32 * (int64_t)g.nlong);
+            if (p.crease) launch(L, "cc_vertex_long", k_cc_vertex_long<ORDER, true>, dim3(gl), dim3(kThreads), 0, s, p, fr, g);
+            else launch(L, "cc_vertex_long", k_cc_vertex_long<ORDER, false>, dim3(gl), dim3(kThreads), 0, s, p, fr, g);
         }
     }
     if (fork) {

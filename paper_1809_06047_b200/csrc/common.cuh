@@ -139,6 +139,7 @@ ALSUB_D float ord2f(int32_t i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffff
 // lanes take slots k = lane, lane + 32, ...; warp_sum is a fixed xor butterfly, so the result is
 // deterministic (and identical between refine and eval_frames, which share the kernels).
 constexpr int32_t kLongRing = 32;
+constexpr int32_t kLongRow = 16;  // M^T rows longer than this are listed by the level-0 build
 ALSUB_D P3 warp_sum(P3 a) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

@@ -284,6 +284,10 @@ struct VSegs {
     int8_t birth[kMaxSeg];  // level m at which the vertex was created
     const int2 *ehh[kMaxLevels];  // ehh[m-1] = edge pairs of level m-1
     const int32_t *vtx_off0, *vtx_list0, *face_off0, *slot_face0, *vbnd0;
+    // level-0 vertices with long M^T rows (> kLongRow slots; the build's list): CC sums their rings
+    // in k_cc_vertex_long
+    const int32_t *long_list = nullptr;
+    int32_t nlong = 0;
     int32_t hs_seg;  // segment whose vertex points come from the half sums (-1 = none)
     // sqrt3: slot multiplier 3^(l-m) per segment and the level m-1 face rows
     int32_t mult[kMaxSeg];

@@ -247,10 +247,9 @@ ALSUB_D void rb_fold(SummaryRec &r, int32_t ra, int32_t rb, const float (&a)[3],
     unsigned long long sum = 0ull;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const int32_t qa = ra >= 0 ? f2ord(a[c]) : INT32_MAX, qb = rb >= 0 ? f2ord(b[c]) : INT32_MAX;
-        const int32_t pa = ra >= 0 ? f2ord(a[c]) : INT32_MIN, pb = rb >= 0 ? f2ord(b[c]) : INT32_MIN;
-        lo[c] = min(qa, qb);
-        hi[c] = max(pa, pb);
+        const int32_t oa = f2ord(a[c]), ob = f2ord(b[c]);
+        lo[c] = min(ra >= 0 ? oa : INT32_MAX, rb >= 0 ? ob : INT32_MAX);
+        hi[c] = max(ra >= 0 ? oa : INT32_MIN, rb >= 0 ? ob : INT32_MIN);
         if (ra >= 0) sum += (unsigned long long)(uint32_t)__float_as_int(a[c]) * (unsigned long long)(6ll * ra + 2 * c + 1);
         if (rb >= 0) sum += (unsigned long long)(uint32_t)__float_as_int(b[c]) * (unsigned long long)(6ll * rb + 2 * c + 1);
     }
