@@ -4,6 +4,7 @@
 // (non-zeros of C); boundary edges are treated as infinitely sharp creases (reading R6).
 // The whole module -- edge overrides, vertex overrides, crease inheritance -- is one
 // gather kernel per level over the special-edge list and the special-vertex CSR (common.cuh).
+#include "crease_fused.cuh"
 #include "internal.h"
 
 namespace alsub {
@@ -29,21 +30,6 @@ struct CreaseArgs {
     int32_t scheme;   // 0 CC (child ids from the boundary prefix), 1 Loop (loop_base)
     int32_t inherit;  // build the child special lists
 };
-
-// mean of the OTHER finite non-boundary creases at special vertex ix (excluding entry j)
-__device__ __forceinline__ float sigma_bar(const LevelDev &p, int32_t ix, int32_t j, float se) {
-    float sum = 0.0f;
-    int n = 0;
-    for (int32_t q = p.sv_off[ix]; q < p.sv_off[ix + 1]; ++q) {
-        const int32_t k = p.sv_list[q];
-        if (k == j) continue;
-        const SpEdge o = p.sp[k];
-        if (!(o.sigma > 0.0f) || is_inf(o.sigma) || (o.flags & kSpBoundary)) continue;
-        sum += o.sigma;
-        ++n;
-    }
-    return n > 0 ? sum / (float)n : se;
-}
 
 __global__ void __launch_bounds__(kThreads) k_crease(CreaseArgs A) {
     ALSUB_GRID_WAIT();

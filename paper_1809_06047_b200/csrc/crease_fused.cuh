@@ -29,8 +29,9 @@ ALSUB_D P3 crease_edge_point(float sg, P3 smooth, P3 mid) {
     return smooth;
 }
 
-// mean of the OTHER finite non-boundary creases at special vertex ix (reading R8)
-ALSUB_D float fused_sigma_bar(const LevelDev &p, int32_t ix, int32_t j, float se) {
+// mean of the OTHER finite non-boundary creases at special vertex ix (reading R8); shared by the
+// fused crease rules and the separate crease pass (crease.cu)
+ALSUB_D float sigma_bar(const LevelDev &p, int32_t ix, int32_t j, float se) {
     float sum = 0.0f;
     int n = 0;
     for (int32_t q = p.sv_off[ix]; q < p.sv_off[ix + 1]; ++q) {
@@ -54,8 +55,8 @@ ALSUB_D void fused_inherit(const LevelDev &p, const ChildDev &c, int32_t j, cons
         if ((se.flags & kSpBoundary) || isinf(se.sigma)) {
             ca = cb = se.sigma;
         } else {
-            ca = fmaxf(0.25f * (fused_sigma_bar(p, se.ia, j, se.sigma) + 3.0f * se.sigma) - 1.0f, 0.0f);
-            cb = fmaxf(0.25f * (fused_sigma_bar(p, se.ib, j, se.sigma) + 3.0f * se.sigma) - 1.0f, 0.0f);
+            ca = fmaxf(0.25f * (sigma_bar(p, se.ia, j, se.sigma) + 3.0f * se.sigma) - 1.0f, 0.0f);
+            cb = fmaxf(0.25f * (sigma_bar(p, se.ib, j, se.sigma) + 3.0f * se.sigma) - 1.0f, 0.0f);
         }
     }
     const int32_t iep = p.nsv + j;
