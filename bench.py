@@ -193,6 +193,31 @@ def shard(n, world, rank):
     return lo, lo + per + (1 if rank < extra else 0)
 
 
+def bench_backend():
+    """Process-group backend of the multi-rank bench: NCCL (the product path).  ALSUB_BENCH_BACKEND=gloo
+    runs the same multi-rank code with gloo and host-side collectives, e.g. two ranks sharing one
+    GPU (NCCL refuses duplicate devices) to exercise the N > 1 paths where only one GPU exists."""
+    return os.environ.get("ALSUB_BENCH_BACKEND", "nccl")
+
+
+def coll_device(dev):
+    """Device of the collectives' tensors: the GPU for NCCL, the host for gloo."""
+    import torch
+    return dev if bench_backend() == "nccl" else torch.device("cpu")
+
+
+def init_dist(local):
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    if bench_backend() == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(bench_backend())
+    return dev
+
+
 def dist_max(x, device=None):
     """Max of a scalar over all ranks (timing only; no data-path collective)."""
     import torch
@@ -212,7 +237,7 @@ def gather_summaries(local, nframes, world, rank, device=None):
     import torch.distributed as dist
     per_max = max(hi - lo for lo, hi in (shard(nframes, world, r) for r in range(world)))
     buf = torch.zeros((per_max, 8), dtype=torch.int32, device=device)
-    buf[:local.shape[0]] = local
+    buf[:local.shape[0]] = local.to(buf.device)
     if world == 1 or not (dist.is_available() and dist.is_initialized()):
         return buf[:nframes]
     out = torch.empty((world * per_max, 8), dtype=torch.int32, device=device)
@@ -328,17 +353,19 @@ def run_alsub(args):
     from paper_1809_06047_b200 import Mesh
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+        dev = init_dist(local)
+    else:
+        dev = torch.device("cuda", local)
+        torch.cuda.set_device(dev)
+    cdev = coll_device(dev)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     def max_over_ranks(x):
-        return dist_max(x, dev)
+        return dist_max(x, cdev)
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     peak, peak_src = peaks()
@@ -380,7 +407,7 @@ def run_alsub(args):
     torch.cuda.synchronize()
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     barrier()
     torch.cuda.synchronize()
     with sampler:
@@ -658,7 +685,7 @@ def run_frames(args, rank, world, dev, barrier, max_over_ranks, peak, peak_src):
         for i in range(nbatch):
             batch(i)
         eg.record(stream)
-        table = gather_summaries(summ[:per_rank], nframes, world, rank, device=dev)
+        table = gather_summaries(summ[:per_rank], nframes, world, rank, device=coll_device(dev))
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -708,7 +735,7 @@ def run_frames(args, rank, world, dev, barrier, max_over_ranks, peak, peak_src):
                                     "row ids once per batch of 32", "peak_source": peak_src},
                "per_gpu_hbm_frac": per_gpu_gbps / peak if per_gpu_gbps else None,
                "summaries": {"frames_gathered": int(table.shape[0]), "bytes_per_frame": 32,
-                             "collective": "all_gather_into_tensor (NCCL)" if world > 1 else "none (1 rank)",
+                             "collective": f"all_gather_into_tensor ({bench_backend()})" if world > 1 else "none (1 rank)",
                              "gather_ms": gather_ms, "fused_into_eval": True,
                              "equal_to_alsub_frame_summary": records_ok},
                "gpu_launches": int(m.last_launch_count * nbatch), "clocks": sampler.summary(),
@@ -722,13 +749,14 @@ def run_frames_line(args):
     import torch
     import torch.distributed as dist
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dev = init_dist(local)
+    else:
+        dev = torch.device("cuda", local)
+        torch.cuda.set_device(dev)
     peak, peak_src = peaks()
     fr = run_frames(args, rank, world, dev, (lambda: dist.barrier()) if world > 1 else (lambda: None),
-                    lambda x: dist_max(x, dev), peak, peak_src)
+                    lambda x: dist_max(x, coll_device(dev)), peak, peak_src)
     if rank == 0:
         line = {"metric": METRIC, "value": fr["value"], "unit": "faces/s", "n_gpus": world, "steps": 1,
                 "warmup": args.warmup, "ms_per_step": fr["ms"], "higher_is_better": True, "scaling": "strong",
