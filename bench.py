@@ -456,6 +456,9 @@ def run_alsub(args):
                 if nc and mb:  # ncu DRAM bytes of the same launch (profiles/ncu_summary.json)
                     kk[n]["dram_bytes"] = nc["dram_bytes"]
                     kk[n]["waste"] = nc["dram_bytes"] / mb  # DRAM traffic / method bytes
+                    # the HBM the kernel actually keeps busy: its DRAM bytes over this run's time
+                    kk[n]["dram_GBps"] = nc["dram_bytes"] / (t * 1e6)
+                    kk[n]["dram_frac"] = kk[n]["dram_GBps"] / peak
             row["kernels"] = kk
         per_level.append(row)
     db = kernel_bytes_cc(dname, cnt[dlvl], cnt[dlvl - 1] if dlvl > 0 else None, dlvl, levels,
