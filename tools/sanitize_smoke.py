@@ -37,5 +37,31 @@ with Mesh(tor["face_off"], tor["face_vtx"], tor["pos"]) as m:
     m.refine("sqrt3", 3)
     m.eval_frames(torch.from_numpy(tor["pos"])[None].cuda(), 3)
 pv, pf = rcm_order(arm["face_off"], arm["face_vtx"], arm["pos"].shape[0])
+# round 2: long M^T rows (block sort in registers, and the global-memory network past 1024 slots),
+# the poles' ring kernels of every scheme, the blocked matrix with fused records (ragged batch,
+# wide supports), isolated control vertices, the single-sync create on invalid input
+for n, scheme in ((300, "cc"), (300, "loop"), (300, "sqrt3"), (1500, "cc")):
+    bp = mg.bipyramid(n)
+    with Mesh(bp["face_off"], bp["face_vtx"], bp["pos"]) as m:
+        m.refine(scheme, 2)
+        m.refine(scheme, 2)
+for mk, scheme, L in ((lambda: mg.bipyramid(30), "loop", 2), (lambda: arm, "cc", 3)):
+    mm = mk()
+    with Mesh(mm["face_off"], mm["face_vtx"], mm["pos"], mm["crease"], mm["sigma"]) as m:
+        m.refine(scheme, L)
+        m.build_refinement_matrix(L)
+        f = torch.from_numpy(np.stack([mm["pos"]] * 37)).cuda()
+        m.eval_frames_matrix_summary(f)
+iso = mg._pack([(0, 1, 2, 3)], [(0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (5, 5, 5)])
+with Mesh(iso["face_off"], iso["face_vtx"], iso["pos"]) as m:
+    m.refine("cc", 3)
+    m.build_refinement_matrix(3)
+    m.eval_frames_matrix(torch.from_numpy(iso["pos"])[None].cuda())
+from paper_1809_06047_b200 import AlsubError  # noqa: E402
+for faces in ([(0, 1, 7)], [(0, 1, 2), (0, 1, 3)], [(0, 1, 2), (1, 0, 3), (0, 1, 4)]):
+    try:
+        Mesh(*[mg._pack(faces, np.zeros((5, 3), np.float32))[k] for k in ("face_off", "face_vtx", "pos")])
+    except AlsubError:
+        pass
 torch.cuda.synchronize()
 print("sanitize smoke ok")
