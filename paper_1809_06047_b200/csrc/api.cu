@@ -93,6 +93,10 @@ struct alsub_mesh {
     float *c0 = nullptr;          // corner-0 contributions (CC, levels >= 1), [3 * max F_l] floats
     int64_t c0_elems = 0;
     float *frame_c0 = nullptr;
+    // last level >= 3 (CC): straddling edge-point groups of the grandparent edge kernel (Frames.gside)
+    float *gside = nullptr, *frame_gside = nullptr;
+    int32_t *gvid = nullptr;
+    int32_t gblk = 0;  // grandparent edge blocks
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
     void *scratch_create = nullptr;
@@ -455,6 +459,17 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
     if (scheme == ALSUB_CATMULL_CLARK)
         for (int l = 1; l < levels; ++l) m->c0_elems = std::max<int64_t>(m->c0_elems, 3 * lv[l].F);
     m->c0 = m->c0_elems ? A<float>(m, m->c0_elems, s, ML, ok) : nullptr;
+    m->gblk = 0;
+    m->gside = nullptr;
+    m->gvid = nullptr;
+    if (scheme == ALSUB_CATMULL_CLARK && levels >= 4) {  // compact c0 + straddling groups (cc.cu)
+        m->gblk = (int32_t)grid_for(lv[levels - 2].E);
+        m->gside = A<float>(m, 12 * (int64_t)m->gblk, s, ML, ok);
+        m->gvid = A<int32_t>(m, m->gblk, s, ML, ok);
+        // the straddling groups are fixed by the topology: every run writes the same entries, so
+        // the -1 of the other blocks is set once
+        if (m->gvid) cudaMemsetAsync(m->gvid, 0xff, sizeof(int32_t) * m->gblk, s);
+    }
     m->b0.sv_vtx = m->sv_vtx;
     m->b0.sv_off = m->sv_off;
     int64_t max_scan = std::max<int64_t>(m->V0, m->S0) + 1;
@@ -671,6 +686,12 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
             // crease module fused into the level kernels on small levels (the latency of a separate
             // pass dominates there), a separate kernel on large ones (fusion costs occupancy)
             p.crease = (special && !use_gp && P.V < kFuseCreaseMaxV) ? 1 : 0;
+            if (use_gp && l >= 3 && m->gside) {  // compact corner sums + straddling groups
+                fr.c0shift = 2;
+                fr.gside = m->gside;
+                fr.gvid = m->gvid;
+                fr.gsidestride = 12 * (int64_t)m->gblk;
+            }
             cc_level(p, c, fr, true, adj, g, use_gp ? &gp : nullptr, s, L);
             if (special && !p.crease) {
                 if (!adj) m->lazy_lists = true;  // last level: lists built on demand
@@ -1063,8 +1084,15 @@ static void static_level(alsub_mesh *m, int l, const Frames &fr, cudaStream_t s,
             g.len[g.hs_seg] = 0;  // the edge kernel smooths the edge points born at level l
         }
         p.crease = (special && !use_gp && Pl.V < kFuseCreaseMaxV) ? 1 : 0;
-        cc_level(p, c, fr, false, false, g, use_gp ? &gp : nullptr, s, L);
-        if (special && !p.crease) crease_level(p, c, fr, (int32_t)(Pl.V + Pl.F), 0, false, s, L);
+        Frames fx = fr;
+        if (use_gp && l >= 3 && m->gside) {  // compact corner sums + straddling groups
+            fx.c0shift = 2;
+            fx.gside = fr.nb == 1 ? m->gside : m->frame_gside;
+            fx.gvid = m->gvid;
+            fx.gsidestride = 12 * (int64_t)m->gblk;
+        }
+        cc_level(p, c, fx, false, false, g, use_gp ? &gp : nullptr, s, L);
+        if (special && !p.crease) crease_level(p, c, fx, (int32_t)(Pl.V + Pl.F), 0, false, s, L);
     } else if (scheme == ALSUB_LOOP) {
         VSegs g = make_segs_loop(m, l);
         loop_level(p, c, fr, false, false, nullptr, nullptr, g, s, L, special ? 0 : -1);
@@ -1381,6 +1409,7 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
             m->frame_buf[l] = A<float>(m, 3 * m->lv[l].V * nb, s, m->mem_frames, ok);
         m->frame_hs = m->hs_elems ? A<float>(m, m->hs_elems * nb, s, m->mem_frames, ok) : nullptr;
         m->frame_c0 = m->c0_elems ? A<float>(m, m->c0_elems * nb, s, m->mem_frames, ok) : nullptr;
+        m->frame_gside = m->gblk ? A<float>(m, 12 * (int64_t)m->gblk * nb, s, m->mem_frames, ok) : nullptr;
         if (!ok) return fail(ALSUB_E_NOMEM, "frame batch buffers");
         m->frames_nb = nb;
     }

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev 
         const P3 p0 = ld3(P, v[0]), p1 = ld3(P, v[1]), p2 = ld3(P, v[2]), p3 = ld3(P, v[3]);
         const P3 fc = 0.25f * (p0 + p1 + p2 + p3);
         if (valid) st3(Pn, V + r, fc);
-        if (valid && fr.c0) st3(fr.c0w(f), r, p1 + fc);
+        if (valid && fr.c0 && (r & ((1 << fr.c0shift) - 1)) == 0) st3(fr.c0w(f), r >> fr.c0shift, p1 + fc);
         if (fpo >= 0) {
             P3 acc = p1 + fc;
             acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 4);
@@ -410,6 +410,16 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
                     s_ring[0][threadIdx.x] = rt.x;
                     s_ring[1][threadIdx.x] = rt.y;
                     s_ring[2][threadIdx.x] = rt.z;
+                    if (fr.gside) {  // a group across two blocks: its terms for k_cc_straddle
+                        const int32_t k = e - 4 * (hi - epo) + (bp >> 1), e0 = e - k;
+                        if ((e0 & (kThreads - 1)) > kThreads - 4) {
+                            float *gs = fr.gside + f * fr.gsidestride + 12 * (int64_t)(e0 / kThreads) + 3 * k;
+                            gs[0] = rt.x;
+                            gs[1] = rt.y;
+                            gs[2] = rt.z;
+                            if (k == 0 && f == 0) fr.gvid[e0 / kThreads] = hi;
+                        }
+                    }
                 }
             }
 
@@ -512,11 +522,12 @@ ALSUB_D void copy_point(const Frames &fr, int32_t v, const VCr &cr) {
 template <int N>
 ALSUB_D void smooth_c0(const Frames &fr, int32_t v, const int32_t (&q)[N], const VCr &cr) {
     constexpr float inv = 1.0f / (float)N;
+    const int cs = fr.c0shift;
     for (int f = 0; f < fr.nb; ++f) {
         const PR c0 = fr.c0r(f);
-        P3 acc = ld3c(c0, q[0]);
+        P3 acc = ld3c(c0, q[0] >> cs);
 #pragma unroll
-        for (int k = 1; k < N; ++k) acc = acc + ld3c(c0, q[k]);
+        for (int k = 1; k < N; ++k) acc = acc + ld3c(c0, q[k] >> cs);
         emit_vertex(fr, f, v, cr, (1.0f - 2.0f * inv) * ld3(fr.rd(f), v) + (inv * inv) * acc);
     }
 }
@@ -614,7 +625,7 @@ ALSUB_D void cc_vertex_smooth(const VtxCtx<ORDER> &x, const Frames &fr, const VS
                 P3 acc = p3zero();
                 for (int32_t k = 0; k < cnt; ++k) {
                     const int32_t b = lv0 ? __ldg(g.vtx_list0 + o + k) : 4 * (o + k) + 2;
-                    acc = acc + ld3c(c0, b << fs);
+                    acc = acc + ld3c(c0, (b << fs) >> fr.c0shift);
                 }
                 const P3 pv = ld3(fr.rd(f), v);
                 if (cnt == 0) { st3(fr.wr(f), v, pv); continue; }
@@ -690,7 +701,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex_long(LevelDev p, Frames 
             if (c0p) {
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
-                    if (b[u] >= 0) acc = acc + ld3c(fr.c0r(f), b[u] << (shift - 2));
+                    if (b[u] >= 0) acc = acc + ld3c(fr.c0r(f), (b[u] << (shift - 2)) >> fr.c0shift);
             } else {
                 int32_t nbr[8];
 #pragma unroll
@@ -770,9 +781,11 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
             if (g.nlong > 0 && g.type[s] == 0 && cc_long_ring(g, p, j, CR)) continue;  // k_cc_vertex_long
             if (s == g.gp_skip_seg) {
                 // done by k_cc_edge_gp when the 4 child edges of interior edge j (ids base ..
-                // base + 3) are in one of its blocks
+                // base + 3) are in one of its blocks, and by k_cc_straddle (gside) when they
+                // straddle two
                 const int m1 = g.birth[s] - 1;
                 if (__ldg(g.ehh[m1] + j).y >= 0) {
+                    if (fr.gside) continue;
                     const int32_t base = 4 * j - (g.bw[m1] ? bprefix(g.bw[m1], g.bwp[m1], j) : 0);
                     if ((base & (kThreads - 1)) <= kThreads - 4) continue;
                 }
@@ -783,6 +796,23 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
 }
 
 // ------------------------------------------------------------------------------------------
+// the edge points born at l-1 whose group of four grandparent edges straddles two blocks of
+// k_cc_edge_gp: S(x) = 1/2 p_x + 1/16 sum_k (p_ep_k + 1/2 (f_a,k + f_b,k)) from the four terms the
+// two blocks left in gside (one group per block boundary at most)
+__global__ void __launch_bounds__(kThreads) k_cc_straddle(Frames fr, int32_t nblk) {
+    ALSUB_GRID_WAIT();
+    const int32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nblk) return;
+    const int32_t x = fr.gvid[b];
+    if (x < 0) return;
+    for (int f = 0; f < fr.nb; ++f) {
+        const float *gs = fr.gside + f * fr.gsidestride + 12 * (int64_t)b;
+        const P3 acc{(gs[0] + gs[3]) + (gs[6] + gs[9]), (gs[1] + gs[4]) + (gs[7] + gs[10]),
+                     (gs[2] + gs[5]) + (gs[8] + gs[11])};
+        st3(fr.wr(f), x, 0.5f * ld3(fr.rd(f), x) + 0.0625f * acc);
+    }
+}
+
 template <int ORDER, bool ADJ, bool BND>
 static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, bool topo, const VSegs &g0,
                       const LevelDev *gp, cudaStream_t s, Launches &L) {
@@ -803,6 +833,7 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, b
     // block sums (the face points born at l-1 from the face kernel's shuffle, above); the older
     // vertices sum their faces' corner sums c0 (dropping c0 at this level and gathering their rings
     // directly was measured slower: 0.715 -> 0.731 ms on config 3)
+    // last level >= 3: compact corner sums (fr.c0shift, set by the caller with the buffers)
     const Frames &fr = fr0;
     int32_t epo = -1;
     if (gp) {
@@ -874,6 +905,10 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, b
     if (fork) {
         cudaEventRecord(L.ev_join, L.side);
         cudaStreamWaitEvent(s, L.ev_join, 0);
+    }
+    if (gp && gp->E > 0 && fr.gside) {  // after the edge kernel (it wrote the straddling groups' terms)
+        const int32_t nblk = (int32_t)grid_for(gp->E);
+        launch(L, "cc_straddle", k_cc_straddle, dim3(grid_for(nblk)), dim3(kThreads), 0, s, fr, nblk);
     }
 }
 

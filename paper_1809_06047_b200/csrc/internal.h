@@ -261,6 +261,16 @@ struct Frames {
     // written by the face kernel; every vertex born before this level sums its faces' c0
     float *c0 = nullptr;
     int64_t c0stride = 0;
+    // the last refined level (>= 3) keeps only the corner sums it reads -- faces r = 0 mod 4, whose
+    // corner 0 is a vertex born before level l-1 -- compacted at r >> 2 (c0shift = 2): full 96-B
+    // runs per warp instead of 12-B stores of every face
+    int32_t c0shift = 0;
+    // last level: the ring terms of the edge-point groups that straddle two blocks of the
+    // grandparent edge kernel, [edge block][4][3] + the group's vertex id per block (gvid, -1 =
+    // none); finished by k_cc_straddle after the edge kernel
+    float *gside = nullptr;
+    int32_t *gvid = nullptr;
+    int64_t gsidestride = 0;
     // per-frame views ([V][3], vertex stride 3)
     ALSUB_HD PR rd(int f) const { return PR{P + f * Pstride, 3}; }
     ALSUB_HD PW wr(int f) const { return PW{Pn + f * Pnstride, 3}; }
