@@ -95,7 +95,7 @@ struct alsub_mesh {
     float *frame_c0 = nullptr;
     // last level >= 3 (CC): straddling edge-point groups of the grandparent edge kernel (Frames.gside)
     float *gside = nullptr, *frame_gside = nullptr;
-    int32_t *gvid = nullptr;
+    int32_t *gcnt = nullptr, *frame_gcnt = nullptr;
     int32_t gblk = 0;  // grandparent edge blocks
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -461,14 +461,13 @@ static alsub_status make_plan(alsub_mesh *m, int scheme, int levels, cudaStream_
     m->c0 = m->c0_elems ? A<float>(m, m->c0_elems, s, ML, ok) : nullptr;
     m->gblk = 0;
     m->gside = nullptr;
-    m->gvid = nullptr;
+    m->gcnt = nullptr;
     if (scheme == ALSUB_CATMULL_CLARK && levels >= 4) {  // compact c0 + straddling groups (cc.cu)
         m->gblk = (int32_t)grid_for(lv[levels - 2].E);
         m->gside = A<float>(m, 12 * (int64_t)m->gblk, s, ML, ok);
-        m->gvid = A<int32_t>(m, m->gblk, s, ML, ok);
-        // the straddling groups are fixed by the topology: every run writes the same entries, so
-        // the -1 of the other blocks is set once
-        if (m->gvid) cudaMemsetAsync(m->gvid, 0xff, sizeof(int32_t) * m->gblk, s);
+        m->gcnt = A<int32_t>(m, m->gblk, s, ML, ok);
+        // zero once: the block that finishes a straddling group resets its counter
+        if (m->gcnt) cudaMemsetAsync(m->gcnt, 0, sizeof(int32_t) * m->gblk, s);
     }
     m->b0.sv_vtx = m->sv_vtx;
     m->b0.sv_off = m->sv_off;
@@ -689,7 +688,7 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
             if (use_gp && l >= 3 && m->gside) {  // compact corner sums + straddling groups
                 fr.c0shift = 2;
                 fr.gside = m->gside;
-                fr.gvid = m->gvid;
+                fr.gcnt = m->gcnt;
                 fr.gsidestride = 12 * (int64_t)m->gblk;
             }
             cc_level(p, c, fr, true, adj, g, use_gp ? &gp : nullptr, s, L);
@@ -1088,7 +1087,7 @@ static void static_level(alsub_mesh *m, int l, const Frames &fr, cudaStream_t s,
         if (use_gp && l >= 3 && m->gside) {  // compact corner sums + straddling groups
             fx.c0shift = 2;
             fx.gside = fr.nb == 1 ? m->gside : m->frame_gside;
-            fx.gvid = m->gvid;
+            fx.gcnt = fr.nb == 1 ? m->gcnt : m->frame_gcnt;
             fx.gsidestride = 12 * (int64_t)m->gblk;
         }
         cc_level(p, c, fx, false, false, g, use_gp ? &gp : nullptr, s, L);
@@ -1410,6 +1409,8 @@ extern "C" alsub_status alsub_eval_frames(alsub_mesh *m, int32_t levels, const f
         m->frame_hs = m->hs_elems ? A<float>(m, m->hs_elems * nb, s, m->mem_frames, ok) : nullptr;
         m->frame_c0 = m->c0_elems ? A<float>(m, m->c0_elems * nb, s, m->mem_frames, ok) : nullptr;
         m->frame_gside = m->gblk ? A<float>(m, 12 * (int64_t)m->gblk * nb, s, m->mem_frames, ok) : nullptr;
+        m->frame_gcnt = m->gblk ? A<int32_t>(m, m->gblk, s, m->mem_frames, ok) : nullptr;
+        if (m->frame_gcnt) cudaMemsetAsync(m->frame_gcnt, 0, sizeof(int32_t) * m->gblk, s);
         if (!ok) return fail(ALSUB_E_NOMEM, "frame batch buffers");
         m->frames_nb = nb;
     }

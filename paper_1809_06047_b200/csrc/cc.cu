@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
 // does the few groups that straddle a block boundary, and boundary e'').
 template <int NBC>
 __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp, ChildDev c, Frames fr,
-                                                       int32_t epo) {
+                                                       int32_t epo, const int2 *ehh2) {
     ALSUB_GRID_WAIT();
     // the block's children are the contiguous id range [base(e_first), base(e_last) + nch): staged
     // in shared memory and written back as one coalesced float run.  Staging is one array per
@@ -376,7 +376,21 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
     __shared__ int32_t s_hi[kThreads];
     const bool inx = valid && epo >= 0 && hi >= epo && hi < Vg && tw >= 0;
     s_hi[threadIdx.x] = inx ? hi : -1;
+    // a group across two blocks (fr.gside, last level): its members leave their terms in gside slot
+    // e0 / kThreads; the second of the two blocks to finish sums them (last-arriver counter gcnt)
+    __shared__ int32_t s_sx[2];  // the straddling group's vertex: [0] from the previous block, [1] into the next
+    if (threadIdx.x < 2) s_sx[threadIdx.x] = -1;
     __syncthreads();
+    int32_t gslot = -1, gk = 0;
+    if (inx && fr.gside) {
+        const int32_t k = e - 4 * (hi - epo) + (bp >> 1), e0 = e - k;
+        // (boundary edges of level l-2 have no such group: their edge point's ring is the vertex kernel's)
+        if ((e0 & (kThreads - 1)) > kThreads - 4 && __ldg(ehh2 + (hi - epo)).y >= 0) {
+            gslot = e0 / kThreads;
+            gk = k;
+            s_sx[gslot - (int32_t)blockIdx.x + 1] = hi;
+        }
+    }
     bool lead = false;
     if (inx && e - 4 * (hi - epo) + (bp >> 1) == 0 && threadIdx.x + 3 < blockDim.x)
         lead = s_hi[threadIdx.x + 1] == hi && s_hi[threadIdx.x + 2] == hi && s_hi[threadIdx.x + 3] == hi;
@@ -410,15 +424,12 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
                     s_ring[0][threadIdx.x] = rt.x;
                     s_ring[1][threadIdx.x] = rt.y;
                     s_ring[2][threadIdx.x] = rt.z;
-                    if (fr.gside) {  // a group across two blocks: its terms for k_cc_straddle
-                        const int32_t k = e - 4 * (hi - epo) + (bp >> 1), e0 = e - k;
-                        if ((e0 & (kThreads - 1)) > kThreads - 4) {
-                            float *gs = fr.gside + f * fr.gsidestride + 12 * (int64_t)(e0 / kThreads) + 3 * k;
-                            gs[0] = rt.x;
-                            gs[1] = rt.y;
-                            gs[2] = rt.z;
-                            if (k == 0 && f == 0) fr.gvid[e0 / kThreads] = hi;
-                        }
+                    if (gslot >= 0) {  // a group across two blocks: its term, published before the block's barrier
+                        float *gs = fr.gside + f * fr.gsidestride + 12 * (int64_t)gslot + 3 * gk;
+                        gs[0] = rt.x;
+                        gs[1] = rt.y;
+                        gs[2] = rt.z;
+                        __threadfence();
                     }
                 }
             }
@@ -451,6 +462,29 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
             }
         }
         __syncthreads();
+    }
+    // straddling groups: S(x) = 1/2 p_x + 1/16 sum_k (p_ep_k + 1/2 (f_a,k + f_b,k)), by the block
+    // that arrives second (both blocks' terms are in gside by then; the counter is reset for the
+    // next launch)
+    if (fr.gside && threadIdx.x < 2) {
+        const int32_t x = s_sx[threadIdx.x];
+        if (x >= 0) {
+            const int32_t slot = (int32_t)blockIdx.x - 1 + threadIdx.x;
+            __threadfence();
+            if (atomicAdd(fr.gcnt + slot, 1) == 1) {
+                __threadfence();
+                fr.gcnt[slot] = 0;
+                for (int f = 0; f < nb; ++f) {
+                    const float *gs = fr.gside + f * fr.gsidestride + 12 * (int64_t)slot;
+                    float t[12];
+#pragma unroll
+                    for (int i = 0; i < 12; ++i) t[i] = __ldcg(gs + i);
+                    const P3 acc{(t[0] + t[3]) + (t[6] + t[9]), (t[1] + t[4]) + (t[7] + t[10]),
+                                 (t[2] + t[5]) + (t[8] + t[11])};
+                    st3(fr.wr(f), x, 0.5f * ld3(fr.rd(f), x) + 0.0625f * acc);
+                }
+            }
+        }
     }
 }
 
@@ -781,8 +815,8 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
             if (g.nlong > 0 && g.type[s] == 0 && cc_long_ring(g, p, j, CR)) continue;  // k_cc_vertex_long
             if (s == g.gp_skip_seg) {
                 // done by k_cc_edge_gp when the 4 child edges of interior edge j (ids base ..
-                // base + 3) are in one of its blocks, and by k_cc_straddle (gside) when they
-                // straddle two
+                // base + 3) are in one of its blocks, and by the second of the two blocks
+                // (gside) when they straddle two
                 const int m1 = g.birth[s] - 1;
                 if (__ldg(g.ehh[m1] + j).y >= 0) {
                     if (fr.gside) continue;
@@ -792,24 +826,6 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, V
             }
             cc_vertex_one<ORDER, CR>(x, fr, g, p, csv_list, s, j);
         }
-    }
-}
-
-// ------------------------------------------------------------------------------------------
-// the edge points born at l-1 whose group of four grandparent edges straddles two blocks of
-// k_cc_edge_gp: S(x) = 1/2 p_x + 1/16 sum_k (p_ep_k + 1/2 (f_a,k + f_b,k)) from the four terms the
-// two blocks left in gside (one group per block boundary at most)
-__global__ void __launch_bounds__(kThreads) k_cc_straddle(Frames fr, int32_t nblk) {
-    ALSUB_GRID_WAIT();
-    const int32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nblk) return;
-    const int32_t x = fr.gvid[b];
-    if (x < 0) return;
-    for (int f = 0; f < fr.nb; ++f) {
-        const float *gs = fr.gside + f * fr.gsidestride + 12 * (int64_t)b;
-        const P3 acc{(gs[0] + gs[3]) + (gs[6] + gs[9]), (gs[1] + gs[4]) + (gs[7] + gs[10]),
-                     (gs[2] + gs[5]) + (gs[8] + gs[11])};
-        st3(fr.wr(f), x, 0.5f * ld3(fr.rd(f), x) + 0.0625f * acc);
     }
 }
 
@@ -836,11 +852,13 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, b
     // last level >= 3: compact corner sums (fr.c0shift, set by the caller with the buffers)
     const Frames &fr = fr0;
     int32_t epo = -1;
+    const int2 *ehh2 = nullptr;  // the level-(l-2) edges of those edge points
     if (gp) {
         for (int k = 0; k < g.nseg; ++k)
             if (g.type[k] == 2 && g.birth[k] == g.level - 1 && g.len[k] > 0) {
                 epo = g.start[k];
                 g.gp_skip_seg = k;
+                ehh2 = g.ehh[g.birth[k] - 1];
             }
     }
     if (p.F > 0) {
@@ -866,8 +884,8 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, b
         se = L.side;
     }
     if (gp && gp->E > 0) {
-        if (one) launch(L, "cc_edge", k_cc_edge_gp<1>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, c, fr, epo);
-        else launch(L, "cc_edge", k_cc_edge_gp<0>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, c, fr, epo);
+        if (one) launch(L, "cc_edge", k_cc_edge_gp<1>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, c, fr, epo, ehh2);
+        else launch(L, "cc_edge", k_cc_edge_gp<0>, dim3(grid_for(gp->E)), dim3(kThreads), 0, se, p, gpd, c, fr, epo, ehh2);
     } else if (p.E > 0) {
         constexpr int IT = 2;
         const unsigned gdim = grid_for(p.E, kThreads * IT);
@@ -905,10 +923,6 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, b
     if (fork) {
         cudaEventRecord(L.ev_join, L.side);
         cudaStreamWaitEvent(s, L.ev_join, 0);
-    }
-    if (gp && gp->E > 0 && fr.gside) {  // after the edge kernel (it wrote the straddling groups' terms)
-        const int32_t nblk = (int32_t)grid_for(gp->E);
-        launch(L, "cc_straddle", k_cc_straddle, dim3(grid_for(nblk)), dim3(kThreads), 0, s, fr, nblk);
     }
 }
 

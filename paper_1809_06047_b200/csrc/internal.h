@@ -266,10 +266,10 @@ struct Frames {
     // runs per warp instead of 12-B stores of every face
     int32_t c0shift = 0;
     // last level: the ring terms of the edge-point groups that straddle two blocks of the
-    // grandparent edge kernel, [edge block][4][3] + the group's vertex id per block (gvid, -1 =
-    // none); finished by k_cc_straddle after the edge kernel
+    // grandparent edge kernel, [edge block][4][3], and an arrival counter per block boundary (gcnt,
+    // zero between launches): the second of the two blocks finishes the group
     float *gside = nullptr;
-    int32_t *gvid = nullptr;
+    int32_t *gcnt = nullptr;
     int64_t gsidestride = 0;
     // per-frame views ([V][3], vertex stride 3)
     ALSUB_HD PR rd(int f) const { return PR{P + f * Pstride, 3}; }
