@@ -68,7 +68,7 @@ ALSUB_D int4 child_edge_row(const LevelDev &gp, int32_t r) {
 // its vertex point 1/2 p + 1/16 sum_t c0[16 j + 4 t + 2] is a shuffle reduction here instead of
 // four c0 gathers in the vertex kernel.
 template <bool ADJ, bool BND, int NBC, bool GPE>
-__global__ void __launch_bounds__(kThreads) k_cc_face_quad(LevelDev p, ChildDev c, Frames fr, bool topo, bool fpv,
+__global__ void __launch_bounds__(kThreads, NBC ? 8 : 0) k_cc_face_quad(LevelDev p, ChildDev c, Frames fr, bool topo, bool fpv,
                                                          LevelDev gp, int32_t fpo) {
     ALSUB_GRID_WAIT();
     __shared__ int4 s_stage[kThreads / 32][128];
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
 // is a block-shared sum over the group when all four threads are in one block (the vertex kernel
 // does the few groups that straddle a block boundary, and boundary e'').
 template <int NBC>
-__global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp, ChildDev c, Frames fr,
+__global__ void __launch_bounds__(kThreads, NBC ? 6 : 0) k_cc_edge_gp(LevelDev p, LevelDev gp, ChildDev c, Frames fr,
                                                        int32_t epo, const int2 *ehh2) {
     ALSUB_GRID_WAIT();
     // the block's children are the contiguous id range [base(e_first), base(e_last) + nch): staged
@@ -353,8 +353,9 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
     const int32_t h = hh.x, tw = hh.y;
     const int32_t R = h >> 2, t = h & 3;
     const int4 row = valid ? __ldg(reinterpret_cast<const int4 *>(gp.face_vtx) + R) : make_int4(0, 0, 0, 0);
-    const int32_t rv[4] = {row.x, row.y, row.z, row.w};
-    const int32_t va = rv[t], vb = rv[(t + 1) & 3];
+    // (selects, not a dynamically indexed array: that would live in local memory)
+    const int32_t va = t == 0 ? row.x : t == 1 ? row.y : t == 2 ? row.z : row.w;
+    const int32_t vb = t == 0 ? row.y : t == 1 ? row.z : t == 2 ? row.w : row.x;
     const int32_t Vg = gp.V, Fg = gp.F;
     const int32_t ep = Vg + Fg + e, fpR = Vg + R, fpS = tw >= 0 ? Vg + (tw >> 2) : 0;
     const int32_t nh = (h & ~3) | ((h + 1) & 3), nt = tw >= 0 ? ((tw & ~3) | ((tw + 1) & 3)) : 0;
@@ -434,7 +435,9 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge_gp(LevelDev p, LevelDev gp
                 }
             }
 
-            for (int k = 0; k < nch; ++k) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (k >= nch) break;
                 const int a = o + k, sa = a + (a >> 5);
                 s_out[sa] = q[k].x;
                 s_out[kSo + sa] = q[k].y;
@@ -751,7 +754,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_vertex_long(LevelDev p, Frames 
 }
 
 template <int ORDER, int PL, bool CR>
-__global__ void __launch_bounds__(kThreads) k_cc_vertex(LevelDev p, Frames fr, VSegs g, int32_t *csv_list) {
+__global__ void __launch_bounds__(kThreads, ORDER == 4 && !CR ? 8 : 0) k_cc_vertex(LevelDev p, Frames fr, VSegs g, int32_t *csv_list) {
     ALSUB_GRID_WAIT();
     constexpr int kVtxTask = 32 * PL;  // vertices per warp task (PL per lane)
     // Work unit = a warp task of 32 PL consecutive vertices of ONE segment (no divergence between
