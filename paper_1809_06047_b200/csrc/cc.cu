@@ -68,7 +68,7 @@ ALSUB_D int4 child_edge_row(const LevelDev &gp, int32_t r) {
 // its vertex point 1/2 p + 1/16 sum_t c0[16 j + 4 t + 2] is a shuffle reduction here instead of
 // four c0 gathers in the vertex kernel.
 template <bool ADJ, bool BND, int NBC, bool GPE>
-__global__ void __launch_bounds__(kThreads, NBC ? 8 : 0) k_cc_face_quad(LevelDev p, ChildDev c, Frames fr, bool topo, bool fpv,
+__global__ void __launch_bounds__(kThreads, NBC ? (ADJ ? 6 : 8) : 0) k_cc_face_quad(LevelDev p, ChildDev c, Frames fr, bool topo, bool fpv,
                                                          LevelDev gp, int32_t fpo) {
     ALSUB_GRID_WAIT();
     __shared__ int4 s_stage[kThreads / 32][128];
