@@ -110,6 +110,17 @@ ALSUB_D P3 ld3c(PW P, int64_t v) {
     const float *q = P.p + P.vs * v;
     return P3{q[0], q[1], q[2]};
 }
+// wide gather: a 12-byte element as one 8-byte and one 4-byte load (whichever half is 8-byte
+// aligned) instead of three 4-byte loads -- scattered gathers are bound by the L1 data pipe's
+// wavefronts (one per load instruction and line touched).  Costs registers: used where measured
+// faster (sqrt3 kernels); on the CC and Loop kernels it raised spills and was slower
+ALSUB_D P3 ld3w(PR P, int64_t v) {
+    const float *q = P.p + P.vs * v;
+    const bool odd = (reinterpret_cast<uintptr_t>(q) & 4) != 0;
+    const float2 d = __ldg(reinterpret_cast<const float2 *>(q + (odd ? 1 : 0)));
+    const float s = __ldg(q + (odd ? 0 : 2));
+    return odd ? P3{s, d.x, d.y} : P3{d.x, d.y, s};
+}
 ALSUB_D void st3(PW P, int64_t v, P3 a) {
     float *q = P.p + P.vs * v;
     q[0] = a.x;

@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(kThreads) k_s3_face(LevelDev p, ChildDev c, Fr
     const int nb = NBC ? NBC : fr.nb;
     for (int f = 0; f < nb; ++f) {
         const PR P = fr.rd(f);
-        const P3 s = ld3(P, v[0]) + ld3(P, v[1]) + ld3(P, v[2]);
+        const P3 s = ld3w(P, v[0]) + ld3w(P, v[1]) + ld3w(P, v[2]);
         if (valid) st3(fr.wr(f), (int64_t)V + i, (1.0f / 3.0f) * s);
     }
     if (!topo) return;
@@ -520,10 +520,10 @@ __global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, V
                             if (q[u] >= 0) q[u] = closed ? vfp + q[u] / 9 : __ldg(p.face_vtx + tri_next(q[u]));
 #pragma unroll
                         for (int u = 0; u < 8; ++u)
-                            if (q[u] >= 0) acc = acc + ld3(P, q[u]);
+                            if (q[u] >= 0) acc = acc + ld3w(P, q[u]);
                     }
                     acc = warp_sum(acc);
-                    if (lane == 0) st3(fr.wr(f), vv, (1.0f - alpha) * ld3(P, vv) + (alpha / (float)nn) * acc);
+                    if (lane == 0) st3(fr.wr(f), vv, (1.0f - alpha) * ld3w(P, vv) + (alpha / (float)nn) * acc);
                 }
             }
             if (lng) continue;
@@ -542,10 +542,10 @@ __global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, V
             constexpr float alpha = 1.0f / 3.0f;  // alpha_6 = (4 - 2 cos(pi/3)) / 9
             for (int f = 0; f < nb; ++f) {
                 const PR P = fr.rd(f);
-                P3 acc = ld3(P, nbv[0]);
+                P3 acc = ld3w(P, nbv[0]);
 #pragma unroll
-                for (int k = 1; k < 6; ++k) acc = acc + ld3(P, nbv[k]);
-                st3(fr.wr(f), v, (1.0f - alpha) * ld3(P, v) + (alpha / 6.0f) * acc);
+                for (int k = 1; k < 6; ++k) acc = acc + ld3w(P, nbv[k]);
+                st3(fr.wr(f), v, (1.0f - alpha) * ld3w(P, v) + (alpha / 6.0f) * acc);
             }
             continue;
         }
@@ -571,20 +571,20 @@ __global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, V
         for (int f = 0; f < nb; ++f) {
             const PR P = fr.rd(f);
             const PW Pn = fr.wr(f);
-            const P3 pv = ld3(P, v);
+            const P3 pv = ld3w(P, v);
             if (n == 0) { st3(Pn, v, pv); continue; }
             P3 acc = p3zero();
             if (list) {
                 for (int32_t k = 0; k < n; ++k) {
                     const int32_t sk = __ldg(list + k) * mult;
-                    acc = acc + ld3(P, closed ? vfp + sk / 9 : __ldg(p.face_vtx + tri_next(sk)));
+                    acc = acc + ld3w(P, closed ? vfp + sk / 9 : __ldg(p.face_vtx + tri_next(sk)));
                 }
             } else {
                 int32_t nbv[6];
 #pragma unroll
                 for (int k = 0; k < 6; ++k) nbv[k] = closed ? vfp + sl[k] / 9 : __ldg(p.face_vtx + tri_next(sl[k]));
 #pragma unroll
-                for (int k = 0; k < 6; ++k) acc = acc + ld3(P, nbv[k]);
+                for (int k = 0; k < 6; ++k) acc = acc + ld3w(P, nbv[k]);
             }
             st3(Pn, v, (1.0f - alpha) * pv + (alpha / (float)n) * acc);
         }
