@@ -90,7 +90,8 @@ def kernel_bytes_cc(name, c, prev, lvl, levels, prev2=None):
         wr += 12 * Fp if fpv else 0               # vertex points of the face points born at lvl
         wr += 12 * Fq                             # vertex points of the face points born at lvl-1
         inter += 12 * F if (fpv and not gp_last) else 0  # half ring sums hs (the last level has none)
-        inter += 12 * F if lvl >= 1 else 0               # corner-0 contributions c0
+        # corner-0 contributions c0; the last level (>= 3) keeps only faces r = 0 mod 4, compacted
+        inter += (12 * ((F + 3) // 4) if (gp_last and lvl >= 3) else 12 * F) if lvl >= 1 else 0
     elif name == "cc_edge":
         if gp_last:
             rd = 8 * Ep + 16 * Fp + 12 * V + 12 * F

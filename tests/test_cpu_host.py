@@ -164,7 +164,8 @@ def test_bench_method_bytes_config3_last_level():
     """The roofline counts method bytes only (the c0 intermediate was counted): for
     config 3's level 5->6 face kernel, read 4S face rows + 12V positions + 48F' grandparent rows,
     write 16S child faces + 12F face points + vertex points of the face points born at levels 5
-    and 4 = 1,045,321,920 B; the 12F corner sums c0 (104,693,760 B) are intermediate."""
+    and 4 = 1,045,321,920 B; the corner sums c0 are intermediate -- at the last level only the faces
+    r = 0 mod 4 keep one, compacted: 12 F/4 = 26,173,440 B."""
     import bench
     V, F, S, E = 10000, 8590, 34080, 18510  # armor9k (SURVEY 8(d))
     cnt = [dict(V=V, F=F, S=S, E=E)]
@@ -172,7 +173,7 @@ def test_bench_method_bytes_config3_last_level():
         V, F, S, E = V + F + E, S, 4 * S, 2 * E + S
         cnt.append(dict(V=V, F=F, S=S, E=E))
     face = bench.kernel_bytes_cc("cc_face", cnt[5], cnt[4], 5, 6, cnt[3])
-    assert face == {"method": 1045321920, "intermediate": 104693760}
+    assert face == {"method": 1045321920, "intermediate": 26173440}
     c5, c4, c3 = cnt[5], cnt[4], cnt[3]
     by_hand = 4 * c5["S"] + 12 * c5["V"] + 48 * c4["F"] + 16 * c5["S"] + 12 * c5["F"] + 12 * c4["F"] + 12 * c3["F"]
     assert face["method"] == by_hand
