@@ -242,17 +242,31 @@ constexpr int kRbXf4 = 3 * kRmLanes / 4;  // float4 per support vertex in XT / s
 // index 3 row + c, bbox over the ordered-int images, checksum sum bits (2 idx + 1) mod 2^64; warp
 // reductions by redux.sync (the 64-bit sum as three exact 32-bit partial sums), one lane's shared
 // atomics into the CTA's record
+// row r's checksum term sum_c bits(x_c) (6 r + 2 c + 1) = (6 r + 1)(b0 + b1 + b2) + 2 b1 + 4 b2
+// (mod 2^64: the distributive law holds in the ring, so the value is the same as term by term)
+ALSUB_D unsigned long long rb_row_sum(int32_t r, const float (&v)[3]) {
+    const unsigned long long b0 = (uint32_t)__float_as_int(v[0]), b1 = (uint32_t)__float_as_int(v[1]),
+                             b2 = (uint32_t)__float_as_int(v[2]);
+    return (6ull * (unsigned long long)r + 1ull) * (b0 + b1 + b2) + 2ull * b1 + 4ull * b2;
+}
+// FULL: both rows of every lane exist (all but a chunk's last row group): no per-row predicates
+template <bool FULL>
 ALSUB_D void rb_fold(SummaryRec &r, int32_t ra, int32_t rb, const float (&a)[3], const float (&b)[3]) {
     int32_t lo[3], hi[3];
-    unsigned long long sum = 0ull;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const int32_t oa = f2ord(a[c]), ob = f2ord(b[c]);
-        lo[c] = min(ra >= 0 ? oa : INT32_MAX, rb >= 0 ? ob : INT32_MAX);
-        hi[c] = max(ra >= 0 ? oa : INT32_MIN, rb >= 0 ? ob : INT32_MIN);
-        if (ra >= 0) sum += (unsigned long long)(uint32_t)__float_as_int(a[c]) * (unsigned long long)(6ll * ra + 2 * c + 1);
-        if (rb >= 0) sum += (unsigned long long)(uint32_t)__float_as_int(b[c]) * (unsigned long long)(6ll * rb + 2 * c + 1);
+        if constexpr (FULL) {
+            lo[c] = min(oa, ob);
+            hi[c] = max(oa, ob);
+        } else {
+            lo[c] = min(ra >= 0 ? oa : INT32_MAX, rb >= 0 ? ob : INT32_MAX);
+            hi[c] = max(ra >= 0 ? oa : INT32_MIN, rb >= 0 ? ob : INT32_MIN);
+        }
     }
+    unsigned long long sum;
+    if constexpr (FULL) sum = rb_row_sum(ra, a) + rb_row_sum(rb, b);
+    else sum = (ra >= 0 ? rb_row_sum(ra, a) : 0ull) + (rb >= 0 ? rb_row_sum(rb, b) : 0ull);
     const unsigned m = 0xffffffffu;
     const uint32_t s0 = __reduce_add_sync(m, (uint32_t)(sum & 0xffffu));
     const uint32_t s1 = __reduce_add_sync(m, (uint32_t)((sum >> 16) & 0xffffu));
@@ -269,16 +283,27 @@ ALSUB_D void rb_fold(SummaryRec &r, int32_t ra, int32_t rb, const float (&a)[3],
             atomicMin(&r.lo[c], l[c]);
             atomicMax(&r.hi[c], h[c]);
         }
-        atomicAdd(&r.sum, (unsigned long long)s0 + ((unsigned long long)s1 << 16) + ((unsigned long long)s2 << 32));
+        // the 64-bit add as two native 32-bit shared atomics (a 64-bit one is a CAS loop): the low
+        // word's returned old value gives this add's exact carry into the high word
+        const unsigned long long x = (unsigned long long)s0 + ((unsigned long long)s1 << 16) + ((unsigned long long)s2 << 32);
+        uint32_t *w = reinterpret_cast<uint32_t *>(&r.sum);
+        const uint32_t xl = (uint32_t)x, old = atomicAdd(w, xl);
+        atomicAdd(w + 1, (uint32_t)(x >> 32) + (old + xl < old ? 1u : 0u));
     }
 }
 
 ALSUB_D void rb_store(float *so, const int32_t (&rid)[6], float *out, int64_t VL, int f0, int nb, int lane,
                       const float (&a)[4][3], const float (&b)[4][3], SummaryRec *srec, int32_t rowa, int32_t rowb) {
     if (srec) {
+        if (__all_sync(0xffffffffu, rowb >= 0)) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (f0 + u < nb) rb_fold(srec[f0 + u], rowa, rowb, a[u], b[u]);
+            for (int u = 0; u < 4; ++u)
+                if (f0 + u < nb) rb_fold<true>(srec[f0 + u], rowa, rowb, a[u], b[u]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (f0 + u < nb) rb_fold<false>(srec[f0 + u], rowa, rowb, a[u], b[u]);
+        }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)

@@ -1,4 +1,5 @@
-"""One blocked-SpMM batch of config 5 (armor50k CC L4, 32 frames) for ncu captures."""
+"""One blocked-SpMM batch of config 5 (armor50k CC L4, 32 frames) for ncu captures;
+`python tools/rm_once.py summary` runs the variant with the per-frame records folded in."""
 import os
 import sys
 
@@ -13,6 +14,10 @@ frames = torch.stack([torch.from_numpy(mg.frame_positions(mesh["pos"], t, 4096))
 m = Mesh(mesh["face_off"], mesh["face_vtx"], mesh["pos"], mesh["crease"], mesh["sigma"])
 m.refine("cc", 4)
 m.build_refinement_matrix(4)
-out = m.eval_frames_matrix(frames)
-out = m.eval_frames_matrix(frames, out=out)
+if len(sys.argv) > 1 and sys.argv[1] == "summary":
+    out, rec = m.eval_frames_matrix_summary(frames)
+    out, rec = m.eval_frames_matrix_summary(frames, out=out, summary=rec)
+else:
+    out = m.eval_frames_matrix(frames)
+    out = m.eval_frames_matrix(frames, out=out)
 torch.cuda.synchronize()
