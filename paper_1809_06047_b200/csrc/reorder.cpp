@@ -13,7 +13,6 @@
 #include <stdint.h>
 
 #include <algorithm>
-#include <numeric>
 #include <vector>
 
 #include "alsub.h"
@@ -60,29 +59,48 @@ extern "C" alsub_status alsub_rcm_order(const int32_t *face_off, const int32_t *
         (num_verts > 0 && !perm_vtx) || (num_faces > 0 && !perm_face))
         return alsub::set_error(ALSUB_E_ARG, "bad argument");
     const int32_t V = num_verts, F = num_faces;
-    // vertex graph of the mesh edges (the off-diagonal pattern of the graph Laplacian)
-    std::vector<std::pair<int32_t, int32_t>> pairs;
+    // vertex graph of the mesh edges (the off-diagonal pattern of the graph Laplacian): both
+    // directions of every face side bucketed by vertex (counting sort), each list sorted and
+    // de-duplicated -- O(slots), not a global sort of the pairs
     for (int32_t r = 0; r < F; ++r) {
         const int32_t o = face_off[r], c = face_off[r + 1] - o;
         if (c < 1) return alsub::set_error(ALSUB_E_MESH, "face with no vertices");
         for (int32_t t = 0; t < c; ++t) {
-            const int32_t a = face_vtx[o + t], b = face_vtx[o + (t + 1) % c];
-            if (a < 0 || a >= V || b < 0 || b >= V) return alsub::set_error(ALSUB_E_MESH, "vertex index out of range");
-            if (a == b) continue;
-            pairs.emplace_back(a, b);
-            pairs.emplace_back(b, a);
+            const int32_t a = face_vtx[o + t];
+            if (a < 0 || a >= V) return alsub::set_error(ALSUB_E_MESH, "vertex index out of range");
         }
     }
-    std::sort(pairs.begin(), pairs.end());
-    pairs.erase(std::unique(pairs.begin(), pairs.end()), pairs.end());
+    std::vector<int32_t> cnt((size_t)V + 1, 0);
+    for (int32_t r = 0; r < F; ++r) {
+        const int32_t o = face_off[r], c = face_off[r + 1] - o;
+        for (int32_t t = 0; t < c; ++t) {
+            const int32_t a = face_vtx[o + t], b = face_vtx[o + (t + 1) % c];
+            if (a == b) continue;
+            ++cnt[a + 1];
+            ++cnt[b + 1];
+        }
+    }
+    for (int32_t v = 0; v < V; ++v) cnt[v + 1] += cnt[v];
+    std::vector<int32_t> raw((size_t)cnt[V]), cur(cnt.begin(), cnt.end() - 1);
+    for (int32_t r = 0; r < F; ++r) {
+        const int32_t o = face_off[r], c = face_off[r + 1] - o;
+        for (int32_t t = 0; t < c; ++t) {
+            const int32_t a = face_vtx[o + t], b = face_vtx[o + (t + 1) % c];
+            if (a == b) continue;
+            raw[cur[a]++] = b;
+            raw[cur[b]++] = a;
+        }
+    }
     Graph g;
     g.off.assign((size_t)V + 1, 0);
-    g.adj.resize(pairs.size());
-    for (size_t i = 0; i < pairs.size(); ++i) {
-        ++g.off[pairs[i].first + 1];
-        g.adj[i] = pairs[i].second;
+    g.adj.reserve(raw.size());
+    for (int32_t v = 0; v < V; ++v) {
+        int32_t *lo = raw.data() + cnt[v], *hi = raw.data() + cnt[v + 1];
+        std::sort(lo, hi);
+        hi = std::unique(lo, hi);
+        g.adj.insert(g.adj.end(), lo, hi);
+        g.off[v + 1] = (int32_t)g.adj.size();
     }
-    for (int32_t v = 0; v < V; ++v) g.off[v + 1] += g.off[v];
     auto less_deg = [&](int32_t a, int32_t b) { return g.deg(a) != g.deg(b) ? g.deg(a) < g.deg(b) : a < b; };
 
     std::vector<int32_t> mark((size_t)V, -1), order, comp_last, last;
@@ -138,15 +156,15 @@ extern "C" alsub_status alsub_rcm_order(const int32_t *face_off, const int32_t *
         perm_vtx[i] = order[(size_t)V - 1 - i];
         newid[perm_vtx[i]] = i;
     }
-    std::vector<int32_t> key((size_t)F);
+    // faces by their minimum new vertex id, ties in the original order: a stable counting sort
+    std::vector<int32_t> key((size_t)F), start((size_t)V + 1, 0);
     for (int32_t r = 0; r < F; ++r) {
         int32_t k = INT32_MAX;
         for (int32_t h = face_off[r]; h < face_off[r + 1]; ++h) k = std::min(k, newid[face_vtx[h]]);
         key[r] = k;
+        ++start[k + 1];
     }
-    std::vector<int32_t> fo((size_t)F);
-    std::iota(fo.begin(), fo.end(), 0);
-    std::stable_sort(fo.begin(), fo.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
-    std::copy(fo.begin(), fo.end(), perm_face);
+    for (int32_t v = 0; v < V; ++v) start[v + 1] += start[v];
+    for (int32_t r = 0; r < F; ++r) perm_face[start[key[r]]++] = r;
     return ALSUB_OK;
 }
