@@ -602,6 +602,21 @@ static VSegs make_segs(alsub_mesh *m, int l) {
     return g;
 }
 
+// CC levels whose edge kernel iterates the grandparent edges (k_cc_edge_gp, cc.cu): the last
+// refined level (its edge pairs are never stored) and, when it is level 3 or later and its crease
+// rules are not fused, the level before it (it then also writes the boundary words of the last
+// level; ALSUB_NO_GP_MID=1 keeps k_cc_edge there, for A/B runs)
+static bool cc_use_gp(const alsub_mesh *m, int l, bool special) {
+    static const bool mid_off = [] {
+        const char *e = getenv("ALSUB_NO_GP_MID");
+        return e && e[0] == '1';
+    }();
+    const LevelHost &P = m->lv[l];
+    if (l < 2) return false;
+    if (P.edge_hh == nullptr) return true;
+    return !mid_off && l >= 3 && l == m->levels - 2 && m->gside && !(special && P.V < kFuseCreaseMaxV);
+}
+
 // NVTX range (eager launches; `ncu --nvtx --nvtx-include "alsub level 5->6/"` selects a level)
 struct Nvtx {
     Nvtx(const char *fmt, int a, int b) {
@@ -677,10 +692,11 @@ static void enqueue_refine(alsub_mesh *m, cudaStream_t s, Launches &L) {
         if (scheme == ALSUB_CATMULL_CLARK) {
             VSegs g = make_segs(m, l);
             LevelDev gp{};
-            const bool use_gp = l >= 2 && P.edge_hh == nullptr;
+            const bool use_gp = cc_use_gp(m, l, special);
             if (use_gp) {
                 gp = dev_of(m->lv[l - 1]);
                 g.len[g.hs_seg] = 0;  // the edge kernel smooths the edge points born at level l
+                fr.hs = nullptr;      // so the face kernel writes no half sums
             }
             // crease module fused into the level kernels on small levels (the latency of a separate
             // pass dominates there), a separate kernel on large ones (fusion costs occupancy)
@@ -1077,13 +1093,14 @@ static void static_level(alsub_mesh *m, int l, const Frames &fr, cudaStream_t s,
     if (scheme == ALSUB_CATMULL_CLARK) {
         VSegs g = make_segs(m, l);
         LevelDev gp{};
-        const bool use_gp = l >= 2 && Pl.edge_hh == nullptr;
+        const bool use_gp = cc_use_gp(m, l, special);
+        Frames fx = fr;
         if (use_gp) {
             gp = dev_of(m->lv[l - 1]);
             g.len[g.hs_seg] = 0;  // the edge kernel smooths the edge points born at level l
+            fx.hs = nullptr;
         }
         p.crease = (special && !use_gp && Pl.V < kFuseCreaseMaxV) ? 1 : 0;
-        Frames fx = fr;
         if (use_gp && l >= 3 && m->gside) {  // compact corner sums + straddling groups
             fx.c0shift = 2;
             fx.gside = fr.nb == 1 ? m->gside : m->frame_gside;

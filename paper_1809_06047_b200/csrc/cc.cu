@@ -109,7 +109,8 @@ __global__ void __launch_bounds__(kThreads, NBC ? (ADJ ? 6 : 8) : 0) k_cc_face_q
             // r and corner 3 of child r+1 (mod 4): its half ring sum from this parent face is
             // (p2 + f_r) + (p0 + f_{r+1}); the vertex kernel adds the two halves of the edge
             // (at the last level the edge kernel finishes these vertices itself, see k_cc_edge_gp)
-            if constexpr (!GPE) {
+            // (not needed when the edge kernel iterates the grandparent edges: fr.hs = nullptr)
+            if (!GPE && fr.hs != nullptr) {
                 const P3 q = p0 + fc;
                 const int src = (lane & ~3) | ((lane + 1) & 3);
                 P3 qn;
@@ -465,6 +466,25 @@ __global__ void __launch_bounds__(kThreads, NBC ? 6 : 0) k_cc_edge_gp(LevelDev p
             }
         }
         __syncthreads();
+    }
+    // a level before the last (c.bnd_word set): the boundary words of level l+1.  Child k of e is
+    // the level-l edge x = base + k, boundary iff e is and k < 2, with the level-l prefix
+    // bprefix(x) = 2 bprefix(e) + bnd_e min(k, 2); x's own children start at 4x - bprefix(x)
+    // (the same closed forms k_cc_edge writes one level at a time)
+    if (c.bnd_word != nullptr && valid) {
+        const int32_t bpe = 4 * e - base;
+        for (int k = 0; k < nch; ++k) {
+            const int32_t x = base + k;
+            const bool bx = tw < 0 && k < 2;
+            const int32_t bpx = 2 * bpe + (tw < 0 ? min(k, 2) : 0);
+            const int32_t b2 = 4 * x - bpx;
+            if (bx) {
+                atomicOr(c.bnd_word + (b2 >> 5), 1u << (b2 & 31));
+                atomicOr(c.bnd_word + ((b2 + 1) >> 5), 1u << ((b2 + 1) & 31));
+            }
+            const int32_t w = (b2 + 31) >> 5;
+            if (32 * w < b2 + (bx ? 3 : 4)) c.bnd_wpre[w] = 2 * bpx + (bx ? min(32 * w - b2, 2) : 0);
+        }
     }
     // straddling groups: S(x) = 1/2 p_x + 1/16 sum_k (p_ep_k + 1/2 (f_a,k + f_b,k)), by the block
     // that arrives second (both blocks' terms are in gside by then; the counter is reset for the
@@ -866,7 +886,9 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, b
     }
     if (p.F > 0) {
         if constexpr (ORDER == 4) {
-            if (gp) {
+            // the last level recomputes its edge rows from the grandparent's (face_edge not
+            // stored); a level before it with the grandparent edge kernel reads its own rows
+            if (gp && p.face_edge == nullptr) {
                 if (one) launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 1, true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd, fpo);
                 else launch(L, "cc_face", k_cc_face_quad<ADJ, BND, 0, true>, dim3(grid_for(p.F)), dim3(kThreads), 0, s, p, c, fr, topo, fpv, gpd, fpo);
             } else {
