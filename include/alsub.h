@@ -242,6 +242,15 @@ alsub_status alsub_probe(alsub_mesh *mesh, int32_t level, const char *kernel, in
  * Errors: E_ARG (null mesh/count, or the probe matched no launch of the captured refine), E_CUDA. */
 alsub_status alsub_probe_read(alsub_mesh *mesh, float *ms, int32_t cap, int32_t *count);
 
+/* Offsets of the probed kernel inside replay i (measurement: the level timeline of DESIGN.md §12):
+ * start_ms[i] / stop_ms[i] = ms from the caller's event ref_events[i] (a cudaEvent_t with timing,
+ * recorded on the refine's stream before replay i) to the probe's start / stop record.  The start
+ * record follows the kernel's predecessors, so it is the time the kernel could start.  Host arrays
+ * of `cap`; *count as alsub_probe_read.  Waits for the last replay.
+ * Errors: E_ARG (null mesh/arrays/count, no matching launch), E_CUDA (e.g. an event without timing). */
+alsub_status alsub_probe_read_offsets(alsub_mesh *mesh, void *const *ref_events, float *start_ms, float *stop_ms,
+                                      int32_t cap, int32_t *count);
+
 /* Per-frame result summary of a batch of frames (what the sharded config-5 job
  * gathers over NCCL -- 32 B per frame instead of the frame).  frames: DEVICE fp32 [num_frames]
  * [num_verts][3] (e.g. the output of alsub_eval_frames); summary: DEVICE, num_frames records of

@@ -81,6 +81,7 @@ def lib():
     L.alsub_frame_summary.argtypes = [vp, i32, i64, vp, vp]
     L.alsub_probe.argtypes = [vp, i32, C.c_char_p, i32]
     L.alsub_probe_read.argtypes = [vp, vp, i32, C.POINTER(i32)]
+    L.alsub_probe_read_offsets.argtypes = [vp, vp, vp, vp, i32, C.POINTER(i32)]
     L.alsub_last_launch_count.argtypes = [vp]
     L.alsub_last_launch_count.restype = i64
     L.alsub_mesh_destroy.argtypes = [vp]
@@ -92,7 +93,7 @@ def lib():
               "alsub_level_positions_ptr", "alsub_reevaluate", "alsub_rcm_order", "alsub_mesh_extract",
               "alsub_extract_maps", "alsub_build_refinement_matrix", "alsub_refinement_matrix_info",
               "alsub_refinement_matrix_csr", "alsub_eval_frames_matrix", "alsub_refinement_matrix_blocks", "alsub_eval_frames_matrix_summary", "alsub_frame_summary", "alsub_probe",
-              "alsub_probe_read"):
+              "alsub_probe_read", "alsub_probe_read_offsets"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -382,6 +383,16 @@ class Mesh:
         n = C.c_int32(0)
         _check(self._lib.alsub_probe_read(self._h, buf, cap, C.byref(n)))
         return [float(buf[i]) for i in range(min(n.value, cap))]
+
+    def probe_read_offsets(self, ref_events):
+        """(start, stop) offsets in ms of the probed kernel in replay i from the torch.cuda.Event
+        ref_events[i] (timing enabled, recorded on the refine's stream before replay i)."""
+        cap = len(ref_events)
+        evs = (C.c_void_p * cap)(*[C.c_void_p(e.cuda_event) for e in ref_events])
+        a, b = (C.c_float * cap)(), (C.c_float * cap)()
+        n = C.c_int32(0)
+        _check(self._lib.alsub_probe_read_offsets(self._h, evs, a, b, cap, C.byref(n)))
+        return [(float(a[i]), float(b[i])) for i in range(min(n.value, cap))]
 
     @property
     def last_launch_count(self):

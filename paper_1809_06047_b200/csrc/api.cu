@@ -1517,6 +1517,23 @@ extern "C" alsub_status alsub_probe_read(alsub_mesh *m, float *ms, int32_t cap, 
     return ALSUB_OK;
 }
 
+extern "C" alsub_status alsub_probe_read_offsets(alsub_mesh *m, void *const *ref_events, float *start_ms, float *stop_ms,
+                                                 int32_t cap, int32_t *count) {
+    if (!m || !ref_events || !start_ms || !stop_ms || !count) return fail(ALSUB_E_ARG, "null argument");
+    const int32_t n = m->probe_next;
+    *count = n;
+    if (!m->probe_start.empty() && m->gexec && !m->probe_node[0])
+        return fail(ALSUB_E_ARG, "the probe matched no kernel of the captured refine");
+    if (n == 0) return ALSUB_OK;
+    CU(cudaEventSynchronize(m->probe_stop[n - 1]));
+    for (int32_t i = 0; i < n && i < cap; ++i) {
+        cudaEvent_t r = (cudaEvent_t)ref_events[i];
+        CU(cudaEventElapsedTime(start_ms + i, r, m->probe_start[i]));
+        CU(cudaEventElapsedTime(stop_ms + i, r, m->probe_stop[i]));
+    }
+    return ALSUB_OK;
+}
+
 extern "C" int64_t alsub_last_launch_count(const alsub_mesh *m) { return m ? m->last_launches : 0; }
 
 extern "C" void alsub_mesh_destroy(alsub_mesh *m) {

@@ -634,3 +634,31 @@ def test_probe_times_kernel_inside_graph():
         m.probe(0, None, 0)  # disarm
         m.refine("cc", 3)
         assert m.probe_read() == [] and torch.equal(m.positions(3), ref)
+
+
+def test_parity_grandparent_edge_kernel_before_last_level():
+    """Level L-2 >= 3 runs the grandparent edge kernel when its crease rules are not fused: always
+    for crease-free closed meshes (cube CC L5 / L6: levels 3 / 4), and on a creased open grid whose
+    level 3 is above the fused-crease threshold (V3 >= 2^20: boundary words of level 4 written in
+    closed form by that kernel, separate crease pass).  Full topology and positions at every level,
+    static mode bitwise equal to dynamic mode."""
+    compare(mg.cube(), "cc", 5)
+    compare(mg.cube(), "cc", 6)
+    import math
+    n = 128
+    g = mg.grid(n, n, tri_cells=[(5, 7), (60, 61)], z=lambda i, j: 0.1 * math.sin(0.1 * i) * math.cos(0.13 * j),
+                name="grid128")
+    vid = lambda i, j: j * (n + 1) + i
+    pairs = [(vid(i, 64), vid(i + 1, 64)) for i in range(10, 100)] + [(vid(30, j), vid(30, j + 1)) for j in range(5, 50)]
+    g["crease"] = np.asarray(pairs, np.int32)
+    g["sigma"] = np.asarray([1.5] * 90 + [np.inf] * 45, np.float32)
+    compare(g, "cc", 5)
+    Mesh = _gpu()
+    frames = torch.stack([torch.from_numpy(mg.frame_positions(g["pos"], t, 16)) for t in range(2)]).cuda()
+    with Mesh(g["face_off"], g["face_vtx"], g["pos"], g["crease"], g["sigma"]) as m:
+        m.refine("cc", 5)
+        out = m.eval_frames(frames, 5)
+        for t in range(2):
+            m.set_positions(frames[t])
+            m.refine("cc", 5)
+            assert torch.equal(out[t], m.positions(5)), f"frame {t}"
