@@ -721,6 +721,132 @@ ALSUB_D void cc_vertex_smooth(const VtxCtx<ORDER> &x, const Frames &fr, const VS
     }
 }
 
+// ---- the fused-crease (small) levels: one smooth evaluation, then the crease rule ----
+// At these sizes the kernel is a chain of dependent loads (and its code size matters: ncu showed
+// a quarter of the level-1 stalls on instruction fetch while cc_vertex_special and its own copy of
+// cc_vertex_smooth were inlined at every call site).  Here the smooth value is computed once per
+// frame by smooth_value (cc_vertex_smooth's arithmetic and summation order, returning the value),
+// its loads in flight together with the special test's, ring slots and their corner sums four at
+// a time; special vertices then apply crease_vertex_point to it (sharp ones ignore it).
+constexpr int kRingBatch = 4;
+
+// ring of a level-0 vertex (list = its M^T row) or of the face point of a level-0 face (list =
+// nullptr, slots 4 (off + k) + 2): c0 corner sums at levels >= 1, slot gathers at level 0
+template <int ORDER>
+ALSUB_D P3 ring_sum(const VtxCtx<ORDER> &x, const Frames &fr, int f, const int32_t *list, int32_t off, int32_t cnt,
+                    int shift) {
+    const PR P = fr.rd(f);
+    const PW Pn = fr.wr(f);
+    const bool c0p = fr.c0 && shift >= 2;
+    P3 acc = p3zero();
+    for (int32_t k0 = 0; k0 < cnt; k0 += kRingBatch) {
+        int32_t b[kRingBatch];
+#pragma unroll
+        for (int u = 0; u < kRingBatch; ++u)
+            b[u] = k0 + u >= cnt ? -1 : list ? __ldg(list + off + k0 + u) : 4 * (off + k0 + u) + 2;
+        if (c0p) {
+            const PR c0 = fr.c0r(f);
+#pragma unroll
+            for (int u = 0; u < kRingBatch; ++u)
+                if (b[u] >= 0) acc = acc + ld3c(c0, (b[u] << (shift - 2)) >> fr.c0shift);
+        } else {
+            int32_t nbv[kRingBatch], fc[kRingBatch];
+#pragma unroll
+            for (int u = 0; u < kRingBatch; ++u) {
+                nbv[u] = fc[u] = 0;
+                if (b[u] >= 0) {
+                    const int32_t sl = b[u] << shift;
+                    fc[u] = x.V + x.tl.face(sl);
+                    nbv[u] = __ldg(x.face_vtx + x.tl.next(sl));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kRingBatch; ++u)
+                if (b[u] >= 0) acc = acc + ld3(P, nbv[u]) + ld3c(Pn, fc[u]);
+        }
+    }
+    return acc;
+}
+
+template <int ORDER>
+ALSUB_D P3 smooth_value(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs &g, int s, int32_t j, int f) {
+    const int32_t v = g.start[s] + j;
+    const int type = g.type[s];
+    const int m1 = g.birth[s] - 1;
+    const int shift = 2 * (g.level - g.birth[s]);
+    const PR P = fr.rd(f);
+    const PW Pn = fr.wr(f);
+    const P3 pv = ld3(P, v);
+    if (type == 2) {
+        const int2 hh = __ldg(g.ehh[m1] + j);
+        if (hh.y < 0) return pv;
+        if (s == g.hs_seg) {  // edge point born at this level: the face kernel's two half sums
+            const PR hs = fr.hsr(f);
+            return 0.5f * pv + 0.0625f * (ld3c(hs, hh.x) + ld3c(hs, hh.y));
+        }
+        int32_t nh, nt;
+        if (m1 == 0) {
+            const Topo<0> t0{g.face_off0, g.slot_face0};
+            nh = t0.next(hh.x);
+            nt = t0.next(hh.y);
+        } else {
+            nh = (hh.x & ~3) | ((hh.x + 1) & 3);
+            nt = (hh.y & ~3) | ((hh.y + 1) & 3);
+        }
+        const int32_t q[4] = {4 * hh.x + 1, 4 * nh + 3, 4 * hh.y + 1, 4 * nt + 3};
+        P3 acc;
+        if (fr.c0 && shift >= 2) {
+            const PR c0 = fr.c0r(f);
+            acc = ld3c(c0, (q[0] << (shift - 2)) >> fr.c0shift);
+#pragma unroll
+            for (int k = 1; k < 4; ++k) acc = acc + ld3c(c0, (q[k] << (shift - 2)) >> fr.c0shift);
+        } else {
+            int32_t nbv[4], fc[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                nbv[k] = __ldg(x.face_vtx + x.tl.next(q[k] << shift));
+                fc[k] = x.V + x.tl.face(q[k] << shift);
+            }
+            acc = ld3(P, nbv[0]) + ld3c(Pn, fc[0]);
+#pragma unroll
+            for (int k = 1; k < 4; ++k) acc = acc + ld3(P, nbv[k]) + ld3c(Pn, fc[k]);
+        }
+        return 0.5f * pv + 0.0625f * acc;
+    }
+    int32_t off, cnt;
+    const int32_t *list = nullptr;
+    if (type == 1 && m1 > 0) {  // face point of a quad: slots 16 j + 2 + 4 t
+        off = 4 * j;
+        cnt = 4;
+    } else if (type == 1) {  // face point of a level-0 face
+        off = __ldg(g.face_off0 + j);
+        cnt = __ldg(g.face_off0 + j + 1) - off;
+    } else {  // level-0 vertex: its M^T row
+        const int32_t o = __ldg(g.vtx_off0 + j), o1 = __ldg(g.vtx_off0 + j + 1);
+        if (__ldg(g.vbnd0 + j)) return pv;
+        off = o;
+        cnt = o1 - o;
+        list = g.vtx_list0;
+    }
+    if (cnt == 0) return pv;
+    const P3 acc = ring_sum<ORDER>(x, fr, f, list, off, cnt, shift);
+    const float inv = 1.0f / (float)cnt;
+    return (1.0f - 2.0f * inv) * pv + (inv * inv) * acc;
+}
+
+template <int ORDER>
+ALSUB_D void cc_vertex_cr(const VtxCtx<ORDER> &x, const Frames &fr, const VSegs &g, const LevelDev &p,
+                          int32_t *csv_list, int s, int32_t j) {
+    const int32_t v = g.start[s] + j;
+    const int32_t i = sv_index(g, s, j);
+    VCr cr{0, 0.0f, -1, -1};
+    for (int f = 0; f < fr.nb; ++f) {
+        const P3 sm = smooth_value<ORDER>(x, fr, g, s, j, f);
+        if (f == 0 && i >= 0 && p.sv_off[i + 1] > p.sv_off[i]) cr = vertex_crease(p, p.inherit ? csv_list : nullptr, i, v);
+        st3(fr.wr(f), v, cr.k >= 2 ? crease_vertex_point(cr, fr.rd(f), v, sm) : sm);
+    }
+}
+
 // a long level-0 ring (n > kLongRing, not boundary, not special), summed by the whole warp; the
 // same two forms as cc_vertex_smooth: c0 corner sums (levels >= 1) or slot gathers (level 0)
 // level-0 vertex j is summed by k_cc_vertex_long: a long M^T row (the build's list, n > 16), not on
@@ -807,6 +933,15 @@ __global__ void __launch_bounds__(kThreads, ORDER == 4 && !CR ? 8 : 0) k_cc_vert
         while (s_pre[s + 1] <= task) ++s;  // tasks ascend: the segment index only moves forward
         const int32_t j0 = (s_lo[s] + (task - s_pre[s])) * kVtxTask + lane;
         const int32_t len = g.len[s];
+        if (CR) {
+            for (int k = 0; k < PL; ++k) {
+                const int32_t j = j0 + 32 * k;
+                if (j >= len) continue;
+                if (s != g.hs_seg && g.nlong > 0 && g.type[s] == 0 && cc_long_ring(g, p, j, CR)) continue;  // k_cc_vertex_long
+                cc_vertex_cr<ORDER>(x, fr, g, p, csv_list, s, j);
+            }
+            continue;
+        }
         if (s == g.hs_seg) {
             // edge points born at this level: two half sums from the face kernel
             const int m1 = g.birth[s] - 1;
@@ -814,6 +949,7 @@ __global__ void __launch_bounds__(kThreads, ORDER == 4 && !CR ? 8 : 0) k_cc_vert
                 const int32_t j = j0 + 32 * k;
                 if (j >= len) continue;
                 const int32_t v = g.start[s] + j;
+                const int2 hh = __ldg(g.ehh[m1] + j);  // (issued beside the special test's loads)
                 if constexpr (CR) {
                     const int32_t i = sv_index(g, s, j);
                     if (i >= 0) {  // boundary / creased parent edge
@@ -821,7 +957,6 @@ __global__ void __launch_bounds__(kThreads, ORDER == 4 && !CR ? 8 : 0) k_cc_vert
                         continue;
                     }
                 }
-                const int2 hh = __ldg(g.ehh[m1] + j);
                 for (int f = 0; f < fr.nb; ++f) {
                     // boundary edge points keep p (set by the separate crease/boundary pass)
                     if (hh.y < 0) { st3(fr.wr(f), v, ld3(fr.rd(f), v)); continue; }
