@@ -236,8 +236,9 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
     const int32_t e0 = blockIdx.x * (kThreads * IT) + threadIdx.x;
     const int32_t V = p.V, F = p.F;
     const int nb = NBC ? NBC : fr.nb;
-    int32_t hv[IT], tv[IT], va[IT], vb[IT], hn[IT], jl[IT];
+    int32_t hv[IT], tv[IT], va[IT], vb[IT], hn[IT], jl[IT], bpk[IT], spk[IT];
     float sg[IT];
+    const bool bnd = ADJ ? BND : p.B > 0;
 #pragma unroll
     for (int k = 0; k < IT; ++k) {
         const int32_t e = e0 + k * kThreads;
@@ -246,6 +247,10 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
         tv[k] = hh.y;
         // fused crease module: list index of the edge (boundary / creased edges are ~1% of a level)
         jl[k] = (CR && e < p.E) ? sp_index(p.spw, p.spwpre, e) : -1;
+        // the topology half's per-word prefixes depend on e alone: loaded here, with the pair, rather
+        // than after the position stores (one round trip fewer per edge on the latency-bound levels)
+        bpk[k] = (topo && bnd && e < p.E) ? bprefix(p.bnd_word, p.bnd_wpre, e) : 0;
+        spk[k] = (CR && ADJ && topo && c.spw && e < p.E) ? sp_prefix(p.spw, p.spwpre, e) : 0;
     }
 #pragma unroll
     for (int k = 0; k < IT; ++k) {
@@ -277,7 +282,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
         if (e >= p.E) continue;
         const int32_t h = hv[k], tw = tv[k];
         // structured child edge ids: block [base, base + 4 - bnd) = (lo,ep), (hi,ep), (fp_min,ep), (fp_max,ep)
-        const int32_t bp = (ADJ ? BND : p.B > 0) ? bprefix(p.bnd_word, p.bnd_wpre, e) : 0;
+        const int32_t bp = bpk[k];
         const int32_t base = 4 * e - bp;
         if (CR && p.inherit && jl[k] >= 0) fused_inherit(p, c, jl[k], p.sp[jl[k]], base, V + F + e);
         if constexpr (ADJ) {
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
                     c.bnd_wpre[w] = 2 * bp + (tw < 0 ? min(kk, 2) : 0);
                 }
             }
-            if (CR && c.spw) fused_child_words(c, base, nch, sp_prefix(p.spw, p.spwpre, e), jl[k] >= 0);
+            if (CR && c.spw) fused_child_words(c, base, nch, spk[k], jl[k] >= 0);
         }
     }
 }
