@@ -58,11 +58,11 @@ def level_counts(m, levels):
     out = []
     for l in range(levels + 1):
         c = m.counts(l)
-        out.append(dict(V=c["verts"], F=c["faces"], S=c["face_slots"], E=c["edges"], level=l))
+        out.append(dict(V=c["verts"], F=c["faces"], S=c["face_slots"], E=c["edges"], B=c["boundary_edges"], level=l))
     return out
 
 
-def kernel_bytes_cc(name, c, prev, lvl, levels, prev2=None):
+def kernel_bytes_cc(name, c, prev, lvl, levels, prev2=None, gp_mid=False):
     """Algorithmic bytes of one launch of a CC level kernel: every array the kernel
     reads or writes, counted once, split into
       "method"       -- the method's own data: parent topology and positions in, child topology and
@@ -72,7 +72,9 @@ def kernel_bytes_cc(name, c, prev, lvl, levels, prev2=None):
     c = counts of the parent level lvl, prev = level lvl-1.  Mirrors the plan in api.cu: the last
     refined level (lvl = levels-1 >= 2) recomputes its edge rows from the grandparent and iterates
     the grandparent's edges, so level levels-1 never stores face_edge / face_twin / edge pairs;
-    twins are only stored where the next level emits adjacency."""
+    twins are only stored where the next level emits adjacency.  gp_mid: level levels-2 (>= 3, crease
+    rules not fused) also iterates the grandparent's edges (cc_use_gp in api.cu): no half sums,
+    compact corner sums, the edge kernel finishes the edge points born at lvl and lvl-1."""
     V, F, S, E = c["V"], c["F"], c["S"], c["E"]
     Fp = prev["F"] if prev else 0
     Ep = prev["E"] if prev else 0
@@ -80,27 +82,28 @@ def kernel_bytes_cc(name, c, prev, lvl, levels, prev2=None):
     Eq = prev2["E"] if (prev2 and lvl >= 2) else 0   # edge points born at lvl-1 (last level: edge kernel)
     adj = lvl < levels - 1                        # this level emits child adjacency
     gp_last = levels >= 3 and lvl == levels - 1   # grandparent path at the last level
+    gp = gp_last or (gp_mid and lvl == levels - 2 and lvl >= 3)
     child_rows = adj and not (levels >= 3 and lvl + 1 == levels - 1)  # child face_edge / edge pairs stored
     child_twin = lvl + 2 < levels
     fpv = lvl >= 2
     inter = 0
     if name == "cc_face":
-        rd = 4 * S + 12 * V + (48 * Fp if gp_last else 4 * S) + (4 * S if adj else 0)
+        rd = 4 * S + 12 * V + (48 * Fp if gp_last else 4 * S) + (4 * S if child_rows else 0)
         wr = 12 * F + 16 * S + (16 * S if child_rows else 0) + (16 * S if child_twin else 0)
         wr += 12 * Fp if fpv else 0               # vertex points of the face points born at lvl
         wr += 12 * Fq                             # vertex points of the face points born at lvl-1
-        inter += 12 * F if (fpv and not gp_last) else 0  # half ring sums hs (the last level has none)
-        # corner-0 contributions c0; the last level (>= 3) keeps only faces r = 0 mod 4, compacted
-        inter += (12 * ((F + 3) // 4) if (gp_last and lvl >= 3) else 12 * F) if lvl >= 1 else 0
+        inter += 12 * F if (fpv and not gp) else 0  # half ring sums hs (none on the grandparent path)
+        # corner-0 contributions c0; the grandparent path (>= 3) keeps only faces r = 0 mod 4, compacted
+        inter += (12 * ((F + 3) // 4) if (gp and lvl >= 3) else 12 * F) if lvl >= 1 else 0
     elif name == "cc_edge":
-        if gp_last:
+        if gp:
             rd = 8 * Ep + 16 * Fp + 12 * V + 12 * F
         else:
             rd = 8 * E + 4 * S + 12 * V + 12 * F
         wr = 12 * E + (8 * (2 * E + S) if child_rows else 0)
-        wr += 12 * (Ep + Eq) if gp_last else 0    # vertex points of the edge points born at lvl, lvl-1
+        wr += 12 * (Ep + Eq) if gp else 0         # vertex points of the edge points born at lvl, lvl-1
     elif name == "cc_vertex":
-        if gp_last:  # vertices born before lvl-1 only: p in, S out; their faces' c0 sums
+        if gp:  # vertices born before lvl-1 only: p in, S out; their faces' c0 sums
             nv = V - Fp - Ep - Fq - Eq
             return {"method": 12 * nv + 12 * nv, "intermediate": 12 * (F - 4 * Fq - 4 * Eq)}
         if Fq:  # the face points born at lvl-1 are done by the face kernel
@@ -381,6 +384,12 @@ def run_alsub(args):
     m.refine("cc", levels)  # records the CUDA graph
     cnt = level_counts(m, levels)
     Fout, Vout = cnt[-1]["F"], cnt[-1]["V"]
+    special = len(mesh["crease"]) > 0 or cnt[0]["B"] > 0
+
+    def gp_mid_at(lvl):  # mirrors cc_use_gp (api.cu): the grandparent edge kernel at level levels-2
+        return (lvl == levels - 2 and lvl >= 3 and not (special and cnt[lvl]["V"] < (1 << 20))
+                and os.environ.get("ALSUB_NO_GP_MID") != "1")
+
     for _ in range(args.warmup):
         flush.fill_(1.0)
         m.refine("cc", levels)
@@ -449,7 +458,7 @@ def run_alsub(args):
             kk = {}
             for n, t in ks.items():
                 b = kernel_bytes_cc(n, c, cnt[lvl - 1] if lvl > 0 else None, lvl, levels,
-                                    cnt[lvl - 2] if lvl > 1 else None)
+                                    cnt[lvl - 2] if lvl > 1 else None, gp_mid=gp_mid_at(lvl))
                 mb = b["method"] if b else None
                 kk[n] = {"ms": t, "alg_bytes": mb, "intermediate_bytes": b["intermediate"] if b else None,
                          "GBps": (mb / (t * 1e6)) if mb else None, "frac": (mb / (t * 1e6) / peak) if mb else None}
@@ -463,7 +472,7 @@ def run_alsub(args):
             row["kernels"] = kk
         per_level.append(row)
     db = kernel_bytes_cc(dname, cnt[dlvl], cnt[dlvl - 1] if dlvl > 0 else None, dlvl, levels,
-                         cnt[dlvl - 2] if dlvl > 1 else None) if dlvl >= 0 else None
+                         cnt[dlvl - 2] if dlvl > 1 else None, gp_mid=gp_mid_at(dlvl)) if dlvl >= 0 else None
     dbytes = db["method"] if db else None
     dms = sum(probe_ms) / len(probe_ms) if probe_ms else dms_profile
     achieved = dbytes / (dms * 1e6) if dbytes else None

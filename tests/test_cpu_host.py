@@ -179,3 +179,26 @@ def test_bench_method_bytes_config3_last_level():
     assert face["method"] == by_hand
     edge = bench.kernel_bytes_cc("cc_edge", cnt[5], cnt[4], 5, 6, cnt[3])
     assert edge["intermediate"] == 0
+
+
+def test_bench_method_bytes_grandparent_path_before_last_level():
+    """Level levels-2 (>= 3, unfused) runs the grandparent edge kernel (api.cu cc_use_gp): the edge
+    kernel reads the level-(l-1) pairs and rows, 12 V positions and 12 F face points, writes 12 E
+    edge points and the vertex points of the edge points born at l and l-1; the face kernel writes
+    no half sums and compact corner sums (12 F/4) -- config 3's level 4->5, counted by hand."""
+    import bench
+    V, F, S, E = 10000, 8590, 34080, 18510  # armor9k (SURVEY 8(d))
+    cnt = [dict(V=V, F=F, S=S, E=E)]
+    for _ in range(6):
+        V, F, S, E = V + F + E, S, 4 * S, 2 * E + S
+        cnt.append(dict(V=V, F=F, S=S, E=E))
+    c4, c3, c2 = cnt[4], cnt[3], cnt[2]
+    edge = bench.kernel_bytes_cc("cc_edge", c4, c3, 4, 6, c2, gp_mid=True)
+    assert edge["method"] == (8 * c3["E"] + 16 * c3["F"] + 12 * c4["V"] + 12 * c4["F"] + 12 * c4["E"]
+                              + 12 * (c3["E"] + c2["E"]))
+    face = bench.kernel_bytes_cc("cc_face", c4, c3, 4, 6, c2, gp_mid=True)
+    assert face["intermediate"] == 12 * ((c4["F"] + 3) // 4)
+    assert bench.kernel_bytes_cc("cc_face", c4, c3, 4, 6, c2)["intermediate"] == 12 * c4["F"] + 12 * c4["F"]
+    # only level levels-2 takes the flag
+    assert bench.kernel_bytes_cc("cc_edge", c3, c2, 3, 6, cnt[1], gp_mid=True) == \
+        bench.kernel_bytes_cc("cc_edge", c3, c2, 3, 6, cnt[1])
