@@ -173,7 +173,7 @@ ALSUB_D int32_t bprefix(const uint32_t *__restrict__ words, const int32_t *__res
 // (reading R6).  Level l's list has K_l = 2^l K_0 entries in edge-id order; entry j's children
 // are entries 2j (endpoint a) and 2j + 1 (endpoint b) of the next level -- dead children keep
 // sigma = 0, so the list never needs compaction and every index is closed-form.
-struct SpEdge {
+struct alignas(16) SpEdge {
     int32_t e, a, b;   // edge id, endpoints a < b
     int32_t ia, ib;    // special-vertex indices of a and b
     float sigma;       // 0 = dead, > 0, +inf for boundary / infinitely sharp
