@@ -57,6 +57,13 @@ with Mesh(iso["face_off"], iso["face_vtx"], iso["pos"]) as m:
     m.refine("cc", 3)
     m.build_refinement_matrix(3)
     m.eval_frames_matrix(torch.from_numpy(iso["pos"])[None].cuda())
+# round 2, late: the grandparent edge kernel before the last level (crease-free closed mesh, levels
+# 3 of 5: cc_use_gp), dynamic and static
+cube = mg.cube()
+with Mesh(cube["face_off"], cube["face_vtx"], cube["pos"]) as m:
+    m.refine("cc", 5)
+    m.refine("cc", 5)
+    m.eval_frames(torch.from_numpy(np.stack([cube["pos"]] * 3)).cuda(), 5)
 from paper_1809_06047_b200 import AlsubError  # noqa: E402
 for faces in ([(0, 1, 7)], [(0, 1, 2), (0, 1, 3)], [(0, 1, 2), (1, 0, 3), (0, 1, 4)]):
     try:
