@@ -1,7 +1,8 @@
 #!/bin/bash
-# same-box A/B of the current tree against _ab_old/ (a built copy of an older commit), config-3
-# graph replay, 3 rounds; then the timeline of both
+# same-box A/B of the current tree against _ab_old/ (a built copy of an older commit), graph replay
+# of MESH SCHEME LEV (default config 3: armor9k cc 6), N rounds (default 3)
+M=${MESH:-armor9k}; S=${SCHEME:-cc}; L=${LEV:-6}
 for i in $(seq ${N:-3}); do
-  echo -n "current "; python tools/level_sweep.py armor9k cc 6 | tail -1
-  echo -n "old     "; (cd _ab_old && python tools/level_sweep.py armor9k cc 6 | tail -1)
+  echo -n "current "; python tools/level_sweep.py $M $S $L | tail -1
+  echo -n "old     "; (cd _ab_old && python tools/level_sweep.py $M $S $L | tail -1)
 done
