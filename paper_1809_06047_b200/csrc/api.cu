@@ -342,7 +342,6 @@ static alsub_status create_impl(const int32_t *face_off, const int32_t *face_vtx
     b.sv_vtx = A<int32_t>(m, num_verts, s, ML, ok);
     b.sv_off = A<int32_t>(m, (int64_t)num_verts + 1, s, ML, ok);
     b.sv_cnt = A<int32_t>(m, num_verts, s, ML, ok);
-    b.sv_cur = A<int32_t>(m, num_verts, s, ML, ok);
     b.sv_list = A<int32_t>(m, 2 * (int64_t)Emax, s, ML, ok);
     b.spw = A<uint32_t>(m, nw, s, ML, ok);
     b.spwpre = A<int32_t>(m, nw, s, ML, ok);

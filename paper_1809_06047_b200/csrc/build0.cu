@@ -403,12 +403,21 @@ __global__ void __launch_bounds__(kThreads) k_b0_flags(const int32_t *__restrict
                                                      int32_t nw, float *__restrict__ edge_sigma,
                                                      int32_t *__restrict__ edge_cidx, int32_t *__restrict__ flag,
                                                      int32_t *__restrict__ wcnt, int32_t *flags, int32_t lenient,
-                                                     const int32_t *__restrict__ Edev) {
+                                                     const int32_t *__restrict__ Edev, int32_t *__restrict__ sv_cnt) {
     ALSUB_GRID_WAIT();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     // inside alsub_mesh_create the arrays are sized by an upper bound and E is only on the device
     if (Edev) E = min(E, *Edev);
-    if (t < E && edge_hh[t].y < 0) atomicOr(flag + t, 1);
+    // every special edge is flagged exactly once (here if boundary, below if creased), so the
+    // special-vertex list lengths (incident special edges) are counted where the flag is set
+    if (t < E) {
+        const int2 hh = edge_hh[t];
+        if (hh.y < 0) {
+            atomicOr(flag + t, 1);
+            atomicAdd(sv_cnt + face_vtx[hh.x], 1);
+            atomicAdd(sv_cnt + face_vtx[tp.next(hh.x)], 1);
+        }
+    }
     if (t < nw) wcnt[t] = __popc(bnd_word[t]);
     // one warp per crease pair: the lanes test the incident slots of max(a, b) in parallel
     const int64_t k = t >> 5;
@@ -445,70 +454,102 @@ __global__ void __launch_bounds__(kThreads) k_b0_flags(const int32_t *__restrict
     if (sg > 0.0f && edge_hh[e].y >= 0) {  // boundary edges are infinitely sharp anyway (R19)
         edge_sigma[e] = sg;
         atomicOr(flag + e, 1);
+        atomicAdd(sv_cnt + a, 1);
+        atomicAdd(sv_cnt + b, 1);
     }
 }
 
-// special-edge list in ascending edge id (compaction by the scanned flags) + list lengths
+// One launch after the two scans (special flags -> list offsets, list lengths -> CSR offsets):
+//   threads [0, E32)       special edge list in ascending edge id (compaction by the scanned
+//                          flags), its bitmask words and per-word prefixes (E32 = E rounded up to
+//                          whole warps: a warp is one bitmask word);
+//   threads [E32, E32 + V) vertex v's special-vertex row: its incident special edges (each once:
+//                          the edge leaving v in every incident face, the edge entering v where it
+//                          is a boundary edge) as list indices, ascending (= the oracle's edge-id
+//                          order, so crease sums match bit for bit); identity table sv_vtx[v] = v.
+// (Replaces a special-edge kernel, an atomic list scatter and a per-row sort: three launches on
+// the chain the level-0 edge and vertex kernels wait for.)
 template <int ORDER>
-__global__ void __launch_bounds__(kThreads) k_b0_special(const int2 *__restrict__ edge_hh, const int32_t *__restrict__ face_vtx,
-                                                       const float *__restrict__ edge_sigma,
-                                                       const int32_t *__restrict__ flag, const int32_t *__restrict__ off,
-                                                       Topo<ORDER> tp, int32_t E, SpEdge *__restrict__ sp,
-                                                       int32_t *__restrict__ sv_cnt, uint32_t *__restrict__ spw,
-                                                       int32_t *__restrict__ spwpre) {
+__global__ void __launch_bounds__(kThreads) k_b0_special_fill(const int2 *__restrict__ edge_hh,
+                                                            const int32_t *__restrict__ face_vtx,
+                                                            const float *__restrict__ edge_sigma,
+                                                            const int32_t *__restrict__ flag,
+                                                            const int32_t *__restrict__ off, Topo<ORDER> tp, int32_t E,
+                                                            SpEdge *__restrict__ sp, uint32_t *__restrict__ spw,
+                                                            int32_t *__restrict__ spwpre, int32_t V,
+                                                            const int32_t *__restrict__ vtx_off,
+                                                            const int32_t *__restrict__ vtx_slot,
+                                                            const int32_t *__restrict__ face_edge,
+                                                            const int32_t *__restrict__ face_twin,
+                                                            const int32_t *__restrict__ sv_off, int32_t *__restrict__ sv_list,
+                                                            int32_t *__restrict__ sv_vtx, int32_t *__restrict__ scalars,
+                                                            int32_t cap) {
     ALSUB_GRID_WAIT();
-    const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    // the special-edge bitmask word of these 32 edges (one warp = one word) and its prefix
-    const int fl = e < E ? flag[e] : 0;
-    const unsigned word = __ballot_sync(0xffffffffu, fl != 0);
-    if ((threadIdx.x & 31) == 0 && e < E) {
-        spw[e >> 5] = word;
-        spwpre[e >> 5] = off[e];
+    const int32_t E32 = (E + 31) & ~31;
+    const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < E32) {
+        const int32_t e = t;
+        // the special-edge bitmask word of these 32 edges (one warp = one word) and its prefix
+        const int fl = e < E ? flag[e] : 0;
+        const unsigned word = __ballot_sync(0xffffffffu, fl != 0);
+        if ((threadIdx.x & 31) == 0 && e < E) {
+            spw[e >> 5] = word;
+            spwpre[e >> 5] = off[e];
+        }
+        if (e >= E || !fl) return;
+        const int2 hh = edge_hh[e];
+        const int32_t va = face_vtx[hh.x], vb = face_vtx[tp.next(hh.x)];
+        const bool bnd = hh.y < 0;
+        SpEdge x;
+        x.e = e;
+        x.a = min(va, vb);
+        x.b = max(va, vb);
+        x.ia = x.a;  // identity special-vertex table at level 0
+        x.ib = x.b;
+        x.sigma = bnd ? __int_as_float(0x7f800000) : edge_sigma[e];
+        x.flags = bnd ? kSpBoundary : 0;
+        x.pad = 0;
+        sp[off[e]] = x;
+        return;
     }
-    if (e >= E || !fl) return;
-    const int2 hh = edge_hh[e];
-    const int32_t va = face_vtx[hh.x], vb = face_vtx[tp.next(hh.x)];
-    const bool bnd = hh.y < 0;
-    SpEdge x;
-    x.e = e;
-    x.a = min(va, vb);
-    x.b = max(va, vb);
-    x.ia = x.a;  // identity special-vertex table at level 0
-    x.ib = x.b;
-    x.sigma = bnd ? __int_as_float(0x7f800000) : edge_sigma[e];
-    x.flags = bnd ? kSpBoundary : 0;
-    x.pad = 0;
-    sp[off[e]] = x;
-    atomicAdd(sv_cnt + x.a, 1);
-    atomicAdd(sv_cnt + x.b, 1);
-}
-
-__global__ void __launch_bounds__(kThreads) k_b0_svlist(const SpEdge *__restrict__ sp, const int32_t *__restrict__ count,
-                                                      int32_t cap, const int32_t *__restrict__ sv_off,
-                                                      int32_t *__restrict__ sv_cur, int32_t *__restrict__ sv_list) {
-    ALSUB_GRID_WAIT();
-    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= cap || j >= *count) return;
-    const int32_t ia = sp[j].ia, ib = sp[j].ib;
-    sv_list[sv_off[ia] + atomicAdd(sv_cur + ia, 1)] = j;
-    sv_list[sv_off[ib] + atomicAdd(sv_cur + ib, 1)] = j;
-}
-
-// ascending lists (= the oracle's edge-id order, so crease sums match bit for bit) + identity table
-__global__ void __launch_bounds__(kThreads) k_b0_svsort(int32_t V, const int32_t *__restrict__ sv_off,
-                                                      int32_t *__restrict__ sv_list, int32_t *__restrict__ sv_vtx,
-                                                      int32_t *__restrict__ scalars) {
-    ALSUB_GRID_WAIT();
-    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v == 0) scalars[3] = V;
+    const int32_t v = t - E32;
     if (v >= V) return;
+    if (v == 0) scalars[3] = V;
     sv_vtx[v] = v;
     const int32_t o = sv_off[v], n = sv_off[v + 1] - o;
-    for (int32_t a = 1; a < n; ++a) {
-        const int32_t x = sv_list[o + a];
-        int32_t b = a - 1;
-        while (b >= 0 && sv_list[o + b] > x) { sv_list[o + b + 1] = sv_list[o + b]; --b; }
-        sv_list[o + b + 1] = x;
+    if (n == 0 || o + n > cap) return;
+    const int32_t r0 = vtx_off[v], r1 = vtx_off[v + 1];
+    int32_t m = 0;
+    // the row's slots kSvBatch at a time, each stage's loads issued together (slot -> its two edges
+    // and the twin test -> flags -> list indices), then inserted into the ascending row
+    constexpr int kSvBatch = 8;
+    for (int32_t q0 = r0; q0 < r1 && m < n; q0 += kSvBatch) {
+        int32_t ea[kSvBatch], eb[kSvBatch];
+#pragma unroll
+        for (int u = 0; u < kSvBatch; ++u) {
+            ea[u] = eb[u] = -1;
+            if (q0 + u < r1) {
+                const int32_t h = vtx_slot[q0 + u], hp = tp.prev(h);
+                ea[u] = face_edge[h];
+                eb[u] = face_twin[hp] < 0 ? face_edge[hp] : -1;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kSvBatch; ++u) {  // flag and offset loaded side by side
+            const int32_t fa = ea[u] >= 0 ? flag[ea[u]] : 0, oa = ea[u] >= 0 ? off[ea[u]] : 0;
+            const int32_t fb = eb[u] >= 0 ? flag[eb[u]] : 0, ob = eb[u] >= 0 ? off[eb[u]] : 0;
+            ea[u] = fa ? oa : -1;
+            eb[u] = fb ? ob : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 2 * kSvBatch; ++u) {
+            const int32_t x = u < kSvBatch ? ea[u] : eb[u - kSvBatch];
+            if (x < 0 || m >= n) continue;
+            int32_t b = m - 1;  // insertion into the ascending row
+            while (b >= 0 && sv_list[o + b] > x) { sv_list[o + b + 1] = sv_list[o + b]; --b; }
+            sv_list[o + b + 1] = x;
+            ++m;
+        }
     }
 }
 
@@ -534,7 +575,6 @@ void build0_zero_segments(Build0 &b, ZeroSegs &z) {
     z.add(b.edge_cidx, E, -1);
     z.add(b.sp_flag, E);
     z.add(b.sv_cnt, b.V);
-    z.add(b.sv_cur, b.V);
     z.add(b.scratch, (int64_t)(build0_scratch_bytes(b.V, b.S) / 4));
     b.zeroed = true;
 }
@@ -607,14 +647,13 @@ static void fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
     }
     if (b.V > 0 && !b.zeroed) {
         cudaMemsetAsync(b.sv_cnt, 0, sizeof(int32_t) * b.V, s);
-        cudaMemsetAsync(b.sv_cur, 0, sizeof(int32_t) * b.V, s);
     }
     if (b.zeroed && b.no_special) return;  // closed and crease-free: no special lists, no boundary words
     const int64_t nf = std::max<int64_t>(std::max<int64_t>(E, 32 * (int64_t)b.K_in), nw);
     launch(L, "b0_flags", k_b0_flags<ORDER>, dim3(grid_for(nf)), dim3(kThreads), 0, s, b.crease_in, b.sigma_in, b.K_in, b.face_vtx, b.vtx_off, b.vtx_slot,
                                                  b.face_edge, b.edge_hh, tp, b.V, E, b.bnd_word, nw, b.edge_sigma,
                                                  b.edge_cidx, b.sp_flag, b.bnd_wcnt, b.flags, b.crease_lenient,
-                                                 b.zeroed ? nullptr : b.scalars + 0);
+                                                 b.zeroed ? nullptr : b.scalars + 0, b.sv_cnt);
     // the special-list chain (special edges, special-vertex CSR) is only read by the crease rules of
     // the level kernels: with a side stream it runs as a parallel branch beside the boundary-word
     // prefix scan and the level-0 face kernel, and stays open (L.build_open) until the level-0
@@ -628,17 +667,18 @@ static void fill(Build0 &b, bool check_fans, cudaStream_t s, Launches &L) {
         sc = L.side;
     }
     scan_exclusive(b.bnd_wcnt, b.bnd_wpre, nw, nullptr, region(b, 3), s, L, b.zeroed);
-    scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, region(b, 4), sc, L, b.zeroed);
-    if (E > 0) {
-        launch(L, "b0_special", k_b0_special<ORDER>, dim3(grid_for(E)), dim3(kThreads), 0, sc, b.edge_hh, b.face_vtx, b.edge_sigma, b.sp_flag, b.sp_off, tp, E,
-                                                      b.sp, b.sv_cnt, b.spw, b.spwpre);
+    if (b.zeroed) {
+        scan_exclusive2(b.sp_flag, b.sp_off, E, b.scalars + 2, region(b, 4), b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V,
+                        region(b, 5), sc, L, true);
+    } else {  // create: one scratch region, reused by scans in sequence
+        scan_exclusive(b.sp_flag, b.sp_off, E, b.scalars + 2, region(b, 4), sc, L, false);
+        scan_exclusive(b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V, region(b, 5), sc, L, false);
     }
-    scan_exclusive(b.sv_cnt, b.sv_off, b.V, b.sv_off + b.V, region(b, 5), sc, L, b.zeroed);
-    if (E > 0) {
-        launch(L, "b0_sv_list", k_b0_svlist, dim3(grid_for(E)), dim3(kThreads), 0, sc, b.sp, b.scalars + 2, E, b.sv_off, b.sv_cur, b.sv_list);
-    }
-    if (b.V > 0) {
-        launch(L, "b0_sv_sort", k_b0_svsort, dim3(grid_for(b.V)), dim3(kThreads), 0, sc, b.V, b.sv_off, b.sv_list, b.sv_vtx, b.scalars);
+    const int64_t nt = (int64_t)((E + 31) & ~31) + b.V;
+    if (nt > 0) {
+        launch(L, "b0_special", k_b0_special_fill<ORDER>, dim3(grid_for(nt)), dim3(kThreads), 0, sc, b.edge_hh, b.face_vtx,
+               b.edge_sigma, b.sp_flag, b.sp_off, tp, E, b.sp, b.spw, b.spwpre, b.V, b.vtx_off, b.vtx_slot, b.face_edge,
+               b.face_twin, b.sv_off, b.sv_list, b.sv_vtx, b.scalars, 2 * b.S);
     }
     if (fork) {
         cudaEventRecord(L.ev_build, L.side);

@@ -105,6 +105,11 @@ inline unsigned grid_for(int64_t n, int threads = kThreads) {
 size_t scan_scratch_bytes(int64_t n);
 void scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *total, void *scratch,
                     cudaStream_t s, Launches &L, bool prezeroed = false);
+// two independent exclusive scans in one launch (the level-0 build's special-edge flags and
+// special-vertex counts)
+void scan_exclusive2(const int32_t *ina, int32_t *outa, int64_t na, int32_t *tota, void *scra,
+                     const int32_t *inb, int32_t *outb, int64_t nb, int32_t *totb, void *scrb, cudaStream_t s,
+                     Launches &L, bool prezeroed);
 // initialise up to kZeroSegs int32 arrays in one launch (the level-0 build's ~11 plus up to 3 per
 // refined level: boundary words, special words, Loop scan status)
 constexpr int kZeroSegs = 64;
@@ -145,7 +150,7 @@ struct Build0 {
     int32_t *sp_flag, *sp_off;    // [E]
     SpEdge *sp;                   // [cap] special edges
     int32_t *sv_vtx;              // [cap] special vertices
-    int32_t *sv_cnt, *sv_off, *sv_cur, *sv_list;  // special-vertex CSR (level 0)
+    int32_t *sv_cnt, *sv_off, *sv_list;  // special-vertex CSR (level 0)
     uint32_t *spw;                // [ceil(E/32)] special-edge bitmask (level 0)
     int32_t *spwpre;              // [ceil(E/32)] its per-word prefix (= sp_off at the word start)
     int32_t *flags;               // device status flags

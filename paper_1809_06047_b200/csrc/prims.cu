@@ -28,6 +28,23 @@ void scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *total, 
            (unsigned long long *)scratch, total);
 }
 
+void scan_exclusive2(const int32_t *ina, int32_t *outa, int64_t na, int32_t *tota, void *scra,
+                     const int32_t *inb, int32_t *outb, int64_t nb, int32_t *totb, void *scrb, cudaStream_t s,
+                     Launches &L, bool prezeroed) {
+    if (na <= 0 || nb <= 0) {  // (degenerate inputs: the plain scans)
+        scan_exclusive(ina, outa, na, tota, scra, s, L, prezeroed);
+        scan_exclusive(inb, outb, nb, totb, scrb, s, L, prezeroed);
+        return;
+    }
+    if (!prezeroed) {
+        cudaMemsetAsync(scra, 0, scan_scratch_bytes(na), s);
+        cudaMemsetAsync(scrb, 0, scan_scratch_bytes(nb), s);
+    }
+    const int64_t ta = ceil_div(na, kScanTile), tb = ceil_div(nb, kScanTile);
+    launch(L, "scan2", k_scan2<ArraySrc>, dim3((unsigned)(ta + tb)), dim3(kScanThreads), 0, s, ArraySrc{ina}, outa, na,
+           (unsigned long long *)scra, tota, ArraySrc{inb}, outb, nb, (unsigned long long *)scrb, totb, (int32_t)ta);
+}
+
 // ------------------------------------------------------------------------------------------
 // one launch that initialises many small arrays (replaces a chain of memset graph nodes)
 // ------------------------------------------------------------------------------------------

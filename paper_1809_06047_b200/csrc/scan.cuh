@@ -30,9 +30,8 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 
 // Src: int32_t operator()(int64_t i) -- the value of element i (i < n)
 template <class Src>
-__global__ void __launch_bounds__(kScanThreads) k_scan(Src in, int32_t *__restrict__ out, int64_t n,
-                                                     unsigned long long *status, int32_t *total) {
-    ALSUB_GRID_WAIT();
+__device__ __forceinline__ void scan_tile(Src in, int32_t *__restrict__ out, int64_t n, unsigned long long *status,
+                                          int32_t *total) {
     __shared__ int s_tile;
     __shared__ int s_data[kScanTile + kScanTile / 32];
     __shared__ int s_warp[kScanThreads / 32];
@@ -118,6 +117,25 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Src in, int32_t *__restri
         if (g < n) out[g] = s_data[i + (i >> 5)];
     }
     if (total && tid == 0 && base + kScanTile >= n) *total = (int)(s_prefix + block_total);
+}
+
+template <class Src>
+__global__ void __launch_bounds__(kScanThreads) k_scan(Src in, int32_t *__restrict__ out, int64_t n,
+                                                     unsigned long long *status, int32_t *total) {
+    ALSUB_GRID_WAIT();
+    scan_tile(in, out, n, status, total);
+}
+
+// two independent scans in one launch: blocks [0, tilesA) scan A, the rest B (each array keeps
+// its own status words and tile counter, so the look-back order stays per array)
+template <class Src>
+__global__ void __launch_bounds__(kScanThreads) k_scan2(Src ina, int32_t *__restrict__ outa, int64_t na,
+                                                      unsigned long long *sta, int32_t *tota, Src inb,
+                                                      int32_t *__restrict__ outb, int64_t nb,
+                                                      unsigned long long *stb, int32_t *totb, int32_t tilesa) {
+    ALSUB_GRID_WAIT();
+    if ((int32_t)blockIdx.x < tilesa) scan_tile(ina, outa, na, sta, tota);
+    else scan_tile(inb, outb, nb, stb, totb);
 }
 
 struct ArraySrc {

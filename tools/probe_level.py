@@ -21,7 +21,7 @@ for _ in range(3):
 names = {"cc": ("cc_face", "cc_edge", "cc_vertex", "crease"), "sqrt3": ("s3_face", "s3_vertex"),
          "loop": ("loop_vertex", "scan", "loop_edge", "loop_face")}[scheme] if lvl >= 0 else (
     "zero", "b0_prep", "scan", "b0_scatter", "b0_edge_count", "b0_edge_fill", "b0_flags", "b0_special",
-    "b0_sv_list", "b0_sv_sort")  # level -1 = the level-0 build (first launch of each name)
+    "scan2")  # level -1 = the level-0 build (first launch of each name)
 for name in names:
     m.probe(lvl, name, 20)
     m.refine(scheme, L)

@@ -18,7 +18,7 @@ L = int(sys.argv[3]) if len(sys.argv) > 3 else 6
 maxl = int(sys.argv[4]) if len(sys.argv) > 4 else L - 1
 mesh = {"armor9k": mg.armor9k, "torus100k": mg.torus100k, "ico": mg.icosahedron}[name]()
 build = ("zero", "b0_prep", "scan", "b0_scatter", "b0_edge_count", "b0_edge_fill", "b0_flags", "b0_special",
-         "b0_sv_list", "b0_sv_sort")
+         "scan2")
 level_k = {"cc": ("cc_face", "cc_edge", "cc_vertex", "crease"), "sqrt3": ("s3_face", "s3_vertex"),
            "loop": ("loop_vertex", "scan", "loop_edge", "loop_face", "crease")}[scheme]
 flush = torch.empty(64 * 1024 * 1024, device="cuda")
