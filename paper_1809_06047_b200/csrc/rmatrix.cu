@@ -251,7 +251,7 @@ ALSUB_D unsigned long long rb_row_sum(int32_t r, const float (&v)[3]) {
 }
 // FULL: both rows of every lane exist (all but a chunk's last row group): no per-row predicates
 template <bool FULL>
-ALSUB_D void rb_fold(SummaryRec &r, int32_t ra, int32_t rb, const float (&a)[3], const float (&b)[3]) {
+ALSUB_D void rb_fold(SummaryRec &acc, int f, int32_t ra, int32_t rb, const float (&a)[3], const float (&b)[3]) {
     int32_t lo[3], hi[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -277,32 +277,29 @@ ALSUB_D void rb_fold(SummaryRec &r, int32_t ra, int32_t rb, const float (&a)[3],
         l[c] = __reduce_min_sync(m, lo[c]);
         h[c] = __reduce_max_sync(m, hi[c]);
     }
-    if ((threadIdx.x & 31) == 0) {
+    // frame f's running record lives in lane f's registers (flushed once per warp at the end of
+    // the kernel) instead of eight shared-memory atomics per frame and row group
+    if ((threadIdx.x & 31) == f) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            atomicMin(&r.lo[c], l[c]);
-            atomicMax(&r.hi[c], h[c]);
+            acc.lo[c] = min(acc.lo[c], l[c]);
+            acc.hi[c] = max(acc.hi[c], h[c]);
         }
-        // the 64-bit add as two native 32-bit shared atomics (a 64-bit one is a CAS loop): the low
-        // word's returned old value gives this add's exact carry into the high word
-        const unsigned long long x = (unsigned long long)s0 + ((unsigned long long)s1 << 16) + ((unsigned long long)s2 << 32);
-        uint32_t *w = reinterpret_cast<uint32_t *>(&r.sum);
-        const uint32_t xl = (uint32_t)x, old = atomicAdd(w, xl);
-        atomicAdd(w + 1, (uint32_t)(x >> 32) + (old + xl < old ? 1u : 0u));
+        acc.sum += (unsigned long long)s0 + ((unsigned long long)s1 << 16) + ((unsigned long long)s2 << 32);
     }
 }
 
 ALSUB_D void rb_store(float *so, const int32_t (&rid)[6], float *out, int64_t VL, int f0, int nb, int lane,
-                      const float (&a)[4][3], const float (&b)[4][3], SummaryRec *srec, int32_t rowa, int32_t rowb) {
-    if (srec) {
+                      const float (&a)[4][3], const float (&b)[4][3], SummaryRec *acc, int32_t rowa, int32_t rowb) {
+    if (acc) {
         if (__all_sync(0xffffffffu, rowb >= 0)) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (f0 + u < nb) rb_fold<true>(srec[f0 + u], rowa, rowb, a[u], b[u]);
+                if (f0 + u < nb) rb_fold<true>(*acc, f0 + u, rowa, rowb, a[u], b[u]);
         } else {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (f0 + u < nb) rb_fold<false>(srec[f0 + u], rowa, rowb, a[u], b[u]);
+                if (f0 + u < nb) rb_fold<false>(*acc, f0 + u, rowa, rowb, a[u], b[u]);
         }
     }
 #pragma unroll
@@ -349,7 +346,13 @@ __global__ void __launch_bounds__(32 * kRbWarps) k_rb_eval(int32_t C, int32_t *_
     __shared__ int32_t s_c;
     // per-frame summary records of this CTA's rows (rec != nullptr), flushed to rec at the end
     __shared__ SummaryRec s_rec[kRmLanes];
-    SummaryRec *srec = rec ? s_rec : nullptr;
+    SummaryRec racc;  // lane f: the running record of frame f over this warp's rows
+    for (int c = 0; c < 3; ++c) {
+        racc.lo[c] = INT32_MAX;
+        racc.hi[c] = INT32_MIN;
+    }
+    racc.sum = 0ull;
+    SummaryRec *srec = rec ? &racc : nullptr;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (rec && threadIdx.x < kRmLanes) {
         SummaryRec r;
@@ -441,7 +444,16 @@ __global__ void __launch_bounds__(32 * kRbWarps) k_rb_eval(int32_t C, int32_t *_
         }
         __syncthreads();  // the positions and s_c are reused by the next chunk
     }
-    if (rec && threadIdx.x < nb) {  // the loop ended with a barrier: s_rec is complete
+    if (rec && lane < nb) {  // the warps' records into the CTA's (the loop ended with a barrier)
+        SummaryRec &r = s_rec[lane];
+        for (int c = 0; c < 3; ++c) {
+            atomicMin(&r.lo[c], racc.lo[c]);
+            atomicMax(&r.hi[c], racc.hi[c]);
+        }
+        atomicAdd(&r.sum, racc.sum);
+    }
+    if (rec) __syncthreads();
+    if (rec && threadIdx.x < nb) {
         const SummaryRec &r = s_rec[threadIdx.x];
         SummaryRec &g = rec[threadIdx.x];
         for (int c = 0; c < 3; ++c) {
