@@ -297,10 +297,29 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
                 return make_int2(min(x, y), max(x, y));
             };
             if (c.edge_hh) {
-                c.edge_hh[base + 0] = pair(a0, a1);
-                c.edge_hh[base + 1] = pair(b0, b1);
-                c.edge_hh[base + 2] = pair(4 * h + 1, 4 * hn[k] + 2);  // (fp of face(h), ep); h < tw
-                if (tw >= 0) c.edge_hh[base + 3] = pair(4 * tw + 1, 4 * tp.next(tw) + 2);
+                const int2 q0 = pair(a0, a1), q1 = pair(b0, b1);
+                const int2 q2 = pair(4 * h + 1, 4 * hn[k] + 2);  // (fp of face(h), ep); h < tw
+                // 16-B stores where the block's start parity allows (the pairs are 8 B each): an
+                // even base takes (0,1) and (2,3) as int4, an odd one (1,2) -- half the store
+                // instructions, each sector written in two halves instead of four quarters
+                int4 *d4 = reinterpret_cast<int4 *>(c.edge_hh);
+                if (tw >= 0) {
+                    const int2 q3 = pair(4 * tw + 1, 4 * tp.next(tw) + 2);
+                    if ((base & 1) == 0) {
+                        d4[base >> 1] = make_int4(q0.x, q0.y, q1.x, q1.y);
+                        d4[(base >> 1) + 1] = make_int4(q2.x, q2.y, q3.x, q3.y);
+                    } else {
+                        c.edge_hh[base] = q0;
+                        d4[(base + 1) >> 1] = make_int4(q1.x, q1.y, q2.x, q2.y);
+                        c.edge_hh[base + 3] = q3;
+                    }
+                } else if ((base & 1) == 0) {
+                    d4[base >> 1] = make_int4(q0.x, q0.y, q1.x, q1.y);
+                    c.edge_hh[base + 2] = q2;
+                } else {
+                    c.edge_hh[base] = q0;
+                    d4[(base + 1) >> 1] = make_int4(q1.x, q1.y, q2.x, q2.y);
+                }
             }
             const int32_t nch = tw < 0 ? 3 : 4;
             if constexpr (BND) {
