@@ -932,21 +932,27 @@ __global__ void __launch_bounds__(kThreads, ORDER == 4 && !CR ? 8 : 0) k_cc_vert
     // segment's tasks, so a block works on one spatial band of the mesh.
     __shared__ int32_t s_lo[kMaxSeg], s_pre[kMaxSeg + 1];
     const int64_t nblk = gridDim.x, b = blockIdx.x;
-    if (threadIdx.x < g.nseg) {
-        const int64_t tasks = (g.len[threadIdx.x] + kVtxTask - 1) / kVtxTask;
-        const int32_t lo = (int32_t)(b * tasks / nblk), hi = (int32_t)((b + 1) * tasks / nblk);
-        s_lo[threadIdx.x] = lo;
-        s_pre[threadIdx.x] = hi - lo;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int32_t acc = 0;
-        for (int s = 0; s < g.nseg; ++s) {
-            const int32_t c = s_pre[s];
-            s_pre[s] = acc;
-            acc += c;
+    // warp 0: this block's task range of every segment (nseg = 1 + 2 l <= 31 for l < 16 levels)
+    // and their exclusive prefix by a shuffle scan -- one barrier; most blocks of a large level
+    // have only a few tasks, so the prologue is a visible share of the kernel
+    if (threadIdx.x < 32) {
+        int32_t lo = 0, cnt = 0;
+        if ((int)threadIdx.x < g.nseg) {
+            const int64_t tasks = (g.len[threadIdx.x] + kVtxTask - 1) / kVtxTask;
+            lo = (int32_t)(b * tasks / nblk);
+            cnt = (int32_t)((b + 1) * tasks / nblk) - lo;
         }
-        s_pre[g.nseg] = acc;
+        int32_t inc = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if ((int)threadIdx.x >= d) inc += o;
+        }
+        if ((int)threadIdx.x < g.nseg) {
+            s_lo[threadIdx.x] = lo;
+            s_pre[threadIdx.x] = inc - cnt;
+        }
+        if ((int)threadIdx.x == g.nseg - 1) s_pre[g.nseg] = inc;
     }
     __syncthreads();
     const VtxCtx<ORDER> x{p.face_vtx, Topo<ORDER>{p.face_off, p.slot_face}, p.V};
