@@ -472,21 +472,26 @@ __global__ void __launch_bounds__(kThreads) k_s3_vertex(LevelDev p, Frames fr, V
     ALSUB_GRID_WAIT();
     __shared__ int32_t s_lo[kMaxSeg], s_pre[kMaxSeg + 1];
     const int64_t nblk = gridDim.x, b = blockIdx.x;
-    if (threadIdx.x < g.nseg) {
-        const int64_t tasks = (g.len[threadIdx.x] + 31) >> 5;
-        const int32_t lo = (int32_t)(b * tasks / nblk), hi = (int32_t)((b + 1) * tasks / nblk);
-        s_lo[threadIdx.x] = lo;
-        s_pre[threadIdx.x] = hi - lo;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int32_t acc = 0;
-        for (int s = 0; s < g.nseg; ++s) {
-            const int32_t c = s_pre[s];
-            s_pre[s] = acc;
-            acc += c;
+    // warp 0: this block's task range of every segment (nseg = 1 + l <= 16) and their exclusive
+    // prefix by a shuffle scan (one barrier)
+    if (threadIdx.x < 32) {
+        int32_t lo = 0, cnt = 0;
+        if ((int)threadIdx.x < g.nseg) {
+            const int64_t tasks = (g.len[threadIdx.x] + 31) >> 5;
+            lo = (int32_t)(b * tasks / nblk);
+            cnt = (int32_t)((b + 1) * tasks / nblk) - lo;
         }
-        s_pre[g.nseg] = acc;
+        int32_t inc = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if ((int)threadIdx.x >= d) inc += o;
+        }
+        if ((int)threadIdx.x < g.nseg) {
+            s_lo[threadIdx.x] = lo;
+            s_pre[threadIdx.x] = inc - cnt;
+        }
+        if ((int)threadIdx.x == g.nseg - 1) s_pre[g.nseg] = inc;
     }
     __syncthreads();
     const int32_t ntask = s_pre[g.nseg];
