@@ -147,8 +147,11 @@ __global__ void k_edge_fill(const int32_t *__restrict__ face_vtx, const int32_t 
     if (n <= kLongRow) {
         const WarpCand c = warp_cand(face_vtx, vtx_slot, tp, o0, n, lane);
         const bool mine = c.first && (uint32_t)c.x < (uint32_t)j;
+        // the rank of each edge this vertex owns among its distinct smaller neighbours: only the
+        // owning lanes need one (about half the distinct neighbours), so the loop visits those
         int32_t rank = 0;
-        for (int k = 0; k < 2 * n; ++k) {  // candidates live in lanes < 2n (n is warp-uniform)
+        for (unsigned mm = __ballot_sync(0xffffffffu, mine); mm; mm &= mm - 1) {
+            const int k = __ffs(mm) - 1;
             const int32_t xk = __shfl_sync(0xffffffffu, c.x, k);
             const unsigned b = __ballot_sync(0xffffffffu, c.first && (uint32_t)c.x < (uint32_t)xk);
             if (lane == k) rank = __popc(b);
