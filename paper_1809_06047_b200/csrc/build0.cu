@@ -101,7 +101,7 @@ __global__ void k_edge_count(const int32_t *__restrict__ face_vtx, const int32_t
         // sort the row by slot: lane q moves its slot to its rank (slots are distinct)
         const int32_t sq = lane < n ? row[lane] : INT32_MAX;
         int32_t rank = 0;
-        for (int p = 0; p < 16; ++p) rank += __shfl_sync(0xffffffffu, sq, p) < sq;
+        for (int p = 0; p < n; ++p) rank += __shfl_sync(0xffffffffu, sq, p) < sq;  // (n warp-uniform)
         __syncwarp();
         if (lane < n) row[rank] = sq;
         __syncwarp();

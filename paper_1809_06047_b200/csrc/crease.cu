@@ -71,8 +71,7 @@ __global__ void __launch_bounds__(kThreads) k_crease(CreaseArgs A) {
         const int32_t tot = 2 * p.nsp;  // = parent sv_off[nsv]
         c.sv_vtx[iep] = ep;
         c.sv_off[iep] = tot + 2 * j;
-        c.sv_list[tot + 2 * j] = 2 * j;
-        c.sv_list[tot + 2 * j + 1] = 2 * j + 1;
+        *reinterpret_cast<int2 *>(c.sv_list + tot + 2 * j) = make_int2(2 * j, 2 * j + 1);  // (tot even: 8-B aligned)
         if (j == p.nsp - 1) c.sv_off[iep + 1] = tot + 2 * p.nsp;
         return;
     }
