@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kThreads) k_cc_edge(LevelDev p, ChildDev c, Fr
 // is a block-shared sum over the group when all four threads are in one block (the vertex kernel
 // does the few groups that straddle a block boundary, and boundary e'').
 template <int NBC>
-__global__ void __launch_bounds__(kThreads, NBC ? 6 : 0) k_cc_edge_gp(LevelDev p, LevelDev gp, ChildDev c, Frames fr,
+__global__ void __launch_bounds__(kThreads, NBC ? 5 : 0) k_cc_edge_gp(LevelDev p, LevelDev gp, ChildDev c, Frames fr,
                                                        int32_t epo, const int2 *ehh2) {
     ALSUB_GRID_WAIT();
     // the block's children are the contiguous id range [base(e_first), base(e_last) + nch): staged
