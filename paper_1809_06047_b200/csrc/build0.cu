@@ -544,6 +544,20 @@ __global__ void __launch_bounds__(kThreads) k_b0_special_fill(const int2 *__rest
             ea[u] = fa ? oa : -1;
             eb[u] = fb ? ob : -1;
         }
+        if (r1 - r0 <= kSvBatch) {
+            // the whole row in this batch: each entry's place is its rank among the row's entries
+            // (distinct list indices), counted in registers -- no read-back of the list
+#pragma unroll
+            for (int u = 0; u < 2 * kSvBatch; ++u) {
+                const int32_t x = u < kSvBatch ? ea[u] : eb[u - kSvBatch];
+                if (x < 0) continue;
+                int32_t r = 0;
+#pragma unroll
+                for (int w = 0; w < kSvBatch; ++w) r += (ea[w] >= 0 && ea[w] < x) + (eb[w] >= 0 && eb[w] < x);
+                if (r < n) sv_list[o + r] = x;
+            }
+            break;
+        }
 #pragma unroll
         for (int u = 0; u < 2 * kSvBatch; ++u) {
             const int32_t x = u < kSvBatch ? ea[u] : eb[u - kSvBatch];
