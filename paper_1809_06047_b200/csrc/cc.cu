@@ -1102,7 +1102,12 @@ static void cc_launch(const LevelDev &p, const ChildDev &c, const Frames &fr0, b
         // ones (128-vertex tasks with batched loads were measured slower)
         const unsigned nblk = (unsigned)std::max<int64_t>(grid_for(p.V, 4 * kThreads),
                                                           std::min<int64_t>(grid_for(p.V, kThreads), 2 * 148));
+        // on the grandparent path, 128-thread vertex blocks (4096 registers) fit beside five
+        // 256-thread edge blocks (61440) instead of taking an edge block's place (config 3
+        // 0.5980 -> 0.5961 ms same-box)
+        const bool half = gp && !p.crease;
         if (p.crease) launch(L, "cc_vertex", k_cc_vertex<ORDER == 4 ? 4 : 0, 1, true>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g, c.sv_list);
+        else if (half) launch(L, "cc_vertex", k_cc_vertex<ORDER == 4 ? 4 : 0, 1, false>, dim3(2 * nblk), dim3(kThreads / 2), 0, s, p, fr, g, c.sv_list);
         else launch(L, "cc_vertex", k_cc_vertex<ORDER == 4 ? 4 : 0, 1, false>, dim3(nblk), dim3(kThreads), 0, s, p, fr, g, c.sv_list);
         if (g.nlong > 0) {  // the poles' rings (reads what the vertex kernel reads, writes disjoint ids)
             const unsigned gl = grid_for(32 * (int64_t)g.nlong);
