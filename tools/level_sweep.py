@@ -11,7 +11,8 @@ from paper_1809_06047_b200 import Mesh  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "armor9k"
 mesh = {"armor9k": mg.armor9k, "torus100k": mg.torus100k, "ico": mg.icosahedron,
-        "armor9k_shuf": lambda: mg.shuffled(mg.armor9k()), "torus100k_shuf": lambda: mg.shuffled(mg.torus100k())}[name]()
+        "armor9k_shuf": lambda: mg.shuffled(mg.armor9k()), "torus100k_shuf": lambda: mg.shuffled(mg.torus100k()),
+        "tet_creased": lambda: mg.tetrahedron(creased=True), "cube": mg.cube}[name]()
 scheme = sys.argv[2] if len(sys.argv) > 2 else "cc"
 L = int(sys.argv[3]) if len(sys.argv) > 3 else 6
 flush = torch.empty(64 * 1024 * 1024, device="cuda")
