@@ -182,6 +182,58 @@ __global__ void __launch_bounds__(kThreads) k_cc_face_gen(LevelDev p, ChildDev c
     const int32_t V = p.V, F = p.F;
     const float inv = 1.0f / (float)n;
     const int nb = NBC ? NBC : fr.nb;
+    if (n == 3 || n == 4) {
+        // triangles and quads (almost every face): the face's rows loaded together, then the
+        // position gathers together (the general loop below is a serial chain per corner)
+        int32_t v[4], e[4], tw[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            v[t] = t < n ? __ldg(p.face_vtx + o + t) : 0;
+            e[t] = (topo && t < n) ? __ldg(p.face_edge + o + t) : 0;
+            tw[t] = (ADJ && topo && t < n) ? __ldg(p.face_twin + o + t) : -1;
+        }
+        for (int f = 0; f < nb; ++f) {
+            const PR P = fr.rd(f);
+            P3 q[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) q[t] = t < n ? ld3(P, v[t]) : p3zero();
+            P3 s = p3zero();
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (t < n) s = s + q[t];
+            st3(fr.wr(f), V + r, inv * s);
+        }
+        if (!topo) return;
+        int32_t base[4];
+        if constexpr (ADJ) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) base[t] = t < n ? cc_base<BND>(p.bnd_word, p.bnd_wpre, e[t]) : 0;
+        }
+        // (neighbours by selects on n, so every register index is a compile-time constant)
+        const bool quad = n == 4;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (t >= n) break;
+            const bool wrap = t + 1 == n;
+            const int tn = wrap ? 0 : t + 1, tq = t == 0 ? n - 1 : t - 1;
+            const int32_t h = o + t, hn = o + tn, hp = o + tq;
+            const int32_t vt = v[t], vn = wrap ? v[0] : v[t < 3 ? t + 1 : 0];
+            const int32_t vp = t == 0 ? (quad ? v[3] : v[2]) : v[t > 0 ? t - 1 : 0];
+            const int32_t et = e[t], ep = t == 0 ? (quad ? e[3] : e[2]) : e[t > 0 ? t - 1 : 0];
+            reinterpret_cast<int4 *>(c.face_vtx)[h] = make_int4(vt, V + F + et, V + r, V + F + ep);
+            if constexpr (ADJ) {
+                const int32_t twt = tw[t], twp = t == 0 ? (quad ? tw[3] : tw[2]) : tw[t > 0 ? t - 1 : 0];
+                const int32_t bt = base[t], bp = t == 0 ? (quad ? base[3] : base[2]) : base[t > 0 ? t - 1 : 0];
+                reinterpret_cast<int4 *>(c.face_edge)[h] =
+                    make_int4(bt + (vt > vn), bt + 2 + (twt >= 0 && twt < h), bp + 2 + (twp >= 0 && twp < hp),
+                              bp + (vt > vp));
+                if (c.face_twin)
+                    reinterpret_cast<int4 *>(c.face_twin)[h] =
+                        make_int4(twt >= 0 ? 4 * tp.next(twt) + 3 : -1, 4 * hn + 2, 4 * hp + 1, twp >= 0 ? 4 * twp : -1);
+            }
+        }
+        return;
+    }
     for (int f = 0; f < nb; ++f) {
         const PR P = fr.rd(f);
         P3 s = p3zero();
