@@ -520,8 +520,8 @@ __global__ void __launch_bounds__(kThreads) k_b0_special_fill(const int2 *__rest
     if (v == 0) scalars[3] = V;
     sv_vtx[v] = v;
     const int32_t o = sv_off[v], n = sv_off[v + 1] - o;
+    const int32_t r0 = vtx_off[v], r1 = vtx_off[v + 1];  // (beside the list bounds)
     if (n == 0 || o + n > cap) return;
-    const int32_t r0 = vtx_off[v], r1 = vtx_off[v + 1];
     int32_t m = 0;
     // the row's slots kSvBatch at a time, each stage's loads issued together (slot -> its two edges
     // and the twin test -> flags -> list indices), then inserted into the ascending row
